@@ -1,0 +1,116 @@
+/*
+ * oaa.h -- C ABI of liboaa.so, the B200 (sm_100a) overlap-and-add convolution layer of
+ * Highlander & Rodriguez, "Very Efficient Training of Convolutional Neural Networks
+ * using Fast Fourier Transform and Overlap-and-Add" (arXiv 1601.06815).
+ *
+ * The operations (citations are /root/reference/PAPER.md lines; SPEC.md lines are the
+ * spec written from the paper):
+ *
+ *   oaa_conv_fwd        the convolutional layer's forward propagation: K output maps,
+ *                       each the sum over the C input channels of the channel convolved
+ *                       with the matching kernel channel (§1 "The total
+ *                       number of convolutions in a CNN convolutional layer is KC"),
+ *                       computed by overlap-and-add (§2: the N×N input is
+ *                       broken into ceil(N/n)² n×n blocks, each block convolution is a
+ *                       Hadamard product in the frequency domain on a (2n−1)-point grid
+ *                       (PAPER.md:27, :85), and the results are "overlapped by n−1 ...
+ *                       and added together").  True convolution (kernel flipped;
+ *                       SPEC.md:267).
+ *   oaa_conv_bwd_data   "one convolution to propagate the error through the layer"
+ *                       (§3.2): dx = Σ_k FullConv(dy_k, flip180 w_kc),
+ *                       cropped at offset n−1−o (the adjoint of the forward).
+ *   oaa_conv_bwd_filter "another to calculate the change in weight":
+ *                       dw[k,c,u,v] = Σ_b Σ_a x[b,c,a]·G[b,k,a+(u,v)], G = dy placed at
+ *                       offset o in the (N+n−1)² Full frame (the adjoint w.r.t. w).
+ *
+ * Shapes and layouts (all dense, row-major, fp32, DEVICE memory):
+ *   x, dx : [B][C][N][N]      w, dw : [K][C][n][n]      y, dy : [B][K][M][M]
+ *   crop  : OAA_CROP_FULL  M = N+n−1, o = 0
+ *           OAA_CROP_VALID M = N−n+1, o = n−1   (requires n ≤ N)
+ *           OAA_CROP_SAME  M = N,     o = floor((n−1)/2)  (= scipy 'same')
+ *   (Valid is the layer default.)  Stride 1, no dilation,
+ *   no bias (readings R5, R6, R12).
+ *
+ * Supported sizes (v1): 1 ≤ n ≤ 8; max(ceil(R/n)·n, Ro) ≤ 256 where (R, Ro) is
+ * (N, M) for fwd and bwd_filter and (M, N) for bwd_data (i.e. N up to ≈ 250);
+ * B, C, K ≥ 1 (B = 0 is a no-op; bwd_filter then zero-fills dw).  Anything else returns
+ * OAA_ERR_UNSUPPORTED (size limits) or OAA_ERR_INVALID_VALUE (nonsense arguments)
+ * and writes nothing.
+ *
+ * Ownership / threading: the caller owns every buffer including the workspace (size
+ * from oaa_conv_workspace_bytes; ≥ 256-byte aligned).  The library never allocates,
+ * frees or synchronises; every call enqueues kernels on `stream` (a cudaStream_t,
+ * NULL = legacy default stream) and returns immediately -- results are valid in stream
+ * order.  Outputs are fully overwritten, never accumulated; dw is the sum over this
+ * call's B images only (the cross-GPU sum is the caller's all-reduce).  Concurrent
+ * calls must use distinct workspaces.  Results are bitwise deterministic for a given
+ * device and arguments.
+ *
+ * Errors: arguments are validated on the host before any launch; on error nothing is
+ * written.  Launch failures are reported as OAA_ERR_CUDA (the call stays asynchronous).
+ */
+#ifndef OAA_H_
+#define OAA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { OAA_CROP_FULL = 0, OAA_CROP_VALID = 1, OAA_CROP_SAME = 2 } oaa_crop_t;
+
+typedef enum {
+  OAA_OK = 0,
+  OAA_ERR_INVALID_VALUE = 1, /* null pointer, negative size, bad crop, Valid with n > N, aliasing */
+  OAA_ERR_UNSUPPORTED = 2,   /* valid arguments outside the v1 size limits */
+  OAA_ERR_WORKSPACE = 3,     /* ws_bytes < oaa_conv_workspace_bytes(...) or ws misaligned */
+  OAA_ERR_CUDA = 4           /* a kernel launch or memset failed (cudaGetLastError) */
+} oaa_status_t;
+
+typedef enum { OAA_OP_FWD = 0, OAA_OP_BWD_DATA = 1, OAA_OP_BWD_FILTER = 2 } oaa_op_t;
+
+/* Output side M for input side N and kernel side n; −1 if invalid. */
+int oaa_conv_out_size(int N, int n, oaa_crop_t crop);
+
+/* Workspace bytes needed by `op` for these arguments (0 is a valid answer only for
+ * B = 0).  Depends only on the arguments.  Returns 0 for invalid arguments. */
+size_t oaa_conv_workspace_bytes(oaa_op_t op, int B, int C, int K, int N, int n, oaa_crop_t crop);
+
+/* y[B][K][M][M] = crop(Σ_c x[b,c] ∗ w[k,c]).  x, w, y: device pointers. */
+oaa_status_t oaa_conv_fwd(const float* x, const float* w, float* y, int B, int C, int K, int N,
+                          int n, oaa_crop_t crop, void* ws, size_t ws_bytes, void* stream);
+
+/* dx[B][C][N][N] from dy[B][K][M][M] and w.  dy, w, dx: device pointers. */
+oaa_status_t oaa_conv_bwd_data(const float* dy, const float* w, float* dx, int B, int C, int K,
+                               int N, int n, oaa_crop_t crop, void* ws, size_t ws_bytes,
+                               void* stream);
+
+/* dw[K][C][n][n] = Σ over this call's batch.  x, dy, dw: device pointers. */
+oaa_status_t oaa_conv_bwd_filter(const float* x, const float* dy, float* dw, int B, int C, int K,
+                                 int N, int n, oaa_crop_t crop, void* ws, size_t ws_bytes,
+                                 void* stream);
+
+/* Static description of a status code. */
+const char* oaa_status_string(oaa_status_t s);
+
+/* Library version string ("oaa-b200 <semver> sm_100a"). */
+const char* oaa_version(void);
+
+/* Number of kernels this process has launched through the library so far (monotone;
+ * used by bench.py to report gpu_launches). */
+uint64_t oaa_launch_count(void);
+
+/* Kernel timing for the roofline report.  When enabled, every call records CUDA events
+ * around its main (dominant) kernel on the call's stream; oaa_profile_collect
+ * synchronises those events, writes the summed milliseconds and launch counts per op
+ * (index = oaa_op_t) into ms[3] / count[3], and clears the record.  Returns the
+ * number of records collected or −1 on a CUDA error. */
+void oaa_profile_enable(int on);
+int oaa_profile_collect(double* ms, int* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OAA_H_ */

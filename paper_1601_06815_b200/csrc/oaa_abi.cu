@@ -1,0 +1,420 @@
+// oaa_abi.cu -- host side of liboaa.so: argument validation, planning, workspace layout
+// and kernel launches behind the C ABI declared in include/oaa.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/oaa.h"
+#define OAA_DEFINE_AUX_KERNELS
+#include "oaa_launch.cuh"
+
+namespace oaa_host {
+std::atomic<uint64_t> g_launches{0};
+}  // namespace oaa_host
+
+namespace {
+using namespace oaa_host;
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+// ------------------------------------------------------------------ profiling
+struct ProfRec {
+  int op;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_event_pool;
+
+cudaEvent_t get_event() {
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct ProfScope {
+  int op;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr, b = nullptr;
+  bool on = false;
+  ProfScope(int op_, cudaStream_t s_) : op(op_), s(s_) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    on = g_prof_on;
+    if (on) {
+      a = get_event();
+      b = get_event();
+    }
+  }
+  void start() { if (on) cudaEventRecord(a, s); }
+  void stop() {
+    if (!on) return;
+    cudaEventRecord(b, s);
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    g_prof.push_back({op, a, b});
+  }
+};
+
+// ---------------------------------------------------------------- geometry
+struct Geo {
+  int n, P, H, M, o;
+};
+
+bool make_geo(int N, int n, oaa_crop_t crop, Geo* g) {
+  if (N < 1 || n < 1) return false;
+  int M = oaa_conv_out_size(N, n, crop);
+  if (M < 1) return false;
+  g->n = n;
+  g->P = 2 * n - 1;
+  g->H = n;
+  g->M = M;
+  g->o = crop == OAA_CROP_FULL ? 0 : crop == OAA_CROP_VALID ? n - 1 : (n - 1) / 2;
+  return true;
+}
+
+// register channel capacity of the engine: CR ∈ {1..4}
+constexpr int kCRMax = 4;
+
+
+int pick_TS(int T, int n) {
+  // stride of the t2 index in the shared Q buffer, chosen so stage-A stores and stage-B
+  // loads are (near) bank-conflict free: TS ≡ 32/n (mod 32).
+  int target = std::max(1, 32 / n) % 32;
+  int TS = T;
+  while ((TS % 32) != target) ++TS;
+  return TS;
+}
+
+bool plan_engine(int R, int Ro, int off, int n, int Cin, int Cout, EnginePlan* e) {
+  e->R = R;
+  e->Ro = Ro;
+  e->off = off;
+  e->T = cdiv(R, n);
+  e->Cin = Cin;
+  e->Cout = Cout;
+  const int laneA = e->T * n;
+  const int need = std::max(laneA, Ro);
+  if (need > oaa::kMaxThreads) return false;
+  e->nthreads = cdiv(need, 32) * 32;
+  e->TS = pick_TS(e->T, n);
+  const int P = 2 * n - 1, H = n;
+  e->smem = sizeof(float) * 2 /*buf*/ * 2 /*re,im*/ * (size_t)H * P * e->TS;
+  if (Cin <= kCRMax) {
+    e->S1 = true;
+    e->CR = Cin;
+  } else {
+    e->S1 = false;
+    e->CR = std::min(Cout, kCRMax);
+  }
+  return e->smem <= 200 * 1024;
+}
+
+
+bool plan_filter(int B, int C, int K, int M, int n, FilterPlan* f) {
+  const int H = n, P = 2 * n - 1;
+  f->Td = cdiv(M, n);
+  f->KG = std::max(1, oaa::kMaxThreads / H);
+  f->KG = std::min(f->KG, K);
+  f->nkg = cdiv(K, f->KG);
+  f->nthreads = cdiv(f->KG * H, 32) * 32;
+  f->CR = std::min(C, kCRMax);
+  // tiles per Ξ̂ chunk: enough (tile, c, f1) tasks to keep every thread busy once
+  f->TCH = std::max(1, std::min(f->Td, f->nthreads / (f->CR * H)));
+  f->smem = sizeof(float2) * (size_t)f->TCH * f->CR * P * H;
+  const int items = std::max(1, B * f->Td);
+  // one persistent wave: ~148 SMs on B200 (fixed so results do not depend on the device)
+  f->G = std::max(1, std::min(items, 148 / f->nkg));
+  return f->smem <= 200 * 1024;
+}
+
+// ---------------------------------------------------------------- dispatch
+}  // namespace
+namespace oaa_host {
+OAA_DECLARE_N(1)
+OAA_DECLARE_N(2)
+OAA_DECLARE_N(3)
+OAA_DECLARE_N(4)
+OAA_DECLARE_N(5)
+OAA_DECLARE_N(6)
+OAA_DECLARE_N(7)
+OAA_DECLARE_N(8)
+}  // namespace oaa_host
+namespace {
+
+cudaError_t launch_engine(int n, const oaa::EngineParams& p, const EnginePlan& e, cudaStream_t s) {
+  switch (n) {
+    case 1: return launch_engine_n<1>(p, e, s);
+    case 2: return launch_engine_n<2>(p, e, s);
+    case 3: return launch_engine_n<3>(p, e, s);
+    case 4: return launch_engine_n<4>(p, e, s);
+    case 5: return launch_engine_n<5>(p, e, s);
+    case 6: return launch_engine_n<6>(p, e, s);
+    case 7: return launch_engine_n<7>(p, e, s);
+    case 8: return launch_engine_n<8>(p, e, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_filter(int n, const oaa::FilterParams& p, const FilterPlan& f, cudaStream_t s) {
+  switch (n) {
+    case 1: return launch_filter_n<1>(p, f, s);
+    case 2: return launch_filter_n<2>(p, f, s);
+    case 3: return launch_filter_n<3>(p, f, s);
+    case 4: return launch_filter_n<4>(p, f, s);
+    case 5: return launch_filter_n<5>(p, f, s);
+    case 6: return launch_filter_n<6>(p, f, s);
+    case 7: return launch_filter_n<7>(p, f, s);
+    case 8: return launch_filter_n<8>(p, f, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+bool overlaps(const void* a, size_t an, const void* b, size_t bn) {
+  const char* pa = static_cast<const char*>(a);
+  const char* pb = static_cast<const char*>(b);
+  return pa < pb + bn && pb < pa + an;
+}
+
+// Common validation. Returns OAA_OK or an error without touching memory.
+oaa_status_t validate(int B, int C, int K, int N, int n, oaa_crop_t crop, Geo* g) {
+  if (B < 0 || C < 1 || K < 1 || N < 1 || n < 1) return OAA_ERR_INVALID_VALUE;
+  if (crop != OAA_CROP_FULL && crop != OAA_CROP_VALID && crop != OAA_CROP_SAME)
+    return OAA_ERR_INVALID_VALUE;
+  if (!make_geo(N, n, crop, g)) return OAA_ERR_INVALID_VALUE;
+  if (n > 8) return OAA_ERR_UNSUPPORTED;
+  return OAA_OK;
+}
+
+// workspace layouts ------------------------------------------------------------
+struct EngineWs {
+  size_t spec_off, flags_off, counter_off, total;
+};
+EngineWs engine_ws(int B, int C, int K, int Tr, const Geo& g) {
+  EngineWs w{};
+  w.spec_off = 0;
+  w.flags_off = align_up(sizeof(float2) * (size_t)K * C * g.P * g.H);
+  w.counter_off = align_up(w.flags_off + sizeof(int) * (size_t)std::max(1, B * Tr));
+  w.total = align_up(w.counter_off + sizeof(int));
+  return w;
+}
+
+oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out, int B, int C,
+                        int K, int N, int n, oaa_crop_t crop, void* ws, size_t ws_bytes,
+                        void* stream) {
+  Geo g;
+  oaa_status_t st = validate(B, C, K, N, n, crop, &g);
+  if (st != OAA_OK) return st;
+  if (!in || !w || !out) return OAA_ERR_INVALID_VALUE;
+  const int R = is_fwd ? N : g.M, Ro = is_fwd ? g.M : N;
+  const int Cin = is_fwd ? C : K, Cout = is_fwd ? K : C;
+  const int off = is_fwd ? g.o : (n - 1 - g.o);
+  const size_t in_bytes = sizeof(float) * (size_t)B * Cin * R * R;
+  const size_t out_bytes = sizeof(float) * (size_t)B * Cout * Ro * Ro;
+  const size_t w_bytes = sizeof(float) * (size_t)K * C * n * n;
+  if (B > 0 && (overlaps(in, in_bytes, out, out_bytes) || overlaps(w, w_bytes, out, out_bytes)))
+    return OAA_ERR_INVALID_VALUE;
+  EnginePlan e;
+  if (!plan_engine(R, Ro, off, n, Cin, Cout, &e)) return OAA_ERR_UNSUPPORTED;
+  if (B == 0) return OAA_OK;
+  EngineWs L = engine_ws(B, C, K, e.T, g);
+  if (!ws || ws_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0)
+    return OAA_ERR_WORKSPACE;
+  if (overlaps(ws, L.total, out, out_bytes) || overlaps(ws, L.total, in, in_bytes))
+    return OAA_ERR_INVALID_VALUE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* base = static_cast<char*>(ws);
+  float2* spec = reinterpret_cast<float2*>(base + L.spec_off);
+  int* flags = reinterpret_cast<int*>(base + L.flags_off);
+  int* counter = reinterpret_cast<int*>(base + L.counter_off);
+
+  // kernel spectra: loop-major layout [Cloop][Cinner][P][H]
+  const int loop_is_k = (is_fwd == e.S1) ? 1 : 0;  // fwd S1 / bwd_data S2 loop over k
+  {
+    const long total = (long)K * C * g.P * g.H;
+    const int thr = 256;
+    const int blocks = (int)std::min<long>((total + thr - 1) / thr, 4096);
+    oaa::oaa_spectrum_kernel<<<blocks, thr, 0, s>>>(w, spec, K, C, n, is_fwd ? 0 : 1, loop_is_k);
+    g_launches++;
+    if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
+  }
+  if (cudaMemsetAsync(base + L.flags_off, 0, L.total - L.flags_off, s) != cudaSuccess)
+    return OAA_ERR_CUDA;
+  oaa::EngineParams p;
+  p.in = in;
+  p.spec = spec;
+  p.out = out;
+  p.flags = flags;
+  p.counter = counter;
+  p.B = B;
+  p.Cin = Cin;
+  p.Cout = Cout;
+  p.R = R;
+  p.T = e.T;
+  p.Ro = Ro;
+  p.off = off;
+  p.TS = e.TS;
+  p.num_items = B * e.T;
+  ProfScope prof(is_fwd ? OAA_OP_FWD : OAA_OP_BWD_DATA, s);
+  prof.start();
+  cudaError_t err = launch_engine(n, p, e, s);
+  prof.stop();
+  return err == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+int oaa_conv_out_size(int N, int n, oaa_crop_t crop) {
+  if (N < 1 || n < 1) return -1;
+  switch (crop) {
+    case OAA_CROP_FULL: return N + n - 1;
+    case OAA_CROP_VALID: return n <= N ? N - n + 1 : -1;
+    case OAA_CROP_SAME: return N;
+  }
+  return -1;
+}
+
+size_t oaa_conv_workspace_bytes(oaa_op_t op, int B, int C, int K, int N, int n, oaa_crop_t crop) {
+  Geo g;
+  if (validate(B, C, K, N, n, crop, &g) != OAA_OK) return 0;
+  if (B == 0) return 0;
+  if (op == OAA_OP_FWD || op == OAA_OP_BWD_DATA) {
+    const int R = op == OAA_OP_FWD ? N : g.M;
+    return engine_ws(B, C, K, cdiv(R, n), g).total;
+  }
+  if (op == OAA_OP_BWD_FILTER) {
+    FilterPlan f;
+    if (!plan_filter(B, C, K, g.M, n, &f)) return 0;
+    return align_up(sizeof(float2) * (size_t)f.G * K * C * g.P * g.H);
+  }
+  return 0;
+}
+
+oaa_status_t oaa_conv_fwd(const float* x, const float* w, float* y, int B, int C, int K, int N,
+                          int n, oaa_crop_t crop, void* ws, size_t ws_bytes, void* stream) {
+  return run_engine(true, x, w, y, B, C, K, N, n, crop, ws, ws_bytes, stream);
+}
+
+oaa_status_t oaa_conv_bwd_data(const float* dy, const float* w, float* dx, int B, int C, int K,
+                               int N, int n, oaa_crop_t crop, void* ws, size_t ws_bytes,
+                               void* stream) {
+  return run_engine(false, dy, w, dx, B, C, K, N, n, crop, ws, ws_bytes, stream);
+}
+
+oaa_status_t oaa_conv_bwd_filter(const float* x, const float* dy, float* dw, int B, int C, int K,
+                                 int N, int n, oaa_crop_t crop, void* ws, size_t ws_bytes,
+                                 void* stream) {
+  Geo g;
+  oaa_status_t st = validate(B, C, K, N, n, crop, &g);
+  if (st != OAA_OK) return st;
+  if (!x || !dy || !dw) return OAA_ERR_INVALID_VALUE;
+  const size_t x_bytes = sizeof(float) * (size_t)B * C * N * N;
+  const size_t dy_bytes = sizeof(float) * (size_t)B * K * g.M * g.M;
+  const size_t dw_bytes = sizeof(float) * (size_t)K * C * n * n;
+  if (overlaps(dw, dw_bytes, x, x_bytes) || overlaps(dw, dw_bytes, dy, dy_bytes))
+    return OAA_ERR_INVALID_VALUE;
+  if (cdiv(g.M, n) * n > 4096) return OAA_ERR_UNSUPPORTED;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (B == 0) {
+    if (cudaMemsetAsync(dw, 0, dw_bytes, s) != cudaSuccess) return OAA_ERR_CUDA;
+    return OAA_OK;
+  }
+  FilterPlan f;
+  if (!plan_filter(B, C, K, g.M, n, &f)) return OAA_ERR_UNSUPPORTED;
+  const size_t need = align_up(sizeof(float2) * (size_t)f.G * K * C * g.P * g.H);
+  if (!ws || ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0)
+    return OAA_ERR_WORKSPACE;
+  if (overlaps(ws, need, dw, dw_bytes) || overlaps(ws, need, x, x_bytes) ||
+      overlaps(ws, need, dy, dy_bytes))
+    return OAA_ERR_INVALID_VALUE;
+  oaa::FilterParams p;
+  p.x = x;
+  p.dy = dy;
+  p.partial = static_cast<float2*>(ws);
+  p.B = B;
+  p.C = C;
+  p.K = K;
+  p.N = N;
+  p.M = g.M;
+  p.off = g.o;
+  p.Td = f.Td;
+  p.G = f.G;
+  p.KG = f.KG;
+  p.TCH = f.TCH;
+  ProfScope prof(OAA_OP_BWD_FILTER, s);
+  prof.start();
+  cudaError_t err = launch_filter(n, p, f, s);
+  prof.stop();
+  if (err != cudaSuccess) return OAA_ERR_CUDA;
+  const int bins = g.P * g.H;
+  oaa::oaa_filter_finalize_kernel<<<K * C, 128, sizeof(double2) * bins, s>>>(
+      static_cast<const float2*>(ws), dw, f.G, K, C, n);
+  g_launches++;
+  if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
+  return OAA_OK;
+}
+
+const char* oaa_status_string(oaa_status_t s) {
+  switch (s) {
+    case OAA_OK: return "OAA_OK";
+    case OAA_ERR_INVALID_VALUE: return "OAA_ERR_INVALID_VALUE: invalid argument";
+    case OAA_ERR_UNSUPPORTED: return "OAA_ERR_UNSUPPORTED: size outside v1 limits (n<=8, N<=~250)";
+    case OAA_ERR_WORKSPACE: return "OAA_ERR_WORKSPACE: workspace too small or misaligned";
+    case OAA_ERR_CUDA: return "OAA_ERR_CUDA: CUDA launch failure";
+  }
+  return "unknown oaa_status_t";
+}
+
+const char* oaa_version(void) { return "oaa-b200 0.1.0 sm_100a"; }
+
+uint64_t oaa_launch_count(void) { return g_launches.load(); }
+
+void oaa_profile_enable(int on) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof_on = on != 0;
+}
+
+int oaa_profile_collect(double* ms, int* count) {
+  std::vector<ProfRec> recs;
+  {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    recs.swap(g_prof);
+  }
+  for (int i = 0; i < 3; ++i) {
+    if (ms) ms[i] = 0.0;
+    if (count) count[i] = 0;
+  }
+  int bad = 0;
+  for (auto& r : recs) {
+    if (cudaEventSynchronize(r.b) != cudaSuccess) bad = 1;
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) bad = 1;
+    if (r.op >= 0 && r.op < 3) {
+      if (ms) ms[r.op] += t;
+      if (count) count[r.op] += 1;
+    }
+  }
+  {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    for (auto& r : recs) {
+      g_event_pool.push_back(r.a);
+      g_event_pool.push_back(r.b);
+    }
+  }
+  return bad ? -1 : (int)recs.size();
+}
+
+}  // extern "C"

@@ -1,0 +1,5 @@
+// Explicit instantiation of the n = 4 kernels (compiled in parallel by build.py).
+#include "oaa_launch.cuh"
+namespace oaa_host {
+OAA_INSTANTIATE_N(4)
+}  // namespace oaa_host

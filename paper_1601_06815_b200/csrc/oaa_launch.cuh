@@ -1,0 +1,94 @@
+// oaa_launch.cuh -- per-kernel-size launch templates.  Each oaa_inst_n<k>.cu explicitly
+// instantiates them for one kernel size n so the 8 sizes compile in parallel.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+
+#include "oaa_kernels.cuh"
+
+namespace oaa_host {
+
+extern std::atomic<uint64_t> g_launches;
+
+struct EnginePlan {
+  int R, Ro, off, T, Cin, Cout, TS, nthreads, CR;
+  bool S1;
+  size_t smem;
+};
+
+struct FilterPlan {
+  int Td, KG, nkg, G, TCH, CR, nthreads;
+  size_t smem;
+};
+
+template <int NN, int CR, bool S1>
+cudaError_t launch_engine_t(const oaa::EngineParams& p, const EnginePlan& e, cudaStream_t s) {
+  auto k = oaa::oaa_engine_kernel<NN, CR, S1>;
+  cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem);
+  if (err != cudaSuccess) return err;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, e.nthreads, e.smem);
+  per_sm = std::max(1, per_sm);
+  const int grid = std::max(1, std::min(p.num_items, sms * per_sm));
+  k<<<grid, e.nthreads, e.smem, s>>>(p);
+  g_launches++;
+  return cudaGetLastError();
+}
+
+template <int NN>
+cudaError_t launch_engine_n(const oaa::EngineParams& p, const EnginePlan& e, cudaStream_t s) {
+  if (e.S1) {
+    switch (e.CR) {
+      case 1: return launch_engine_t<NN, 1, true>(p, e, s);
+      case 2: return launch_engine_t<NN, 2, true>(p, e, s);
+      case 3: return launch_engine_t<NN, 3, true>(p, e, s);
+      default: return launch_engine_t<NN, 4, true>(p, e, s);
+    }
+  } else {
+    switch (e.CR) {
+      case 1: return launch_engine_t<NN, 1, false>(p, e, s);
+      case 2: return launch_engine_t<NN, 2, false>(p, e, s);
+      case 3: return launch_engine_t<NN, 3, false>(p, e, s);
+      default: return launch_engine_t<NN, 4, false>(p, e, s);
+    }
+  }
+}
+
+template <int NN, int CR>
+cudaError_t launch_filter_t(const oaa::FilterParams& p, const FilterPlan& f, cudaStream_t s) {
+  auto k = oaa::oaa_bwd_filter_kernel<NN, CR>;
+  cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem);
+  if (err != cudaSuccess) return err;
+  dim3 grid(f.G, f.nkg);
+  k<<<grid, f.nthreads, f.smem, s>>>(p);
+  g_launches++;
+  return cudaGetLastError();
+}
+
+template <int NN>
+cudaError_t launch_filter_n(const oaa::FilterParams& p, const FilterPlan& f, cudaStream_t s) {
+  switch (f.CR) {
+    case 1: return launch_filter_t<NN, 1>(p, f, s);
+    case 2: return launch_filter_t<NN, 2>(p, f, s);
+    case 3: return launch_filter_t<NN, 3>(p, f, s);
+    default: return launch_filter_t<NN, 4>(p, f, s);
+  }
+}
+
+#define OAA_DECLARE_N(NN)                                                                      \
+  extern template cudaError_t launch_engine_n<NN>(const oaa::EngineParams&, const EnginePlan&, \
+                                                  cudaStream_t);                              \
+  extern template cudaError_t launch_filter_n<NN>(const oaa::FilterParams&, const FilterPlan&, \
+                                                  cudaStream_t);
+#define OAA_INSTANTIATE_N(NN)                                                                 \
+  template cudaError_t launch_engine_n<NN>(const oaa::EngineParams&, const EnginePlan&,       \
+                                           cudaStream_t);                                     \
+  template cudaError_t launch_filter_n<NN>(const oaa::FilterParams&, const FilterPlan&,       \
+                                           cudaStream_t);
+
+}  // namespace oaa_host

@@ -1,0 +1,100 @@
+"""CPU-side checks of the C-ABI library (no GPU needed, no compute launched):
+liboaa.so builds/loads, exports every symbol include/oaa.h declares, and its host-side
+argument validation / size bookkeeping behave as documented.  Validation runs before
+any CUDA call, so invalid arguments can be exercised without a device."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_1601_06815_b200 as oaa
+from workloads import out_size as ref_out_size
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    hdr = open(os.path.join(ROOT, "include", "oaa.h")).read()
+    return sorted(set(re.findall(r"\b(oaa_[a-z_]+)\s*\(", hdr)))
+
+
+def test_header_symbols_exported():
+    L = oaa.lib()
+    syms = declared_symbols()
+    assert {"oaa_conv_fwd", "oaa_conv_bwd_data", "oaa_conv_bwd_filter"} <= set(syms)
+    for s in syms:
+        assert hasattr(L, s), f"liboaa.so does not export {s}"
+
+
+def test_version():
+    assert "sm_100a" in oaa.version()
+
+
+@pytest.mark.parametrize("crop", ["full", "valid", "same"])
+@pytest.mark.parametrize("N,n", [(1, 1), (5, 3), (32, 3), (224, 8), (27, 5), (3, 5), (8, 8)])
+def test_out_size_matches_convmode(N, n, crop):
+    if crop == "valid" and n > N:
+        with pytest.raises(ValueError):
+            oaa.out_size(N, n, crop)
+        return
+    assert oaa.out_size(N, n, crop) == ref_out_size(N, n, crop)
+
+
+def _call(name, B=1, C=1, K=1, N=8, n=3, crop=1, ptrs=(0x1000, 0x200000, 0x40000000),
+          ws=0x7000000000, ws_bytes=1 << 30):
+    f = getattr(oaa.lib(), name)
+    return f(ctypes.c_void_p(ptrs[0]), ctypes.c_void_p(ptrs[1]), ctypes.c_void_p(ptrs[2]),
+             B, C, K, N, n, crop, ctypes.c_void_p(ws), ctypes.c_size_t(ws_bytes), None)
+
+
+@pytest.mark.parametrize("name", ["oaa_conv_fwd", "oaa_conv_bwd_data", "oaa_conv_bwd_filter"])
+def test_invalid_arguments_rejected_before_launch(name):
+    INVALID, UNSUP = 1, 2
+    assert _call(name, B=-1) == INVALID
+    assert _call(name, C=0) == INVALID
+    assert _call(name, K=0) == INVALID
+    assert _call(name, N=0) == INVALID
+    assert _call(name, n=0) == INVALID
+    assert _call(name, crop=7) == INVALID
+    assert _call(name, N=3, n=5, crop=1) == INVALID          # Valid needs n <= N
+    assert _call(name, ptrs=(0, 0x200000, 0x40000000)) == INVALID
+    assert _call(name, n=9, N=20) == UNSUP                      # v1: n <= 8
+    assert _call(name, N=2000, n=3) == UNSUP or name == "oaa_conv_bwd_filter"
+
+
+def test_aliasing_rejected():
+    # output range overlapping an input range
+    assert _call("oaa_conv_fwd", ptrs=(0x1000, 0x200000, 0x1000)) == 1
+
+
+def test_workspace_sizes():
+    for op in (oaa.OP_FWD, oaa.OP_BWD_DATA, oaa.OP_BWD_FILTER):
+        assert oaa.workspace_bytes(op, 128, 3, 64, 224, 8, "valid") > 0
+        assert oaa.workspace_bytes(op, 128, 3, 64, 224, 8, "valid") % 256 == 0
+        assert oaa.workspace_bytes(op, 0, 3, 64, 224, 8, "valid") == 0
+        assert oaa.workspace_bytes(op, 1, 3, 64, 3, 5, "valid") == 0    # invalid -> 0
+    # too-small workspace is reported, not overrun
+    assert _call("oaa_conv_fwd", N=32, n=3, ws_bytes=16) == 3
+
+
+def test_status_strings():
+    L = oaa.lib()
+    for s in range(5):
+        assert L.oaa_status_string(s)
+
+
+def test_missing_extension_fails_loudly(monkeypatch):
+    import paper_1601_06815_b200 as pkg
+    monkeypatch.setattr(pkg, "_lib", None)
+    monkeypatch.setattr(pkg, "_LIB_PATH", "/nonexistent/liboaa.so")
+    with pytest.raises(pkg.OaAError):
+        pkg.lib()
+
+
+def test_cpu_tensors_rejected():
+    import torch
+    x = torch.zeros(1, 1, 8, 8)
+    w = torch.zeros(1, 1, 3, 3)
+    with pytest.raises(ValueError):
+        oaa.conv_fwd(x, w)

@@ -1,0 +1,263 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU float64 oracle.
+
+Bar (BASELINE.json north_star): for every output tensor, rel-L2 = ‖out−ref‖₂/‖ref‖₂ ≤ 1e-5
+and max|out−ref| ≤ 1e-4·max|ref|.  Small cases compare every element with the full
+oracle; BASELINE's full-size configs compare seeded samples of outputs that the oracle
+evaluates one by one (oracle.*_sample), plus the adjoint identity at full size.
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1601_06815_b200 as oaa
+from workloads import CONFIGS, SWEEP, make_inputs, out_size
+
+pytestmark = pytest.mark.gpu
+
+RTOL_L2 = 1e-5
+RTOL_MAX = 1e-4
+CROPS = ["full", "valid", "same"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    torch.cuda.init()
+
+
+def check(got, ref, what=""):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    assert got.shape == ref.shape, (what, got.shape, ref.shape)
+    assert np.isfinite(got).all(), f"{what}: non-finite output"
+    nref = np.linalg.norm(ref)
+    err = np.linalg.norm(got - ref)
+    mref = np.abs(ref).max() if ref.size else 0.0
+    merr = np.abs(got - ref).max() if ref.size else 0.0
+    if nref == 0:
+        assert merr == 0.0, f"{what}: expected zeros, max err {merr}"
+        return
+    assert err <= RTOL_L2 * nref, f"{what}: rel-L2 {err / nref:.3e} > {RTOL_L2}"
+    assert merr <= RTOL_MAX * mref, f"{what}: max-abs {merr:.3e} > {RTOL_MAX}·{mref:.3e}"
+
+
+def run_all(d, N, n, crop):
+    x = torch.from_numpy(d["x"]).cuda()
+    w = torch.from_numpy(d["w"]).cuda()
+    dy = torch.from_numpy(d["dy"]).cuda()
+    y = oaa.conv_fwd(x, w, crop)
+    dx = oaa.conv_bwd_data(dy, w, N, crop)
+    dw = oaa.conv_bwd_filter(x, dy, n, crop)
+    torch.cuda.synchronize()
+    return y.cpu().numpy(), dx.cpu().numpy(), dw.cpu().numpy()
+
+
+SMALL = [(N, n) for n in range(1, 9) for N in sorted({1, 2, n, n + 1, 2 * n - 1, 3 * n + 2, 17, 20})]
+
+
+@pytest.mark.parametrize("crop", CROPS)
+@pytest.mark.parametrize("N,n", SMALL)
+def test_small_grid_all_passes(N, n, crop):
+    if crop == "valid" and n > N:
+        pytest.skip("Valid needs n <= N")
+    for (B, C, K) in [(1, 1, 1), (2, 3, 2), (3, 2, 3)]:
+        d = make_inputs(B, C, K, N, n, crop, seed=N * 100 + n * 7 + B)
+        y, dx, dw = run_all(d, N, n, crop)
+        check(y, oracle.conv_fwd(d["x"], d["w"], crop), f"fwd N={N} n={n} {crop} BCK={B,C,K}")
+        check(dx, oracle.conv_bwd_data(d["dy"], d["w"], N, crop), f"bwd_data N={N} n={n} {crop}")
+        check(dw, oracle.conv_bwd_filter(d["x"], d["dy"], n, crop), f"bwd_filter N={N} n={n} {crop}")
+
+
+@pytest.mark.parametrize("crop", CROPS)
+@pytest.mark.parametrize("B,C,K", [(2, 5, 3), (1, 4, 9), (2, 7, 6), (1, 1, 13)])
+def test_channel_regimes(B, C, K, crop):
+    """C ≤ 4 takes the input-stationary path, C > 4 the output-stationary chunked one;
+    K > 4 / C > 4 exercise the chunk loops of bwd_data and bwd_filter."""
+    N, n = 19, 4
+    d = make_inputs(B, C, K, N, n, crop, seed=B * 31 + C * 7 + K)
+    y, dx, dw = run_all(d, N, n, crop)
+    check(y, oracle.conv_fwd(d["x"], d["w"], crop), "fwd")
+    check(dx, oracle.conv_bwd_data(d["dy"], d["w"], N, crop), "bwd_data")
+    check(dw, oracle.conv_bwd_filter(d["x"], d["dy"], n, crop), "bwd_filter")
+
+
+@pytest.mark.parametrize("crop", CROPS)
+def test_config1_parity(crop):
+    """BASELINE config 1: N=32, n=3, C=K=B=1, forward, vs CPU float64 direct."""
+    c = CONFIGS["parity"]
+    d = make_inputs(c.B, c.C, c.K, c.N, c.n, crop, seed=0)
+    x = torch.from_numpy(d["x"]).cuda()
+    w = torch.from_numpy(d["w"]).cuda()
+    y = oaa.conv_fwd(x, w, crop).cpu().numpy()
+    check(y, oracle.conv_fwd(d["x"], d["w"], crop), f"config1 {crop}")
+
+
+def test_delta_kernel_and_zero():
+    N, n = 23, 5
+    x = torch.rand(2, 3, N, N, device="cuda") * 2 - 1
+    w = torch.zeros(4, 3, n, n, device="cuda")
+    assert oaa.conv_fwd(x, w, "valid").abs().max().item() == 0.0
+    w[1, 2, 0, 0] = 1.0
+    y = oaa.conv_fwd(x, w, "full")
+    exp = torch.zeros(2, N + n - 1, N + n - 1, device="cuda")
+    exp[:, :N, :N] = x[:, 2]
+    assert (y[:, 1] - exp).abs().max().item() <= 1e-5
+    dy = torch.zeros(2, 4, N - n + 1, N - n + 1, device="cuda")
+    assert oaa.conv_bwd_data(dy, w, N, "valid").abs().max().item() == 0.0
+    assert oaa.conv_bwd_filter(x, dy, n, "valid").abs().max().item() == 0.0
+
+
+def test_batch_zero_is_noop_and_dw_zeroed():
+    x = torch.empty(0, 3, 16, 16, device="cuda")
+    w = torch.rand(4, 3, 3, 3, device="cuda")
+    dy = torch.empty(0, 4, 14, 14, device="cuda")
+    assert oaa.conv_fwd(x, w).shape == (0, 4, 14, 14)
+    assert oaa.conv_bwd_data(dy, w, 16).shape == (0, 3, 16, 16)
+    dw = torch.full((4, 3, 3, 3), 7.0, device="cuda")
+    oaa.conv_bwd_filter(x, dy, 3, out=dw)
+    assert dw.abs().max().item() == 0.0
+
+
+def test_deterministic_and_stream_ordered():
+    c = CONFIGS["headline"]
+    d = make_inputs(4, c.C, c.K, c.N, c.n, "valid", seed=3)
+    x = torch.from_numpy(d["x"]).cuda(); w = torch.from_numpy(d["w"]).cuda()
+    dy = torch.from_numpy(d["dy"]).cuda()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        y1 = oaa.conv_fwd(x, w); dx1 = oaa.conv_bwd_data(dy, w, c.N); dw1 = oaa.conv_bwd_filter(x, dy, c.n)
+        y2 = oaa.conv_fwd(x, w); dx2 = oaa.conv_bwd_data(dy, w, c.N); dw2 = oaa.conv_bwd_filter(x, dy, c.n)
+    s.synchronize()
+    assert torch.equal(y1, y2) and torch.equal(dx1, dx2) and torch.equal(dw1, dw2)
+
+
+def test_outputs_fully_overwritten():
+    N, n, crop = 30, 6, "same"
+    d = make_inputs(2, 2, 3, N, n, crop, seed=11)
+    x = torch.from_numpy(d["x"]).cuda(); w = torch.from_numpy(d["w"]).cuda()
+    out = torch.full((2, 3, N, N), float("nan"), device="cuda")
+    oaa.conv_fwd(x, w, crop, out=out)
+    check(out.cpu().numpy(), oracle.conv_fwd(d["x"], d["w"], crop), "fwd into NaN buffer")
+
+
+def test_autograd_module():
+    N, n = 18, 3
+    d = make_inputs(2, 3, 4, N, n, "valid", seed=5)
+    layer = oaa.OaAConv2d(3, 4, n).cuda()
+    with torch.no_grad():
+        layer.weight.copy_(torch.from_numpy(d["w"]))
+    x = torch.from_numpy(d["x"]).cuda().requires_grad_(True)
+    y = layer(x)
+    y.backward(torch.from_numpy(d["dy"]).cuda())
+    check(y.detach().cpu().numpy(), oracle.conv_fwd(d["x"], d["w"], "valid"), "module fwd")
+    check(x.grad.cpu().numpy(), oracle.conv_bwd_data(d["dy"], d["w"], N, "valid"), "module dx")
+    check(layer.weight.grad.cpu().numpy(), oracle.conv_bwd_filter(d["x"], d["dy"], n, "valid"), "module dw")
+
+
+# ----------------------------------------------------------- full-size, sampled
+def _gpu_inputs(B, C, K, N, n, crop, seed):
+    """Seeded synthetic inputs drawn on the device (uniform [-1,1), the SURVEY §8(d)
+    recipe) -- for sizes where a CPU draw + copy would dominate the test time."""
+    M = out_size(N, n, crop)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1000 + seed)
+    x = torch.rand((B, C, N, N), generator=g, device="cuda") * 2 - 1
+    w = torch.rand((K, C, n, n), generator=g, device="cuda") * 2 - 1
+    dy = torch.rand((B, K, M, M), generator=g, device="cuda") * 2 - 1
+    return x, w, dy
+
+
+def _sample_idx(rng, shape, count, extra=()):
+    idx = [tuple(int(rng.integers(0, s)) for s in shape) for _ in range(count)]
+    # edges and corners of the spatial dims (ragged tails / tile seams)
+    S1, S2 = shape[2], shape[3]
+    for a, b in itertools.product([0, 1, S1 // 2, S1 - 2, S1 - 1], [0, 1, S2 // 2, S2 - 2, S2 - 1]):
+        idx.append((int(rng.integers(0, shape[0])), int(rng.integers(0, shape[1])), max(0, a), max(0, b)))
+    idx += list(extra)
+    return np.array(idx, dtype=np.int64)
+
+
+def _check_sampled(got_t, idx, ref, what):
+    got = got_t[tuple(torch.from_numpy(idx[:, i]).to(got_t.device) for i in range(4))].double().cpu().numpy()
+    # the sampled oracle values stand in for the full tensor's norm: compare per-sample
+    # errors against the sampled reference scale (≥ the RMS of a dense sample)
+    err = np.abs(got - ref)
+    scale = np.sqrt(np.mean(ref ** 2))
+    assert np.isfinite(got).all(), what
+    assert np.sqrt(np.mean(err ** 2)) <= RTOL_L2 * scale * 1.0 + 1e-30, \
+        f"{what}: sampled rel-L2 {np.sqrt(np.mean(err ** 2)) / scale:.3e}"
+    assert err.max() <= RTOL_MAX * max(np.abs(ref).max(), scale), f"{what}: sampled max err {err.max():.3e}"
+
+
+def _adjoint(y, dy, x, dx, w, dw):
+    a = float((y.double() * dy.double()).sum())
+    b = float((x.double() * dx.double()).sum())
+    c = float((w.double() * dw.double()).sum())
+    scale = math.sqrt(float((y.double() ** 2).sum()) * float((dy.double() ** 2).sum()))
+    assert abs(a - b) <= 1e-5 * scale, (a, b, scale)
+    assert abs(a - c) <= 1e-5 * scale, (a, c, scale)
+
+
+def _full_size(cfg, crop="valid", n_samples=1500, n_dw=48, seed=0, sub_b=None):
+    B, C, K, N, n = cfg.B, cfg.C, cfg.K, cfg.N, cfg.n
+    x, w, dy = _gpu_inputs(B, C, K, N, n, crop, seed)
+    y = oaa.conv_fwd(x, w, crop)
+    dx = oaa.conv_bwd_data(dy, w, N, crop)
+    dw = oaa.conv_bwd_filter(x, dy, n, crop)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(seed)
+    # fwd / bwd_data: sampled images only need their own inputs on the host
+    bsel = sorted(set(int(v) for v in rng.integers(0, B, size=sub_b or 4)) | {0, B - 1})
+    xs = x[bsel].cpu().numpy(); ws_ = w.cpu().numpy(); dys = dy[bsel].cpu().numpy()
+    M = out_size(N, n, crop)
+    iy = _sample_idx(rng, (len(bsel), K, M, M), n_samples)
+    ref = oracle.fwd_sample(xs, ws_, crop, iy)
+    iy_g = iy.copy(); iy_g[:, 0] = np.array(bsel)[iy[:, 0]]
+    _check_sampled(y, iy_g, ref, f"{cfg.name} fwd")
+    ix = _sample_idx(rng, (len(bsel), C, N, N), n_samples)
+    ref = oracle.bwd_data_sample(dys, ws_, N, crop, ix)
+    ix_g = ix.copy(); ix_g[:, 0] = np.array(bsel)[ix[:, 0]]
+    _check_sampled(dx, ix_g, ref, f"{cfg.name} bwd_data")
+    # bwd_filter: each sampled dw element sums the whole batch
+    kc = sorted(set((int(rng.integers(0, K)), int(rng.integers(0, C))) for _ in range(max(1, n_dw // (n * n)))))
+    for (k, c) in kc:
+        xk = x[:, c:c + 1].contiguous().cpu().numpy()
+        dyk = dy[:, k:k + 1].contiguous().cpu().numpy()
+        iw = np.array([(0, 0, u, v) for u in range(n) for v in range(n)], dtype=np.int64)
+        ref = oracle.bwd_filter_sample(xk, dyk, n, crop, iw)
+        got = dw[k, c].reshape(-1).double().cpu().numpy()
+        err = np.linalg.norm(got - ref)
+        assert err <= RTOL_L2 * np.linalg.norm(ref), f"{cfg.name} dw[{k},{c}] rel {err / np.linalg.norm(ref):.3e}"
+    _adjoint(y, dy, x, dx, w, dw)
+
+
+def test_headline_full_size():
+    """BASELINE config 2 at full size, in the launch configuration bench.py times."""
+    _full_size(CONFIGS["headline"])
+
+
+@pytest.mark.parametrize("crop", ["full", "same"])
+def test_headline_other_crops(crop):
+    _full_size(CONFIGS["headline"], crop=crop, n_samples=600, n_dw=64, seed=1)
+
+
+def test_alexnet_full_size():
+    _full_size(CONFIGS["alexnet"], n_samples=800, n_dw=50, seed=2)
+
+
+@pytest.mark.parametrize("wl", SWEEP, ids=lambda w: w.name)
+def test_sweep_point(wl):
+    _full_size(wl, n_samples=300, n_dw=2 * wl.n * wl.n, seed=3)
+
+
+@pytest.mark.slow
+def test_sharded_config_one_gpu_shard():
+    """BASELINE config 5 per-GPU shard at G=8 (B=128 of the global 1024)."""
+    c = CONFIGS["sharded"]
+    from workloads import Workload
+    _full_size(Workload("sharded_shard", B=128, C=c.C, K=c.K, N=c.N, n=c.n), n_samples=400, n_dw=64, seed=4)
