@@ -29,7 +29,7 @@ __all__ = [
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_PKG, "liboaa.so")
+_LIB_PATH = os.environ.get("OAA_LIB") or os.path.join(_PKG, "liboaa.so")  # OAA_LIB: experiment builds
 CROPS = {"full": 0, "valid": 1, "same": 2}
 OP_FWD, OP_BWD_DATA, OP_BWD_FILTER = 0, 1, 2
 _STATUS = {0: "OAA_OK", 1: "OAA_ERR_INVALID_VALUE", 2: "OAA_ERR_UNSUPPORTED",

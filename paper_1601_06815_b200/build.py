@@ -47,7 +47,13 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, defines=(), out=None) -> str:
+    """Compile liboaa.so.  `defines` / `out` build an experiment variant into another
+    directory (never used by the product path)."""
+    global BUILD, LIB
+    if defines or out:
+        BUILD = os.path.join(PKG, "_build_" + "_".join(d.lower() for d in defines))
+        LIB = out or os.path.join(BUILD, "liboaa.so")
     os.makedirs(BUILD, exist_ok=True)
     srcs, hdrs = _sources(), _headers()
     objs = []
@@ -56,7 +62,8 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
         o = os.path.join(BUILD, os.path.basename(s)[:-3] + ".o")
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
-            cmd = [nvcc()] + ARCH + FLAGS + (["-Xptxas", "-v"] if ptxas_v else []) + ["-c", s, "-o", o]
+            cmd = [nvcc()] + ARCH + FLAGS + ["-D" + d for d in defines] + \
+                (["-Xptxas", "-v"] if ptxas_v else []) + ["-c", s, "-o", o]
             jobs.append(cmd)
     if jobs:
         with cf.ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
@@ -76,4 +83,6 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, ptxas_v="--ptxas" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, ptxas_v="--ptxas" in sys.argv,
+                defines=defs))

@@ -89,11 +89,12 @@ constexpr int kCRMax = 4;
 
 
 int pick_TS(int T, int n) {
-  // stride of the t2 index in the shared Q buffer, chosen so stage-A stores and stage-B
-  // loads are (near) bank-conflict free: TS ≡ 32/n (mod 32).
-  int target = std::max(1, 32 / n) % 32;
+  // stride (in float2) of the t2 index in the shared Q buffer, chosen so stage-A stores
+  // and stage-B loads (64-bit, two 16-lane phases) are (near) bank-conflict free:
+  // TS ≡ 16/n (mod 16).
+  int target = std::max(1, 16 / n) % 16;
   int TS = T;
-  while ((TS % 32) != target) ++TS;
+  while ((TS % 16) != target) ++TS;
   return TS;
 }
 
@@ -109,8 +110,8 @@ bool plan_engine(int R, int Ro, int off, int n, int Cin, int Cout, EnginePlan* e
   if (need > oaa::kMaxThreads) return false;
   e->nthreads = cdiv(need, 32) * 32;
   e->TS = pick_TS(e->T, n);
-  const int P = 2 * n - 1, H = n;
-  e->smem = sizeof(float) * 2 /*buf*/ * 2 /*re,im*/ * (size_t)H * P * e->TS;
+  e->BW = cdiv(e->T * n, 4) * 4;
+  const int P = 2 * n - 1, H = n, P2 = (P + 1) / 2;
   if (Cin <= kCRMax) {
     e->S1 = true;
     e->CR = Cin;
@@ -118,9 +119,14 @@ bool plan_engine(int R, int Ro, int off, int n, int Cin, int Cout, EnginePlan* e
     e->S1 = false;
     e->CR = std::min(Cout, kCRMax);
   }
-  return e->smem <= 200 * 1024;
+  const int nsb = e->S1 ? 3 : 2;
+  const int cin_s = e->S1 ? Cin : e->CR;
+  const int nband = e->S1 ? Cin : 2;
+  e->smem = sizeof(float2) * 2 * ((size_t)H * P * e->TS + 2) + sizeof(float4) * (size_t)nsb * cin_s * P2 * H +
+            sizeof(float) * (size_t)nband * n * e->BW +
+            sizeof(float) * (size_t)oaa::kRingDepth * (n - 1) * e->nthreads;
+  return e->smem <= 220 * 1024;
 }
-
 
 bool plan_filter(int B, int C, int K, int M, int n, FilterPlan* f) {
   const int H = n, P = 2 * n - 1;
@@ -130,13 +136,15 @@ bool plan_filter(int B, int C, int K, int M, int n, FilterPlan* f) {
   f->nkg = cdiv(K, f->KG);
   f->nthreads = cdiv(f->KG * H, 32) * 32;
   f->CR = std::min(C, kCRMax);
-  // tiles per Ξ̂ chunk: enough (tile, c, f1) tasks to keep every thread busy once
-  f->TCH = std::max(1, std::min(f->Td, f->nthreads / (f->CR * H)));
-  f->smem = sizeof(float2) * (size_t)f->TCH * f->CR * P * H;
+  f->TCH = std::max(1, std::min(f->Td, 32 / n));
+  f->XW = cdiv(f->Td * n + n - 1, 4) * 4;
+  f->DW = cdiv(f->TCH * n, 4) * 4;
+  f->smem = sizeof(float) * (size_t)f->CR * P * f->XW + sizeof(float2) * (size_t)f->Td * f->CR * P * H +
+            2 * sizeof(float) * (size_t)f->KG * n * f->DW + sizeof(float2) * 16;
   const int items = std::max(1, B * f->Td);
   // one persistent wave: ~148 SMs on B200 (fixed so results do not depend on the device)
   f->G = std::max(1, std::min(items, 148 / f->nkg));
-  return f->smem <= 200 * 1024;
+  return f->smem <= 220 * 1024;
 }
 
 // ---------------------------------------------------------------- dispatch
@@ -204,7 +212,7 @@ struct EngineWs {
 EngineWs engine_ws(int B, int C, int K, int Tr, const Geo& g) {
   EngineWs w{};
   w.spec_off = 0;
-  w.flags_off = align_up(sizeof(float2) * (size_t)K * C * g.P * g.H);
+  w.flags_off = align_up(sizeof(float4) * (size_t)K * C * ((g.P + 1) / 2) * g.H);
   w.counter_off = align_up(w.flags_off + sizeof(int) * (size_t)std::max(1, B * Tr));
   w.total = align_up(w.counter_off + sizeof(int));
   return w;
@@ -216,7 +224,7 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
   Geo g;
   oaa_status_t st = validate(B, C, K, N, n, crop, &g);
   if (st != OAA_OK) return st;
-  if (!in || !w || !out) return OAA_ERR_INVALID_VALUE;
+  if (!w || (B > 0 && (!in || !out))) return OAA_ERR_INVALID_VALUE;
   const int R = is_fwd ? N : g.M, Ro = is_fwd ? g.M : N;
   const int Cin = is_fwd ? C : K, Cout = is_fwd ? K : C;
   const int off = is_fwd ? g.o : (n - 1 - g.o);
@@ -235,14 +243,14 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
     return OAA_ERR_INVALID_VALUE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   char* base = static_cast<char*>(ws);
-  float2* spec = reinterpret_cast<float2*>(base + L.spec_off);
+  float4* spec = reinterpret_cast<float4*>(base + L.spec_off);
   int* flags = reinterpret_cast<int*>(base + L.flags_off);
   int* counter = reinterpret_cast<int*>(base + L.counter_off);
 
   // kernel spectra: loop-major layout [Cloop][Cinner][P][H]
   const int loop_is_k = (is_fwd == e.S1) ? 1 : 0;  // fwd S1 / bwd_data S2 loop over k
   {
-    const long total = (long)K * C * g.P * g.H;
+    const long total = (long)K * C * ((g.P + 1) / 2) * g.H;
     const int thr = 256;
     const int blocks = (int)std::min<long>((total + thr - 1) / thr, 4096);
     oaa::oaa_spectrum_kernel<<<blocks, thr, 0, s>>>(w, spec, K, C, n, is_fwd ? 0 : 1, loop_is_k);
@@ -265,6 +273,7 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
   p.Ro = Ro;
   p.off = off;
   p.TS = e.TS;
+  p.BW = e.BW;
   p.num_items = B * e.T;
   ProfScope prof(is_fwd ? OAA_OP_FWD : OAA_OP_BWD_DATA, s);
   prof.start();
@@ -320,7 +329,7 @@ oaa_status_t oaa_conv_bwd_filter(const float* x, const float* dy, float* dw, int
   Geo g;
   oaa_status_t st = validate(B, C, K, N, n, crop, &g);
   if (st != OAA_OK) return st;
-  if (!x || !dy || !dw) return OAA_ERR_INVALID_VALUE;
+  if (!dw || (B > 0 && (!x || !dy))) return OAA_ERR_INVALID_VALUE;
   const size_t x_bytes = sizeof(float) * (size_t)B * C * N * N;
   const size_t dy_bytes = sizeof(float) * (size_t)B * K * g.M * g.M;
   const size_t dw_bytes = sizeof(float) * (size_t)K * C * n * n;
@@ -354,6 +363,8 @@ oaa_status_t oaa_conv_bwd_filter(const float* x, const float* dy, float* dw, int
   p.G = f.G;
   p.KG = f.KG;
   p.TCH = f.TCH;
+  p.XW = f.XW;
+  p.DW = f.DW;
   ProfScope prof(OAA_OP_BWD_FILTER, s);
   prof.start();
   cudaError_t err = launch_filter(n, p, f, s);

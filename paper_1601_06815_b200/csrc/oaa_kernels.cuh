@@ -2,21 +2,24 @@
 //
 // Notation: input blocks are n×n, transforms are P×P with
 // P = 2n−1, the half spectrum keeps rows f1 ∈ [0,H), H = n, and all
-// columns f2 ∈ [0,P).  A "work item" is one tile row (b, t1) of one image.
+// columns f2 ∈ [0,P) (stored as P2 = (P+1)/2 pairs, the last one zero-padded).  A
+// "work item" is one tile row (b, t1) of one image.
 //
 //  * oaa_engine_kernel<n, CR, S1>: forward and bwd_data
 //    -- tile, pad, 2-D DFT, per-bin channel contraction, inverse DFT, overlap-add, crop --
-//    in ONE pass.  Stage A lanes own (tile t2, spectrum row f1); stage B lanes own one
-//    output column.  Horizontal overlap (n−1 columns) is resolved inside stage B by
-//    summing the two contributing block columns BEFORE the last inverse transform
-//    (linearity); vertical overlap (n−1 rows) is a read-modify-write of the previous
-//    tile row's partial rows, ordered by a per-item release/acquire flag.
+//    in ONE pass.  The item's input rows are staged in shared memory (cp.async, zero
+//    padded); stage-A lanes own (tile t2, spectrum row f1); stage-B lanes own one output
+//    column.  Horizontal overlap (n−1 columns) is resolved inside stage B by summing the
+//    two contributing block columns BEFORE the last inverse transform (linearity);
+//    vertical overlap (n−1 rows) is a read-modify-write of the previous tile row's
+//    partial rows, ordered by a per-item release flag and deferred by two output
+//    channels so the predecessor is normally already past it.
 //      S1 (input-stationary): the input spectra of ≤ CR channels live in registers and
 //         every output channel is contracted + inverse-transformed in turn.
 //      S2 (output-stationary): ≤ CR output-channel accumulators live in registers and
 //         every input channel is transformed + contracted into them.
 //  * oaa_bwd_filter_kernel<n, CR>: weight gradient: per dy block s the
-//    (2n−1)² x-window spectrum Ξ̂ and the block spectrum Ĝ, dŴ += conj(Ĝ)·Ξ̂, lanes own
+//    (2n−1)² x-window spectrum Ξ̂ and the block spectrum Ĝ, dŴ += conj(Ĝ)·Ξ̂; lanes own
 //    (k, f1) and accumulate over a static, deterministic slice of the batch.
 //  * oaa_filter_finalize_kernel: fixed-order fp64 sum of the per-CTA partial spectra,
 //    inverse DFT, lag read-out dw[k,c,u,v] = r[n−1−u, n−1−v].
@@ -30,46 +33,98 @@
 
 namespace oaa {
 
-constexpr int kMaxThreads = 256;  // CTA size cap: max(T·H, Ro) ≤ 256 ⇒ N ≲ 250
+constexpr int kMaxThreads = 256;  // CTA size cap: max(T·n, Ro) ≤ 256 ⇒ N ≲ 250
 
 struct EngineParams {
   const float* in;      // [B][Cin][R][R]
-  const float2* spec;   // [Cloop][Cinner][P][H]  (S1: loop=cout, S2: loop=cin)
+  const float4* spec;   // [Cloop][Cinner][P2][H] (f2 pairs; S1: loop=cout, S2: loop=cin)
   float* out;           // [B][Cout][Ro][Ro]
   int* flags;           // [B*T] progress of each work item (# output channels stored)
   int* counter;         // dynamic work-item counter
-  int B, Cin, Cout, R, T, Ro, off, TS, num_items;
+  int B, Cin, Cout, R, T, Ro, off, TS, BW, num_items;
 };
 
 struct FilterParams {
   const float* x;       // [B][C][N][N]
   const float* dy;      // [B][K][M][M]
   float2* partial;      // [G][K][C][P][H]
-  int B, C, K, N, M, off, Td, G, KG, TCH;
+  int B, C, K, N, M, off, Td, G, KG, TCH, XW, DW;
 };
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
+// ------------------------------------------------------------ memory helpers
+__device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_release(int* p, int v) {
+#ifdef OAA_EXP_RELAXED_PUBLISH
+  asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+#else
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+#endif
+}
+__device__ __forceinline__ void cp_async4(float* smem, const float* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s), "l"(gmem),
+               "r"(valid ? 4 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// Stage rows [r0, r0+nrows) × cols [c0, c0+ncols) of an R×R plane into smem rows of
+// stride `ld` (zero outside the plane: the zero-filled edge blocks of PAPER.md:18).
+// Threads own columns (no integer division); rows whose start is 16-byte aligned and
+// whose column range is a multiple of 4 go through 16-byte cp.async.
+__device__ __forceinline__ void stage_rows(float* dst, int ld, const float* __restrict__ plane,
+                                           int R, int r0, int nrows, int c0, int ncols, int tid,
+                                           int nthr) {
+  if (((R | c0 | ncols | ld) & 3) == 0) {
+    for (int g = tid; g < (ncols >> 2); g += nthr) {
+      const int q = c0 + 4 * g;
+      const bool qok = q >= 0 && q < R;  // groups are entirely in or out (R % 4 == 0)
+      for (int rr = 0; rr < nrows; ++rr) {
+        const int r = r0 + rr;
+        const bool ok = qok && r >= 0 && r < R;
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + rr * ld + 4 * g);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa),
+                     "l"(ok ? plane + (size_t)r * R + q : plane), "r"(ok ? 16 : 0)
+                     : "memory");
+      }
+    }
+  } else {
+    for (int cc = tid; cc < ncols; cc += nthr) {
+      const int q = c0 + cc;
+      const bool qok = q >= 0 && q < R;
+      for (int rr = 0; rr < nrows; ++rr) {
+        const int r = r0 + rr;
+        const bool ok = qok && r >= 0 && r < R;
+        cp_async4(dst + rr * ld + cc, ok ? plane + (size_t)r * R + q : plane, ok);
+      }
+    }
+  }
 }
 
-// Load one n×n block (rows r0.., cols c0..) of an R×R plane, zero outside (PAPER.md:18
-// "rounded up" edge blocks are zero-filled; reading R13).
+// Read one n×n block from staged rows (row stride ld, block column origin c).
 template <int NN>
-__device__ __forceinline__ void load_block(const float* __restrict__ plane, int R, int r0, int c0,
-                                           float (&z)[NN][NN]) {
+__device__ __forceinline__ void read_block(const float* src, int ld, int c, float (&z)[NN][NN]) {
 #pragma unroll
   for (int p1 = 0; p1 < NN; ++p1) {
-    const int r = r0 + p1;
-    const bool rok = (r >= 0) && (r < R);
+    if constexpr (NN % 4 == 0) {
 #pragma unroll
-    for (int p2 = 0; p2 < NN; ++p2) {
-      const int q = c0 + p2;
-      z[p1][p2] = (rok && q >= 0 && q < R) ? __ldg(plane + (size_t)r * R + q) : 0.f;
+      for (int q = 0; q < NN; q += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(src + p1 * ld + c + q);
+        z[p1][q] = v.x; z[p1][q + 1] = v.y; z[p1][q + 2] = v.z; z[p1][q + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < NN; ++q) z[p1][q] = src[p1 * ld + c + q];
     }
   }
 }
@@ -86,9 +141,9 @@ __device__ __forceinline__ void block_row_spectrum(const float (&z)[NN][NN], con
   float rr[P], ri[P];
 #pragma unroll
   for (int p2 = 0; p2 < NN; ++p2) {
-    float a = 0.f, b = 0.f;
+    float a = z[0][p2], b = 0.f;  // p1 = 0 twiddle is 1
 #pragma unroll
-    for (int p1 = 0; p1 < NN; ++p1) {
+    for (int p1 = 1; p1 < NN; ++p1) {
       a = fmaf(z[p1][p2], cf[p1], a);
       b = fmaf(-z[p1][p2], sf[p1], b);
     }
@@ -101,87 +156,97 @@ __device__ __forceinline__ void block_row_spectrum(const float (&z)[NN][NN], con
 }
 
 // Stage A tail: inverse DFT along f2 of one spectrum row and store it, transposed, to
-// the shared Q buffer  Q[f1][p2][t2]  (separate re / im planes).
+// the shared Q buffer  Q[f1][p2][t2]  (complex, float2).
 template <int NN>
-__device__ __forceinline__ void stage_a_store(float (&yr)[2 * NN - 1], float (&yi)[2 * NN - 1],
-                                              float* __restrict__ Qr, float* __restrict__ Qi,
-                                              int f1, int t2, int TS) {
+__device__ __forceinline__ void stage_a_store(const float (&yr)[2 * NN - 1], const float (&yi)[2 * NN - 1],
+                                              float2* __restrict__ Q, int f1, int t2, int TS) {
   constexpr int P = 2 * NN - 1;
   float qr[P], qi[P];
   dft<P, +1>(yr, yi, qr, qi);
 #pragma unroll
-  for (int p2 = 0; p2 < P; ++p2) {
-    Qr[(f1 * P + p2) * TS + t2] = qr[p2];
-    Qi[(f1 * P + p2) * TS + t2] = qi[p2];
-  }
+  for (int p2 = 0; p2 < P; ++p2) Q[(f1 * P + p2) * TS + t2] = make_float2(qr[p2], qi[p2]);
 }
 
-// Stage B: one output column j.  Sums the two block columns that land on it, applies the
-// Hermitian inverse along f1 (c2r), and writes the rows of this tile row:
-//   rows p1 ∈ [n−1, 2n−1) are plain stores (p1 ≥ n are partial until the next tile row
-//   adds its top rows), rows p1 ∈ [0, n−1) are added onto the previous tile row's partial
-//   values once its flag says channel `ch` is stored.
+// Stage-B lane geometry for output column J (Full-frame coordinate): the two block
+// columns that land on it (block tA at p2 = pA, block tA−1 at p2 = pA + n) as float2
+// offsets into a Q buffer; an absent contributor points at the buffer's zero slot with
+// stride 0, so the loads are branch-free.
+struct ColGeo {
+  int offA, strA, offB, strB;
+};
 template <int NN>
-__device__ __forceinline__ void stage_b(const float* __restrict__ Qr, const float* __restrict__ Qi,
-                                        int TS, int T, int j, int off, int Ro, int t1,
-                                        float* __restrict__ plane, const int* prev_flag, int ch,
-                                        int lane, unsigned bmask) {
-  constexpr int P = 2 * NN - 1, H = NN;
-  const int J = j + off;
+__device__ __forceinline__ ColGeo col_geo(int J, int T, int TS, int qzero) {
+  constexpr int P = 2 * NN - 1;
   const int tA = J / NN, pA = J - tA * NN;
   const bool vA = tA < T;
   const bool vB = (tA >= 1) && (pA <= NN - 2);
-  float zr[H], zi[H];
-#pragma unroll
-  for (int f1 = 0; f1 < H; ++f1) {
-    float a = 0.f, b = 0.f;
-    if (vA) { a = Qr[(f1 * P + pA) * TS + tA]; b = Qi[(f1 * P + pA) * TS + tA]; }
-    if (vB) { a += Qr[(f1 * P + pA + NN) * TS + tA - 1]; b += Qi[(f1 * P + pA + NN) * TS + tA - 1]; }
-    zr[f1] = a;
-    zi[f1] = b;
-  }
-  float y[P];
-  c2r_half<P>(zr, zi, y);
-  const int I0 = t1 * NN - off;  // output row of block row p1 = 0
-#pragma unroll
-  for (int p1 = NN - 1; p1 < P; ++p1) {
-    const int i = I0 + p1;
-    if (i >= 0 && i < Ro) plane[(size_t)i * Ro + j] = y[p1];
-  }
-  if (NN > 1) {
-    if (prev_flag == nullptr) {
-#pragma unroll
-      for (int p1 = 0; p1 < NN - 1; ++p1) {
-        const int i = I0 + p1;
-        if (i >= 0 && i < Ro) plane[(size_t)i * Ro + j] = y[p1];
-      }
-    } else {
-      // one poll per warp; __syncwarp orders the other lanes' loads after the acquire
-      if (lane == 0) {
-        while (ld_acquire(prev_flag) < ch + 1) __nanosleep(64);
-      }
-      __syncwarp(bmask);
-#pragma unroll
-      for (int p1 = 0; p1 < NN - 1; ++p1) {
-        const int i = I0 + p1;
-        if (i >= 0 && i < Ro) {
-          float* a = plane + (size_t)i * Ro + j;
-          *a = __ldcg(a) + y[p1];
-        }
-      }
-    }
-  }
+  ColGeo g;
+  g.offA = vA ? pA * TS + tA : qzero;
+  g.strA = vA ? P * TS : 0;
+  g.offB = vB ? (pA + NN) * TS + tA - 1 : qzero;
+  g.strB = vB ? P * TS : 0;
+  return g;
 }
 
+// Sum the two block columns and apply the Hermitian inverse along f1 (c2r): y[p1] is
+// block row p1 of this tile row in output column J.
+template <int NN>
+__device__ __forceinline__ void stage_b_column(const float2* __restrict__ Q, const ColGeo& g,
+                                               float (&y)[2 * NN - 1]) {
+  constexpr int P = 2 * NN - 1, H = NN;
+  float zr[H], zi[H];
+  const float2* qa = Q + g.offA;
+  const float2* qb = Q + g.offB;
+#pragma unroll
+  for (int f1 = 0; f1 < H; ++f1) {
+    const float2 a = qa[f1 * g.strA];
+    const float2 b = qb[f1 * g.strB];
+    zr[f1] = a.x + b.x;
+    zi[f1] = a.y + b.y;
+  }
+  c2r_half<P>(zr, zi, y);
+}
+
+constexpr int kRingDepth = 8;   // deferred output channels per stage-B lane (smem ring)
+constexpr int kPublishEvery = 4;  // progress-flag granularity (output channels)
+
+// Poll (one lane per warp) until the predecessor item published ≥ need channels.  The
+// data that follows is read with ld.global.cg (L2, the point of coherence), so no L1
+// invalidation (acquire / fence) is needed on this path.
+__device__ __forceinline__ void wait_flag(const int* flag, int need, int lane, unsigned mask) {
+#ifdef OAA_EXP_NO_WAIT
+  return;
+#endif
+  if (lane == (__ffs(mask) - 1)) {
+    while (ld_relaxed(flag) < need) __nanosleep(32);
+  }
+  __syncwarp(mask);
+}
+
+// ------------------------------------------------------------------ engine
+// Shared memory: Q[2][H][P][TS] (+1 zero slot each) float2 | spectra[NSB][Cinner][P2][H]
+// float4 | staged input rows [S1: Cin | S2: 2][n][BW] floats | top-row ring
+// [kRingDepth][n−1][nthr] floats.
 template <int NN, int CR, bool S1>
 __global__ void __launch_bounds__(kMaxThreads, 1) oaa_engine_kernel(const EngineParams p) {
-  constexpr int P = 2 * NN - 1, H = NN;
-  extern __shared__ float smem[];
+  constexpr int P = 2 * NN - 1, H = NN, P2 = (P + 1) / 2, TR = NN - 1;
+  constexpr int NSB = S1 ? 3 : 2;  // spectrum buffers
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_item;
-  const int TS = p.TS;
-  const int qplane = H * P * TS;
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
+  const int TS = p.TS, BW = p.BW;
+  const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
+  const int qsz = H * P * TS + 2;                  // float2 per Q buffer (+ zero slot, pad)
+  const int CIN_S = S1 ? p.Cin : CR;               // inner channels per spectrum buffer
+  const int ssz = CIN_S * P2 * H;                  // float4 per spectrum buffer
+  float2* Qs = reinterpret_cast<float2*>(smem_raw);
+  float4* Ss = reinterpret_cast<float4*>(Qs + 2 * qsz);
+  float* band = reinterpret_cast<float*>(Ss + NSB * ssz);
+  const int bandsz = NN * BW;                      // floats per staged channel
+  float* ring = band + (S1 ? p.Cin : 2) * bandsz;  // [kRingDepth][TR][nthr]
+  if (tid == 0) {
+    Qs[qsz - 2] = make_float2(0.f, 0.f);
+    Qs[2 * qsz - 2] = make_float2(0.f, 0.f);
+  }
 
   // stage A lane = (t2, f1)
   const int a_t = tid / H, a_f1 = tid - (tid / H) * H;
@@ -197,123 +262,256 @@ __global__ void __launch_bounds__(kMaxThreads, 1) oaa_engine_kernel(const Engine
   // stage B lane = output column j
   const bool laneB = tid < p.Ro;
   const unsigned bmask = __ballot_sync(0xffffffffu, laneB);
+  const ColGeo cg = col_geo<NN>(tid + p.off, p.T, TS, qsz - 2);
+  const size_t plane_sz = (size_t)p.Ro * p.Ro;
 
   for (;;) {
+    __syncthreads();  // previous item fully done with smem / s_item
     if (tid == 0) s_item = atomicAdd(p.counter, 1);
     __syncthreads();
     const int item = s_item;
     if (item >= p.num_items) break;
     const int b = item / p.T, t1 = item - (item / p.T) * p.T;
-    const int* prev_flag = (t1 > 0) ? (p.flags + item - 1) : nullptr;
+    const bool has_pred = (t1 > 0) && (TR > 0);
+    const int* pred_flag = p.flags + item - 1;
     const float* in_b = p.in + (size_t)b * p.Cin * p.R * p.R;
-    float* out_b = p.out + (size_t)b * p.Cout * p.Ro * p.Ro;
-    int done = 0;  // output channels whose bottom rows are stored (published at barriers)
+    const int I0 = t1 * NN - p.off;  // output row of block row p1 = 0
+    // rows of this tile row inside the output window, as a bit mask over p1
+    unsigned rows = 0;
+#pragma unroll
+    for (int p1 = 0; p1 < P; ++p1)
+      if (I0 + p1 >= 0 && I0 + p1 < p.Ro) rows |= 1u << p1;
+    // column pointer of block row 0 in output channel 0 (may point outside; only
+    // dereferenced for rows in `rows`)
+    float* colp = p.out + (size_t)b * p.Cout * plane_sz + (ptrdiff_t)I0 * p.Ro + tid;
+
+    // finish the top rows of output channel c: predecessor's partial rows + ours
+    auto finalize = [&](int c, const float (&pend)[TR > 0 ? TR : 1]) {
+      float* cp = colp + (size_t)c * plane_sz;
+      const float* rg = ring + (c % kRingDepth) * TR * nthr + tid;
+#pragma unroll
+      for (int p1 = 0; p1 < TR; ++p1)
+        if ((rows >> p1) & 1u) __stcs(cp + (ptrdiff_t)p1 * p.Ro, pend[p1] + rg[p1 * nthr]);
+    };
+    auto prefetch = [&](int c, float (&pend)[TR > 0 ? TR : 1]) {
+      const float* cp = colp + (size_t)c * plane_sz;
+#pragma unroll
+      for (int p1 = 0; p1 < TR; ++p1)
+        pend[p1] = ((rows >> p1) & 1u) ? __ldcg(cp + (ptrdiff_t)p1 * p.Ro) : 0.f;
+    };
+
+    // per output channel: stage A (given this lane's row spectrum yr/yi), barrier,
+    // publish, stage B with the deferred overlap-add.
+    auto out_channel = [&](int co, const float (&yr)[P], const float (&yi)[P]) {
+      float2* Q = Qs + (co & 1) * qsz;
+      float pend[TR > 0 ? TR : 1];
+      const bool fin = laneB && has_pred && co >= kRingDepth;
+      if (fin) {
+        wait_flag(pred_flag, co - kRingDepth + 1, lane, bmask);
+        prefetch(co - kRingDepth, pend);
+      }
+      if (laneA) stage_a_store<NN>(yr, yi, Q, a_f1, a_t, TS);
+      cp_async_wait_1();  // all but the newest group (the spectrum prefetch for co+2)
+      __syncthreads();
+      if (tid == 0 && co > 0 && (co % kPublishEvery) == 0) st_release(p.flags + item, co);
+      if (laneB) {
+        float y[P];
+        stage_b_column<NN>(Q, cg, y);
+        float* cp = colp + (size_t)co * plane_sz;
+#pragma unroll
+        for (int p1 = TR; p1 < P; ++p1) {
+          if ((rows >> p1) & 1u) {
+            if (p1 >= NN) __stcg(cp + (ptrdiff_t)p1 * p.Ro, y[p1]);   // partial: the next tile row adds
+            else __stcs(cp + (ptrdiff_t)p1 * p.Ro, y[p1]);           // final
+          }
+        }
+        if (!has_pred) {
+#pragma unroll
+          for (int p1 = 0; p1 < TR; ++p1)
+            if ((rows >> p1) & 1u) __stcs(cp + (ptrdiff_t)p1 * p.Ro, y[p1]);
+        } else {
+          if (fin) finalize(co - kRingDepth, pend);
+          float* rg = ring + (co % kRingDepth) * TR * nthr + tid;
+#pragma unroll
+          for (int p1 = 0; p1 < TR; ++p1) rg[p1 * nthr] = y[p1];
+        }
+      }
+    };
 
     if constexpr (S1) {
+      // stage the item's input rows and the first two output channels' spectra
+      for (int c = 0; c < p.Cin; ++c)
+        stage_rows(band + c * bandsz, BW, in_b + (size_t)c * p.R * p.R, p.R, t1 * NN, NN, 0, BW, tid, nthr);
+      for (int co = 0; co < 2 && co < p.Cout; ++co)
+        for (int e = tid; e < ssz; e += nthr) cp_async16(Ss + co * ssz + e, p.spec + (size_t)co * ssz + e);
+      cp_async_commit();
+      cp_async_wait_all();
+      __syncthreads();
       float xr[CR][P], xi[CR][P];
       if (laneA) {
 #pragma unroll
         for (int c = 0; c < CR; ++c) {
           if (c < p.Cin) {
             float z[NN][NN];
-            load_block<NN>(in_b + (size_t)c * p.R * p.R, p.R, t1 * NN, a_t * NN, z);
+            read_block<NN>(band + c * bandsz, BW, a_t * NN, z);
             block_row_spectrum<NN>(z, cf, sf, xr[c], xi[c]);
           }
         }
       }
       for (int co = 0; co < p.Cout; ++co) {
-        const int buf = co & 1;
-        float* Qr = smem + buf * 2 * qplane;
-        float* Qi = Qr + qplane;
+        float yr[P], yi[P];
         if (laneA) {
-          float yr[P], yi[P];
 #pragma unroll
           for (int f2 = 0; f2 < P; ++f2) { yr[f2] = 0.f; yi[f2] = 0.f; }
-          const float2* s = p.spec + (size_t)co * p.Cin * P * H + a_f1;
+          const float4* S = Ss + (co % NSB) * ssz + a_f1;
 #pragma unroll
           for (int c = 0; c < CR; ++c) {
             if (c < p.Cin) {
 #pragma unroll
-              for (int f2 = 0; f2 < P; ++f2) {
-                const float2 w = __ldg(s + (c * P + f2) * H);
-                yr[f2] = fmaf(w.x, xr[c][f2], yr[f2]);
-                yr[f2] = fmaf(-w.y, xi[c][f2], yr[f2]);
-                yi[f2] = fmaf(w.x, xi[c][f2], yi[f2]);
-                yi[f2] = fmaf(w.y, xr[c][f2], yi[f2]);
-              }
-            }
-          }
-          stage_a_store<NN>(yr, yi, Qr, Qi, a_f1, a_t, TS);
-        }
-        __syncthreads();
-        if (tid == 0 && co > 0) st_release(p.flags + item, co);
-        if (laneB)
-          stage_b<NN>(Qr, Qi, TS, p.T, tid, p.off, p.Ro, t1, out_b + (size_t)co * p.Ro * p.Ro,
-                      prev_flag, co, lane, bmask);
-      }
-      done = p.Cout;
-    } else {
-      for (int c0 = 0; c0 < p.Cout; c0 += CR) {
-        const int nc = min(CR, p.Cout - c0);
-        float ar[CR][P], ai[CR][P];
-#pragma unroll
-        for (int cc = 0; cc < CR; ++cc)
-#pragma unroll
-          for (int f2 = 0; f2 < P; ++f2) { ar[cc][f2] = 0.f; ai[cc][f2] = 0.f; }
-        if (laneA) {
-          for (int ci = 0; ci < p.Cin; ++ci) {
-            float z[NN][NN];
-            load_block<NN>(in_b + (size_t)ci * p.R * p.R, p.R, t1 * NN, a_t * NN, z);
-            float gr[P], gi[P];
-            block_row_spectrum<NN>(z, cf, sf, gr, gi);
-            const float2* s = p.spec + ((size_t)ci * p.Cout + c0) * P * H + a_f1;
-#pragma unroll
-            for (int cc = 0; cc < CR; ++cc) {
-              if (cc < nc) {
-#pragma unroll
-                for (int f2 = 0; f2 < P; ++f2) {
-                  const float2 w = __ldg(s + (cc * P + f2) * H);
-                  ar[cc][f2] = fmaf(w.x, gr[f2], ar[cc][f2]);
-                  ar[cc][f2] = fmaf(-w.y, gi[f2], ar[cc][f2]);
-                  ai[cc][f2] = fmaf(w.x, gi[f2], ai[cc][f2]);
-                  ai[cc][f2] = fmaf(w.y, gr[f2], ai[cc][f2]);
+              for (int q = 0; q < P2; ++q) {
+                const float4 w = S[(c * P2 + q) * H];
+                const int f = 2 * q;
+                yr[f] = fmaf(w.x, xr[c][f], yr[f]);
+                yr[f] = fmaf(-w.y, xi[c][f], yr[f]);
+                yi[f] = fmaf(w.x, xi[c][f], yi[f]);
+                yi[f] = fmaf(w.y, xr[c][f], yi[f]);
+                if (f + 1 < P) {
+                  yr[f + 1] = fmaf(w.z, xr[c][f + 1], yr[f + 1]);
+                  yr[f + 1] = fmaf(-w.w, xi[c][f + 1], yr[f + 1]);
+                  yi[f + 1] = fmaf(w.z, xi[c][f + 1], yi[f + 1]);
+                  yi[f + 1] = fmaf(w.w, xr[c][f + 1], yi[f + 1]);
                 }
               }
             }
           }
         }
+        // prefetch the spectrum of channel co+2 (its buffer was last read before the
+        // previous barrier)
+        if (co + 2 < p.Cout)
+          for (int e = tid; e < ssz; e += nthr)
+            cp_async16(Ss + ((co + 2) % NSB) * ssz + e, p.spec + (size_t)(co + 2) * ssz + e);
+        cp_async_commit();  // always (possibly empty) so wait_group 1 keeps its meaning
+        out_channel(co, yr, yi);
+      }
+    } else {
+      for (int c0 = 0; c0 < p.Cout; c0 += CR) {
+        const int nc = min(CR, p.Cout - c0);
+        const int ssz_c = nc * P2 * H;
+        float ar[CR][P], ai[CR][P];
 #pragma unroll
-        for (int cc = 0; cc < CR; ++cc) {
-          if (cc < nc) {
-            const int co = c0 + cc;
-            const int buf = co & 1;
-            float* Qr = smem + buf * 2 * qplane;
-            float* Qi = Qr + qplane;
-            if (laneA) stage_a_store<NN>(ar[cc], ai[cc], Qr, Qi, a_f1, a_t, TS);
-            __syncthreads();
-            if (tid == 0 && co > 0) st_release(p.flags + item, co);
-            if (laneB)
-              stage_b<NN>(Qr, Qi, TS, p.T, tid, p.off, p.Ro, t1, out_b + (size_t)co * p.Ro * p.Ro,
-                          prev_flag, co, lane, bmask);
+        for (int cc = 0; cc < CR; ++cc)
+#pragma unroll
+          for (int f2 = 0; f2 < P; ++f2) { ar[cc][f2] = 0.f; ai[cc][f2] = 0.f; }
+        // prologue: stage input channel 0
+        stage_rows(band, BW, in_b, p.R, t1 * NN, NN, 0, BW, tid, nthr);
+        for (int e = tid; e < ssz_c; e += nthr) cp_async16(Ss + e, p.spec + (size_t)c0 * P2 * H + e);
+        cp_async_commit();
+        for (int ci = 0; ci < p.Cin; ++ci) {
+          cp_async_wait_all();
+          __syncthreads();
+          if (ci + 1 < p.Cin) {  // stage the next input channel while this one computes
+            const int nb = (ci + 1) & 1;
+            stage_rows(band + nb * bandsz, BW, in_b + (size_t)(ci + 1) * p.R * p.R, p.R, t1 * NN, NN, 0,
+                       BW, tid, nthr);
+            for (int e = tid; e < ssz_c; e += nthr)
+              cp_async16(Ss + nb * ssz + e, p.spec + ((size_t)(ci + 1) * p.Cout + c0) * P2 * H + e);
+            cp_async_commit();
+          }
+          if (laneA) {
+            float z[NN][NN];
+            read_block<NN>(band + (ci & 1) * bandsz, BW, a_t * NN, z);
+            float gr[P], gi[P];
+            block_row_spectrum<NN>(z, cf, sf, gr, gi);
+            const float4* S = Ss + (ci & 1) * ssz + a_f1;
+#pragma unroll
+            for (int cc = 0; cc < CR; ++cc) {
+              if (cc < nc) {
+#pragma unroll
+                for (int q = 0; q < P2; ++q) {
+                  const float4 w = S[(cc * P2 + q) * H];
+                  const int f = 2 * q;
+                  ar[cc][f] = fmaf(w.x, gr[f], ar[cc][f]);
+                  ar[cc][f] = fmaf(-w.y, gi[f], ar[cc][f]);
+                  ai[cc][f] = fmaf(w.x, gi[f], ai[cc][f]);
+                  ai[cc][f] = fmaf(w.y, gr[f], ai[cc][f]);
+                  if (f + 1 < P) {
+                    ar[cc][f + 1] = fmaf(w.z, gr[f + 1], ar[cc][f + 1]);
+                    ar[cc][f + 1] = fmaf(-w.w, gi[f + 1], ar[cc][f + 1]);
+                    ai[cc][f + 1] = fmaf(w.z, gi[f + 1], ai[cc][f + 1]);
+                    ai[cc][f + 1] = fmaf(w.w, gr[f + 1], ai[cc][f + 1]);
+                  }
+                }
+              }
+            }
           }
         }
+        __syncthreads();  // all lanes done with band / spectra before the next chunk
+        cp_async_commit();  // empty group: keeps wait_group 1 in out_channel exact
+#pragma unroll
+        for (int cc = 0; cc < CR; ++cc)
+          if (cc < nc) out_channel(c0 + cc, ar[cc], ai[cc]);
       }
-      done = p.Cout;
     }
+
+    // item end: publish everything, then finish the deferred channels
+    cp_async_wait_all();
     __syncthreads();
-    if (tid == 0) st_release(p.flags + item, done);
+    if (tid == 0) st_release(p.flags + item, p.Cout);
+    if (laneB && has_pred) {
+      wait_flag(pred_flag, p.Cout, lane, bmask);
+      for (int c = max(0, p.Cout - kRingDepth); c < p.Cout; ++c) {
+        float pend[TR > 0 ? TR : 1];
+        prefetch(c, pend);
+        finalize(c, pend);
+      }
+    }
   }
 }
 
 // ------------------------------------------------------------------ bwd_filter
+// Stage rows r0..r0+nrows of `nplanes` consecutive R×R planes (plane stride R·R), columns
+// [c0, c0+ncols), into dst[plane][row][ld] (zero outside).  Threads own (row-group,
+// column) pairs, so all threads issue copies even when ncols is small.
+__device__ __forceinline__ void stage_planes_rows(float* dst, int ld, const float* __restrict__ base,
+                                                  int nplanes, int R, int r0, int nrows, int c0,
+                                                  int ncols, int tid, int nthr) {
+  const int groups = max(1, nthr / ncols);
+  const int cc = tid % ncols, grp = tid / ncols;
+  if (grp >= groups) return;
+  const int q = c0 + cc;
+  const bool qok = q >= 0 && q < R;
+  const int total = nplanes * nrows;
+  for (int row = grp; row < total; row += groups) {
+    const int pl = row / nrows, rr = row - (row / nrows) * nrows;
+    const int r = r0 + rr;
+    const bool ok = qok && r >= 0 && r < R;
+    cp_async4(dst + row * ld + cc, ok ? base + ((size_t)pl * R + r) * R + q : base, ok);
+  }
+}
+
+// Shared memory: x window rows [CR][P][XW] floats | Ξ̂ for the item's tiles [Td][CR][P][H]
+// float2 | dy blocks of TCH tiles [2][KG][NN][DW] floats (double buffered) | twiddles.
 template <int NN, int CR>
 __global__ void __launch_bounds__(kMaxThreads, 1) oaa_bwd_filter_kernel(const FilterParams p) {
   constexpr int P = 2 * NN - 1, H = NN;
-  extern __shared__ float2 xs[];  // Ξ̂ chunk [TCH][CR][P][H]
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int kk = tid / H, f1 = tid - (tid / H) * H;
-  const int k = blockIdx.y * p.KG + kk;
-  const bool laneK = (kk < p.KG) && (k < p.K);
+  const int k0 = blockIdx.y * p.KG;
+  const int k = k0 + kk;
+  const int nk = min(p.KG, p.K - k0);
+  const bool laneK = kk < nk;
+  const int XW = p.XW, DW = p.DW;
+  const int dysz = p.KG * NN * DW;
+  float* xwin = reinterpret_cast<float*>(smem_raw);                        // [CR][P][XW]
+  float2* xs = reinterpret_cast<float2*>(xwin + CR * P * XW);              // [Td][CR][P][H]
+  float* dyb = reinterpret_cast<float*>(xs + (size_t)p.Td * CR * P * H);   // [2][KG][NN][DW]
+  float2* tw = reinterpret_cast<float2*>(dyb + 2 * dysz);                  // [P] (cos, sin)(2πm/P)
+  if (tid < P) {
+    float s, c;
+    sincospif(2.0f * (float)tid / (float)P, &s, &c);
+    tw[tid] = make_float2(c, s);
+  }
   float cf[NN], sf[NN];
 #pragma unroll
   for (int p1 = 0; p1 < NN; ++p1) {
@@ -323,6 +521,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) oaa_bwd_filter_kernel(const Fi
     sf[p1] = s;
   }
   const int items = p.B * p.Td;
+  const int w0 = p.off - (NN - 1);  // x-window origin relative to the dy block origin
+  const int nchunks = (p.Td + p.TCH - 1) / p.TCH;
   for (int c0 = 0; c0 < p.C; c0 += CR) {
     const int nc = min(CR, p.C - c0);
     float ar[CR][P], ai[CR][P];
@@ -332,58 +532,69 @@ __global__ void __launch_bounds__(kMaxThreads, 1) oaa_bwd_filter_kernel(const Fi
       for (int f2 = 0; f2 < P; ++f2) { ar[cc][f2] = 0.f; ai[cc][f2] = 0.f; }
     for (int item = blockIdx.x; item < items; item += p.G) {
       const int b = item / p.Td, t1 = item - (item / p.Td) * p.Td;
-      for (int tc0 = 0; tc0 < p.Td; tc0 += p.TCH) {
-        const int ntc = min(p.TCH, p.Td - tc0);
-        __syncthreads();
-        // x-window spectra: tasks (tile tt, channel cc, row fr)
-        const int ntask = ntc * nc * H;
-        for (int task = tid; task < ntask; task += nthr) {
-          const int fr = task % H;
-          const int cc = (task / H) % nc;
-          const int tt = task / (H * nc);
-          const int t2 = tc0 + tt;
-          const int r0 = t1 * NN + p.off - (NN - 1), q0 = t2 * NN + p.off - (NN - 1);
-          const float* xp = p.x + ((size_t)b * p.C + c0 + cc) * p.N * p.N;
-          float tcf[P], tsf[P];
+      const float* dyk = p.dy + ((size_t)b * p.K + k0) * p.M * p.M;
+      __syncthreads();  // previous item done with xwin / xs / dyb
+      // x rows of this item's windows (zero outside x) and the first dy chunk
+      for (int cc = 0; cc < nc; ++cc)
+        stage_rows(xwin + cc * P * XW, XW, p.x + ((size_t)b * p.C + c0 + cc) * p.N * p.N, p.N,
+                   t1 * NN + w0, P, w0, XW, tid, nthr);
+      stage_planes_rows(dyb, DW, dyk, nk, p.M, t1 * NN, NN, 0, min(p.TCH, p.Td) * NN, tid, nthr);
+      cp_async_commit();
+      cp_async_wait_all();
+      __syncthreads();
+      // Ξ̂ of every window of the item: tasks (tile t2, channel cc, row fr)
+      const int ntask = p.Td * nc * H;
+      for (int task = tid; task < ntask; task += nthr) {
+        const int fr = task % H;
+        const int cc = (task / H) % nc;
+        const int t2 = task / (H * nc);
+        const float* src = xwin + cc * P * XW + t2 * NN;
+        float tc[P], ts[P];
 #pragma unroll
-          for (int p1 = 0; p1 < P; ++p1) {
-            float s, c;
-            sincospif(2.0f * (float)((fr * p1) % P) / (float)P, &s, &c);
-            tcf[p1] = c;
-            tsf[p1] = s;
-          }
-          float rr[P], ri[P];
-#pragma unroll
-          for (int p2 = 0; p2 < P; ++p2) {
-            const int q = q0 + p2;
-            const bool qok = q >= 0 && q < p.N;
-            float a = 0.f, bb = 0.f;
-#pragma unroll
-            for (int p1 = 0; p1 < P; ++p1) {
-              const int r = r0 + p1;
-              const float v = (qok && r >= 0 && r < p.N) ? __ldg(xp + (size_t)r * p.N + q) : 0.f;
-              a = fmaf(v, tcf[p1], a);
-              bb = fmaf(-v, tsf[p1], bb);
-            }
-            rr[p2] = a;
-            ri[p2] = bb;
-          }
-          float xr[P], xi[P];
-          dft<P, -1>(rr, ri, xr, xi);
-          float2* dst = xs + ((size_t)(tt * CR + cc) * P) * H + fr;
-#pragma unroll
-          for (int f2 = 0; f2 < P; ++f2) dst[f2 * H] = make_float2(xr[f2], xi[f2]);
+        for (int p1 = 0; p1 < P; ++p1) {
+          const float2 t = tw[(fr * p1) % P];
+          tc[p1] = t.x;
+          ts[p1] = t.y;
         }
-        __syncthreads();
+        float rr[P], ri[P];
+#pragma unroll
+        for (int p2 = 0; p2 < P; ++p2) {
+          float a = src[p2], bb = 0.f;
+#pragma unroll
+          for (int p1 = 1; p1 < P; ++p1) {
+            const float v = src[p1 * XW + p2];
+            a = fmaf(v, tc[p1], a);
+            bb = fmaf(-v, ts[p1], bb);
+          }
+          rr[p2] = a;
+          ri[p2] = bb;
+        }
+        float xr[P], xi[P];
+        dft<P, -1>(rr, ri, xr, xi);
+        float2* dst = xs + ((size_t)(t2 * CR + cc) * P) * H + fr;
+#pragma unroll
+        for (int f2 = 0; f2 < P; ++f2) dst[f2 * H] = make_float2(xr[f2], xi[f2]);
+      }
+      // dy blocks, TCH tiles per chunk, the next chunk staged while this one computes
+      for (int ch = 0; ch < nchunks; ++ch) {
+        const int tc0 = ch * p.TCH;
+        const int ntc = min(p.TCH, p.Td - tc0);
+        cp_async_wait_all();
+        __syncthreads();  // chunk ch landed, Ξ̂ written, chunk ch−1's buffer free
+        if (ch + 1 < nchunks) {
+          const int t0n = tc0 + p.TCH;
+          stage_planes_rows(dyb + ((ch + 1) & 1) * dysz, DW, dyk, nk, p.M, t1 * NN, NN, t0n * NN,
+                            min(p.TCH, p.Td - t0n) * NN, tid, nthr);
+          cp_async_commit();
+        }
         if (laneK) {
-          const float* gp = p.dy + ((size_t)b * p.K + k) * p.M * p.M;
+          const float* db = dyb + (ch & 1) * dysz + kk * NN * DW;
           for (int tt = 0; tt < ntc; ++tt) {
-            const int t2 = tc0 + tt;
             float z[NN][NN];
-            load_block<NN>(gp, p.M, t1 * NN, t2 * NN, z);
+            read_block<NN>(db, DW, tt * NN, z);
             float gr[P], gi[P];
             block_row_spectrum<NN>(z, cf, sf, gr, gi);
-            const float2* src = xs + ((size_t)(tt * CR) * P) * H + f1;
+            const float2* src = xs + ((size_t)((tc0 + tt) * CR) * P) * H + f1;
 #pragma unroll
             for (int cc = 0; cc < CR; ++cc) {
               if (cc < nc) {
@@ -452,36 +663,42 @@ __global__ void oaa_filter_finalize_kernel(const float2* __restrict__ partial, f
   }
 }
 
-// spec[((a·Binner + bb)·P + f2)·H + f1] = DFT_P(w_kc or flip180(w_kc))[f1][f2] / P²,
-// (k, c) = loop_is_k ? (a, bb) : (bb, a).
-__global__ void oaa_spectrum_kernel(const float* __restrict__ w, float2* __restrict__ spec, int K,
+// spec4[((a·Binner + bb)·P2 + f2/2)·H + f1].{xy|zw} = DFT_P(w_kc or flip180(w_kc))[f1][f2] / P²
+// with (k, c) = loop_is_k ? (a, bb) : (bb, a); the odd last f2 slot is zero.
+__global__ void oaa_spectrum_kernel(const float* __restrict__ w, float4* __restrict__ spec, int K,
                                     int C, int n, int flip, int loop_is_k) {
-  const int P = 2 * n - 1, H = n;
-  const long total = (long)K * C * P * H;
+  const int P = 2 * n - 1, H = n, P2 = (P + 1) / 2;
+  const long total = (long)K * C * P2 * H;
   for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total;
        t += (long)gridDim.x * blockDim.x) {
     const int f1 = (int)(t % H);
-    const int f2 = (int)((t / H) % P);
-    const long ab = t / ((long)H * P);
+    const int q = (int)((t / H) % P2);
+    const long ab = t / ((long)H * P2);
     int k, c;
     if (loop_is_k) { k = (int)(ab / C); c = (int)(ab % C); }
     else { c = (int)(ab / K); k = (int)(ab % K); }
     const float* wk = w + ((size_t)k * C + c) * n * n;
-    double sr = 0.0, si = 0.0;
-    for (int p1 = 0; p1 < n; ++p1)
-      for (int p2 = 0; p2 < n; ++p2) {
-        const float v = flip ? wk[(n - 1 - p1) * n + (n - 1 - p2)] : wk[p1 * n + p2];
-        const int m = (f1 * p1 + f2 * p2) % P;
-        double s, cc;
-        sincospi(2.0 * (double)m / (double)P, &s, &cc);
-        sr += (double)v * cc;
-        si -= (double)v * s;
-      }
-    const double inv = 1.0 / ((double)P * (double)P);
-    spec[t] = make_float2((float)(sr * inv), (float)(si * inv));
+    double out[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int h = 0; h < 2; ++h) {
+      const int f2 = 2 * q + h;
+      if (f2 >= P) continue;
+      double sr = 0.0, si = 0.0;
+      for (int p1 = 0; p1 < n; ++p1)
+        for (int p2 = 0; p2 < n; ++p2) {
+          const float v = flip ? wk[(n - 1 - p1) * n + (n - 1 - p2)] : wk[p1 * n + p2];
+          const int m = (f1 * p1 + f2 * p2) % P;
+          double s, cc;
+          sincospi(2.0 * (double)m / (double)P, &s, &cc);
+          sr += (double)v * cc;
+          si -= (double)v * s;
+        }
+      const double inv = 1.0 / ((double)P * (double)P);
+      out[2 * h] = sr * inv;
+      out[2 * h + 1] = si * inv;
+    }
+    spec[t] = make_float4((float)out[0], (float)out[1], (float)out[2], (float)out[3]);
   }
 }
-
 #endif  // OAA_DEFINE_AUX_KERNELS
 
 }  // namespace oaa

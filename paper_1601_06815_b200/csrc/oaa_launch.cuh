@@ -14,13 +14,13 @@ namespace oaa_host {
 extern std::atomic<uint64_t> g_launches;
 
 struct EnginePlan {
-  int R, Ro, off, T, Cin, Cout, TS, nthreads, CR;
+  int R, Ro, off, T, Cin, Cout, TS, BW, nthreads, CR;
   bool S1;
   size_t smem;
 };
 
 struct FilterPlan {
-  int Td, KG, nkg, G, TCH, CR, nthreads;
+  int Td, KG, nkg, G, TCH, CR, nthreads, XW, DW;
   size_t smem;
 };
 

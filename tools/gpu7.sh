@@ -1,0 +1,5 @@
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "not slow" 2>&1 | tail -4
+for v in "" _build_oaa_exp_no_wait/liboaa.so; do
+  if [ -n "$v" ]; then export OAA_LIB=$PWD/paper_1601_06815_b200/$v; else unset OAA_LIB; fi
+  timeout 300 python tools/time_ops.py
+done
