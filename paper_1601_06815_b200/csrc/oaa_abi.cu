@@ -88,16 +88,6 @@ bool make_geo(int N, int n, oaa_crop_t crop, Geo* g) {
 constexpr int kCRMax = 4;
 
 
-int pick_TS(int T, int n) {
-  // stride (in float2) of the t2 index in the shared Q buffer, chosen so stage-A stores
-  // and stage-B loads (64-bit, two 16-lane phases) are (near) bank-conflict free:
-  // TS ≡ 16/n (mod 16).
-  int target = std::max(1, 16 / n) % 16;
-  int TS = T;
-  while ((TS % 16) != target) ++TS;
-  return TS;
-}
-
 bool plan_engine(int R, int Ro, int off, int n, int Cin, int Cout, EnginePlan* e) {
   e->R = R;
   e->Ro = Ro;
@@ -108,8 +98,9 @@ bool plan_engine(int R, int Ro, int off, int n, int Cin, int Cout, EnginePlan* e
   const int laneA = e->T * n;
   const int need = std::max(laneA, Ro);
   if (need > oaa::kMaxThreads) return false;
-  e->nthreads = cdiv(need, 32) * 32;
-  e->TS = pick_TS(e->T, n);
+  e->ncomp = cdiv(need, 32) * 32;
+  e->nthreads = e->ncomp + 32 <= oaa::kMaxThreads ? e->ncomp + 32 : e->ncomp;  // + publisher warp
+  e->TS = oaa::q_stride(n);
   e->BW = cdiv(e->T * n, 4) * 4;
   const int P = 2 * n - 1, H = n, P2 = (P + 1) / 2;
   if (Cin <= kCRMax) {
@@ -122,9 +113,10 @@ bool plan_engine(int R, int Ro, int off, int n, int Cin, int Cout, EnginePlan* e
   const int nsb = e->S1 ? 3 : 2;
   const int cin_s = e->S1 ? Cin : e->CR;
   const int nband = e->S1 ? Cin : 2;
-  e->smem = sizeof(float2) * 2 * ((size_t)H * P * e->TS + 2) + sizeof(float4) * (size_t)nsb * cin_s * P2 * H +
-            sizeof(float) * (size_t)nband * n * e->BW +
-            sizeof(float) * (size_t)oaa::kRingDepth * (n - 1) * e->nthreads;
+  const size_t band_b = sizeof(float) * (size_t)nband * n * e->BW;
+  const size_t ring_b = sizeof(float) * (size_t)oaa::kRingDepth * (n - 1) * oaa::kMaxThreads;
+  e->smem = sizeof(float2) * 2 * ((size_t)H * P * e->TS) + sizeof(float4) * (size_t)nsb * cin_s * P2 * H +
+            (e->S1 ? std::max(band_b, ring_b) : band_b + ring_b);
   return e->smem <= 220 * 1024;
 }
 
@@ -275,6 +267,7 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
   p.TS = e.TS;
   p.BW = e.BW;
   p.num_items = B * e.T;
+  p.ncomp = e.ncomp;
   ProfScope prof(is_fwd ? OAA_OP_FWD : OAA_OP_BWD_DATA, s);
   prof.start();
   cudaError_t err = launch_engine(n, p, e, s);

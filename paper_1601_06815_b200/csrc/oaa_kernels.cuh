@@ -35,6 +35,18 @@ namespace oaa {
 
 constexpr int kMaxThreads = 256;  // CTA size cap: max(T·n, Ro) ≤ 256 ⇒ N ≲ 250
 
+// Compile-time stride (in float2) of the tile index t2 in the shared Q buffer
+// Q[f1][p2][t2]: ≥ the largest T = kMaxThreads/n, and ≡ 16/n (mod 16) so stage-A
+// stores (lanes = (t2, f1)) and stage-B loads (lanes = consecutive output columns) of
+// 64-bit words are (near) bank-conflict free.  Shared by host planning and kernels.
+__host__ __device__ constexpr int q_stride(int n) {
+  int target = (16 / n) % 16;
+  if (target == 0) target = 16 % 16;
+  int ts = (kMaxThreads + n - 1) / n;
+  while ((ts % 16) != target) ++ts;
+  return ts;
+}
+
 struct EngineParams {
   const float* in;      // [B][Cin][R][R]
   const float4* spec;   // [Cloop][Cinner][P2][H] (f2 pairs; S1: loop=cout, S2: loop=cin)
@@ -42,6 +54,7 @@ struct EngineParams {
   int* flags;           // [B*T] progress of each work item (# output channels stored)
   int* counter;         // dynamic work-item counter
   int B, Cin, Cout, R, T, Ro, off, TS, BW, num_items;
+  int ncomp;            // compute threads; a trailing extra warp (if any) only publishes flags
 };
 
 struct FilterParams {
@@ -159,32 +172,30 @@ __device__ __forceinline__ void block_row_spectrum(const float (&z)[NN][NN], con
 // the shared Q buffer  Q[f1][p2][t2]  (complex, float2).
 template <int NN>
 __device__ __forceinline__ void stage_a_store(const float (&yr)[2 * NN - 1], const float (&yi)[2 * NN - 1],
-                                              float2* __restrict__ Q, int f1, int t2, int TS) {
-  constexpr int P = 2 * NN - 1;
+                                              float2* __restrict__ Qlane) {
+  constexpr int P = 2 * NN - 1, TS = q_stride(NN);
   float qr[P], qi[P];
   dft<P, +1>(yr, yi, qr, qi);
 #pragma unroll
-  for (int p2 = 0; p2 < P; ++p2) Q[(f1 * P + p2) * TS + t2] = make_float2(qr[p2], qi[p2]);
+  for (int p2 = 0; p2 < P; ++p2) Qlane[p2 * TS] = make_float2(qr[p2], qi[p2]);
 }
 
 // Stage-B lane geometry for output column J (Full-frame coordinate): the two block
-// columns that land on it (block tA at p2 = pA, block tA−1 at p2 = pA + n) as float2
-// offsets into a Q buffer; an absent contributor points at the buffer's zero slot with
-// stride 0, so the loads are branch-free.
+// columns that land on it -- block tA at p2 = pA and block tA−1 at p2 = pA + n -- as
+// float2 offsets into a Q buffer, with validity flags.
 struct ColGeo {
-  int offA, strA, offB, strB;
+  int offA, offB;
+  bool vA, vB;
 };
 template <int NN>
-__device__ __forceinline__ ColGeo col_geo(int J, int T, int TS, int qzero) {
-  constexpr int P = 2 * NN - 1;
+__device__ __forceinline__ ColGeo col_geo(int J, int T) {
+  constexpr int TS = q_stride(NN);
   const int tA = J / NN, pA = J - tA * NN;
-  const bool vA = tA < T;
-  const bool vB = (tA >= 1) && (pA <= NN - 2);
   ColGeo g;
-  g.offA = vA ? pA * TS + tA : qzero;
-  g.strA = vA ? P * TS : 0;
-  g.offB = vB ? (pA + NN) * TS + tA - 1 : qzero;
-  g.strB = vB ? P * TS : 0;
+  g.vA = tA < T;
+  g.vB = (tA >= 1) && (pA <= NN - 2);
+  g.offA = g.vA ? pA * TS + tA : 0;
+  g.offB = g.vB ? (pA + NN) * TS + tA - 1 : 0;
   return g;
 }
 
@@ -193,34 +204,50 @@ __device__ __forceinline__ ColGeo col_geo(int J, int T, int TS, int qzero) {
 template <int NN>
 __device__ __forceinline__ void stage_b_column(const float2* __restrict__ Q, const ColGeo& g,
                                                float (&y)[2 * NN - 1]) {
-  constexpr int P = 2 * NN - 1, H = NN;
+  constexpr int P = 2 * NN - 1, H = NN, TS = q_stride(NN);
   float zr[H], zi[H];
   const float2* qa = Q + g.offA;
   const float2* qb = Q + g.offB;
 #pragma unroll
   for (int f1 = 0; f1 < H; ++f1) {
-    const float2 a = qa[f1 * g.strA];
-    const float2 b = qb[f1 * g.strB];
+    const float2 a = g.vA ? qa[f1 * P * TS] : make_float2(0.f, 0.f);
+    const float2 b = g.vB ? qb[f1 * P * TS] : make_float2(0.f, 0.f);
     zr[f1] = a.x + b.x;
     zi[f1] = a.y + b.y;
   }
   c2r_half<P>(zr, zi, y);
 }
 
-constexpr int kRingDepth = 8;   // deferred output channels per stage-B lane (smem ring)
-constexpr int kPublishEvery = 4;  // progress-flag granularity (output channels)
+#ifndef OAA_RING_DEPTH
+#define OAA_RING_DEPTH 12
+#endif
+#ifndef OAA_PUBLISH_EVERY
+#define OAA_PUBLISH_EVERY 8
+#endif
+constexpr int kRingDepth = OAA_RING_DEPTH;      // deferred output channels per stage-B lane (smem ring)
+constexpr int kPublishEvery = OAA_PUBLISH_EVERY;  // progress-flag granularity (output channels)
+static_assert(kRingDepth > kPublishEvery, "ring must cover the publication lag");
 
-// Poll (one lane per warp) until the predecessor item published ≥ need channels.  The
-// data that follows is read with ld.global.cg (L2, the point of coherence), so no L1
+// Wait (one lane per warp polls) until the predecessor item published ≥ need channels.
+// `seen` caches the last observed value (warp-uniform) and `inflight` is a value loaded
+// one iteration earlier, so in the steady state no poll latency is exposed.  The data
+// that follows is read with ld.global.cg (L2, the point of coherence), so no L1
 // invalidation (acquire / fence) is needed on this path.
-__device__ __forceinline__ void wait_flag(const int* flag, int need, int lane, unsigned mask) {
+__device__ __forceinline__ void wait_flag(const int* flag, int need, int lane, int leader,
+                                          unsigned mask, int& seen, int inflight) {
 #ifdef OAA_EXP_NO_WAIT
   return;
 #endif
-  if (lane == (__ffs(mask) - 1)) {
-    while (ld_relaxed(flag) < need) __nanosleep(32);
+  if (seen >= need) return;
+  seen = max(seen, __shfl_sync(mask, inflight, leader));
+  while (seen < need) {
+    int v = 0;
+    if (lane == leader) {
+      v = ld_relaxed(flag);
+      if (v < need) __nanosleep(64);
+    }
+    seen = __shfl_sync(mask, v, leader);
   }
-  __syncwarp(mask);
 }
 
 // ------------------------------------------------------------------ engine
@@ -228,41 +255,41 @@ __device__ __forceinline__ void wait_flag(const int* flag, int need, int lane, u
 // float4 | staged input rows [S1: Cin | S2: 2][n][BW] floats | top-row ring
 // [kRingDepth][n−1][nthr] floats.
 template <int NN, int CR, bool S1>
-__global__ void __launch_bounds__(kMaxThreads, 1) oaa_engine_kernel(const EngineParams p) {
+#ifndef OAA_ENGINE_MINB
+#define OAA_ENGINE_MINB 1
+#endif
+__global__ void __launch_bounds__(kMaxThreads, OAA_ENGINE_MINB) oaa_engine_kernel(const EngineParams p) {
   constexpr int P = 2 * NN - 1, H = NN, P2 = (P + 1) / 2, TR = NN - 1;
   constexpr int NSB = S1 ? 3 : 2;  // spectrum buffers
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_item;
-  const int TS = p.TS, BW = p.BW;
+  constexpr int TS = q_stride(NN);
+  constexpr int RS = kMaxThreads;                  // ring stride (floats per ring row)
+  const int BW = p.BW;
   const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
-  const int qsz = H * P * TS + 2;                  // float2 per Q buffer (+ zero slot, pad)
+  constexpr int qsz = H * P * TS;                  // float2 per Q buffer
   const int CIN_S = S1 ? p.Cin : CR;               // inner channels per spectrum buffer
   const int ssz = CIN_S * P2 * H;                  // float4 per spectrum buffer
   float2* Qs = reinterpret_cast<float2*>(smem_raw);
   float4* Ss = reinterpret_cast<float4*>(Qs + 2 * qsz);
   float* band = reinterpret_cast<float*>(Ss + NSB * ssz);
   const int bandsz = NN * BW;                      // floats per staged channel
-  float* ring = band + (S1 ? p.Cin : 2) * bandsz;  // [kRingDepth][TR][nthr]
-  if (tid == 0) {
-    Qs[qsz - 2] = make_float2(0.f, 0.f);
-    Qs[2 * qsz - 2] = make_float2(0.f, 0.f);
-  }
+  // S1 reads the staged rows only at item start, when the ring is empty: they share space
+  float* ring = S1 ? band : band + 2 * bandsz;     // [kRingDepth][TR][RS]
 
   // stage A lane = (t2, f1)
   const int a_t = tid / H, a_f1 = tid - (tid / H) * H;
-  const bool laneA = a_t < p.T;
-  float cf[NN], sf[NN];
-#pragma unroll
-  for (int p1 = 0; p1 < NN; ++p1) {
-    float s, c;
-    sincospif(2.0f * (float)((a_f1 * p1) % P) / (float)P, &s, &c);
-    cf[p1] = c;
-    sf[p1] = s;
-  }
+  const bool comp = tid < p.ncomp;                 // compute lane (else: publisher warp)
+  const bool laneA = comp && a_t < p.T;
+  const int a_qoff = a_f1 * P * TS + a_t;          // this lane's Q[f1][0][t2]
+  // The release that publishes progress costs a full memory fence; a dedicated warp
+  // with no stores of its own issues it, so the compute warps never wait on it.
+  const int pub_tid = (nthr > p.ncomp) ? p.ncomp : 0;
   // stage B lane = output column j
-  const bool laneB = tid < p.Ro;
+  const bool laneB = comp && tid < p.Ro;
   const unsigned bmask = __ballot_sync(0xffffffffu, laneB);
-  const ColGeo cg = col_geo<NN>(tid + p.off, p.T, TS, qsz - 2);
+  const int leader = bmask ? __ffs(bmask) - 1 : 0;
+  const ColGeo cg = col_geo<NN>(tid + p.off, p.T);
   const size_t plane_sz = (size_t)p.Ro * p.Ro;
 
   for (;;) {
@@ -276,6 +303,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) oaa_engine_kernel(const Engine
     const int* pred_flag = p.flags + item - 1;
     const float* in_b = p.in + (size_t)b * p.Cin * p.R * p.R;
     const int I0 = t1 * NN - p.off;  // output row of block row p1 = 0
+    int seen = 0, inflight = 0;      // predecessor progress (see wait_flag)
     // rows of this tile row inside the output window, as a bit mask over p1
     unsigned rows = 0;
 #pragma unroll
@@ -288,10 +316,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) oaa_engine_kernel(const Engine
     // finish the top rows of output channel c: predecessor's partial rows + ours
     auto finalize = [&](int c, const float (&pend)[TR > 0 ? TR : 1]) {
       float* cp = colp + (size_t)c * plane_sz;
-      const float* rg = ring + (c % kRingDepth) * TR * nthr + tid;
+      const float* rg = ring + (c % kRingDepth) * TR * RS + tid;
 #pragma unroll
       for (int p1 = 0; p1 < TR; ++p1)
-        if ((rows >> p1) & 1u) __stcs(cp + (ptrdiff_t)p1 * p.Ro, pend[p1] + rg[p1 * nthr]);
+        if ((rows >> p1) & 1u) __stcs(cp + (ptrdiff_t)p1 * p.Ro, pend[p1] + rg[p1 * RS]);
     };
     auto prefetch = [&](int c, float (&pend)[TR > 0 ? TR : 1]) {
       const float* cp = colp + (size_t)c * plane_sz;
@@ -300,42 +328,62 @@ __global__ void __launch_bounds__(kMaxThreads, 1) oaa_engine_kernel(const Engine
         pend[p1] = ((rows >> p1) & 1u) ? __ldcg(cp + (ptrdiff_t)p1 * p.Ro) : 0.f;
     };
 
-    // per output channel: stage A (given this lane's row spectrum yr/yi), barrier,
-    // publish, stage B with the deferred overlap-add.
-    auto out_channel = [&](int co, const float (&yr)[P], const float (&yi)[P]) {
-      float2* Q = Qs + (co & 1) * qsz;
-      float pend[TR > 0 ? TR : 1];
-      const bool fin = laneB && has_pred && co >= kRingDepth;
+    // Stage B of output channel cb, split so that it can be software-pipelined against
+    // stage A of the next channel:  pre_b (before the barrier-delimited block) waits for
+    // the predecessor and prefetches the partial rows channel cb − kRingDepth will be
+    // added onto; do_b stores this tile row's rows of channel cb, parks its top rows in
+    // the ring and finalises channel cb − kRingDepth.
+    const unsigned rowsB = laneB ? rows : 0u;
+    auto pre_b = [&](int cb, float (&pend)[TR > 0 ? TR : 1]) -> bool {
+      const bool fin = laneB && has_pred && cb >= kRingDepth;
       if (fin) {
-        wait_flag(pred_flag, co - kRingDepth + 1, lane, bmask);
-        prefetch(co - kRingDepth, pend);
+        wait_flag(pred_flag, cb - kRingDepth + 1, lane, leader, bmask, seen, inflight);
+        prefetch(cb - kRingDepth, pend);
       }
-      if (laneA) stage_a_store<NN>(yr, yi, Q, a_f1, a_t, TS);
-      cp_async_wait_1();  // all but the newest group (the spectrum prefetch for co+2)
+      return fin;
+    };
+    auto do_b = [&](int cb, bool fin, const float (&pend)[TR > 0 ? TR : 1]) {
+      float y[P];
+      stage_b_column<NN>(Qs + (cb & 1) * qsz, cg, y);
+      float* cp = colp + (size_t)cb * plane_sz;
+#pragma unroll
+      for (int p1 = TR; p1 < P; ++p1) {
+        if ((rowsB >> p1) & 1u) {
+          if (p1 >= NN) __stcg(cp + (ptrdiff_t)p1 * p.Ro, y[p1]);   // partial: the next tile row adds
+          else __stcs(cp + (ptrdiff_t)p1 * p.Ro, y[p1]);           // final
+        }
+      }
+      // The partial rows of channels < cb+1 are published at the next barrier when
+      // cb+1 is a publication point: every thread that stored them fences first
+      // (bar.sync alone does not make other warps' global stores visible device-wide).
+      if (((cb + 1) % kPublishEvery) == 0 && rowsB) __threadfence();
+      if (!has_pred) {
+#pragma unroll
+        for (int p1 = 0; p1 < TR; ++p1)
+          if ((rowsB >> p1) & 1u) __stcs(cp + (ptrdiff_t)p1 * p.Ro, y[p1]);
+      } else {
+        if (fin) finalize(cb - kRingDepth, pend);
+        float* rg = ring + (cb % kRingDepth) * TR * RS + tid;
+#pragma unroll
+        for (int p1 = 0; p1 < TR; ++p1) rg[p1 * RS] = y[p1];
+        // issue the next flag read now; it is consumed an iteration later
+        if (laneB && lane == leader && seen < cb + 2 - kRingDepth + kPublishEvery)
+          inflight = ld_relaxed(pred_flag);
+      }
+    };
+    // barrier; afterwards channels [0, done) have their bottom rows stored by everyone
+    auto sync_publish = [&](int done) {
+      cp_async_wait_1();  // all but the newest group (the spectrum prefetch two channels ahead)
       __syncthreads();
-      if (tid == 0 && co > 0 && (co % kPublishEvery) == 0) st_release(p.flags + item, co);
-      if (laneB) {
-        float y[P];
-        stage_b_column<NN>(Q, cg, y);
-        float* cp = colp + (size_t)co * plane_sz;
-#pragma unroll
-        for (int p1 = TR; p1 < P; ++p1) {
-          if ((rows >> p1) & 1u) {
-            if (p1 >= NN) __stcg(cp + (ptrdiff_t)p1 * p.Ro, y[p1]);   // partial: the next tile row adds
-            else __stcs(cp + (ptrdiff_t)p1 * p.Ro, y[p1]);           // final
-          }
-        }
-        if (!has_pred) {
-#pragma unroll
-          for (int p1 = 0; p1 < TR; ++p1)
-            if ((rows >> p1) & 1u) __stcs(cp + (ptrdiff_t)p1 * p.Ro, y[p1]);
-        } else {
-          if (fin) finalize(co - kRingDepth, pend);
-          float* rg = ring + (co % kRingDepth) * TR * nthr + tid;
-#pragma unroll
-          for (int p1 = 0; p1 < TR; ++p1) rg[p1 * nthr] = y[p1];
-        }
-      }
+      if (tid == pub_tid && done > 0 && (done % kPublishEvery) == 0) st_release(p.flags + item, done);
+    };
+    // unpipelined channel (S2): stage A, barrier, stage B
+    auto out_channel = [&](int co, const float (&yr)[P], const float (&yi)[P]) {
+      float pend[TR > 0 ? TR : 1];
+      const bool fin = pre_b(co, pend);
+      if (laneA) stage_a_store<NN>(yr, yi, Qs + (co & 1) * qsz + a_qoff);
+      sync_publish(co);
+      if (laneB) do_b(co, fin, pend);
     };
 
     if constexpr (S1) {
@@ -348,7 +396,19 @@ __global__ void __launch_bounds__(kMaxThreads, 1) oaa_engine_kernel(const Engine
       cp_async_wait_all();
       __syncthreads();
       float xr[CR][P], xi[CR][P];
+#pragma unroll
+      for (int c = 0; c < CR; ++c)
+#pragma unroll
+        for (int f2 = 0; f2 < P; ++f2) { xr[c][f2] = 0.f; xi[c][f2] = 0.f; }
       if (laneA) {
+        float cf[NN], sf[NN];  // this lane's column twiddles e^{−iθ f1 p1}
+#pragma unroll
+        for (int p1 = 0; p1 < NN; ++p1) {
+          float s, c;
+          sincospif(2.0f * (float)((a_f1 * p1) % P) / (float)P, &s, &c);
+          cf[p1] = c;
+          sf[p1] = s;
+        }
 #pragma unroll
         for (int c = 0; c < CR; ++c) {
           if (c < p.Cin) {
@@ -358,42 +418,79 @@ __global__ void __launch_bounds__(kMaxThreads, 1) oaa_engine_kernel(const Engine
           }
         }
       }
-      for (int co = 0; co < p.Cout; ++co) {
+      __syncthreads();  // staged rows consumed: the ring may now overwrite them
+      // stage A of channel co for this lane (every lane runs it: lanes past the last
+      // tile write unused Q columns), plus the spectrum prefetch two channels ahead
+      auto stage_a = [&](int co) {
         float yr[P], yi[P];
-        if (laneA) {
+        const float4* S = Ss + (co % NSB) * ssz + a_f1;
 #pragma unroll
-          for (int f2 = 0; f2 < P; ++f2) { yr[f2] = 0.f; yi[f2] = 0.f; }
-          const float4* S = Ss + (co % NSB) * ssz + a_f1;
+        for (int c = 0; c < CR; ++c) {
+          if (c < p.Cin) {
 #pragma unroll
-          for (int c = 0; c < CR; ++c) {
-            if (c < p.Cin) {
-#pragma unroll
-              for (int q = 0; q < P2; ++q) {
-                const float4 w = S[(c * P2 + q) * H];
-                const int f = 2 * q;
+            for (int q = 0; q < P2; ++q) {
+              const float4 w = S[(c * P2 + q) * H];
+              const int f = 2 * q;
+              if (c == 0) {
+                yr[f] = w.x * xr[c][f];
+                yi[f] = w.x * xi[c][f];
+              } else {
                 yr[f] = fmaf(w.x, xr[c][f], yr[f]);
-                yr[f] = fmaf(-w.y, xi[c][f], yr[f]);
                 yi[f] = fmaf(w.x, xi[c][f], yi[f]);
-                yi[f] = fmaf(w.y, xr[c][f], yi[f]);
-                if (f + 1 < P) {
+              }
+              yr[f] = fmaf(-w.y, xi[c][f], yr[f]);
+              yi[f] = fmaf(w.y, xr[c][f], yi[f]);
+              if (f + 1 < P) {
+                if (c == 0) {
+                  yr[f + 1] = w.z * xr[c][f + 1];
+                  yi[f + 1] = w.z * xi[c][f + 1];
+                } else {
                   yr[f + 1] = fmaf(w.z, xr[c][f + 1], yr[f + 1]);
-                  yr[f + 1] = fmaf(-w.w, xi[c][f + 1], yr[f + 1]);
                   yi[f + 1] = fmaf(w.z, xi[c][f + 1], yi[f + 1]);
-                  yi[f + 1] = fmaf(w.w, xr[c][f + 1], yi[f + 1]);
                 }
+                yr[f + 1] = fmaf(-w.w, xi[c][f + 1], yr[f + 1]);
+                yi[f + 1] = fmaf(w.w, xr[c][f + 1], yi[f + 1]);
               }
             }
           }
         }
-        // prefetch the spectrum of channel co+2 (its buffer was last read before the
-        // previous barrier)
+        stage_a_store<NN>(yr, yi, Qs + (co & 1) * qsz + a_qoff);
+      };
+      // spectrum prefetch two channels ahead (all threads, publisher warp included)
+      auto prefetch_spec = [&](int co) {
         if (co + 2 < p.Cout)
           for (int e = tid; e < ssz; e += nthr)
             cp_async16(Ss + ((co + 2) % NSB) * ssz + e, p.spec + (size_t)(co + 2) * ssz + e);
         cp_async_commit();  // always (possibly empty) so wait_group 1 keeps its meaning
-        out_channel(co, yr, yi);
+      };
+      // software pipeline: stage A of channel it overlaps stage B of channel it−1
+      if (comp) stage_a(0);
+      prefetch_spec(0);
+      sync_publish(0);
+      for (int it = 1; it < p.Cout; ++it) {
+        if (comp) {
+          float pend[TR > 0 ? TR : 1];
+          const bool fin = pre_b(it - 1, pend);
+          stage_a(it);
+          do_b(it - 1, fin, pend);
+        }
+        prefetch_spec(it);
+        sync_publish(it);
+      }
+      if (comp) {
+        float pend[TR > 0 ? TR : 1];
+        const bool fin = pre_b(p.Cout - 1, pend);
+        do_b(p.Cout - 1, fin, pend);
       }
     } else {
+      float cf[NN], sf[NN];  // this lane's column twiddles e^{−iθ f1 p1}
+#pragma unroll
+      for (int p1 = 0; p1 < NN; ++p1) {
+        float s, c;
+        sincospif(2.0f * (float)((a_f1 * p1) % P) / (float)P, &s, &c);
+        cf[p1] = c;
+        sf[p1] = s;
+      }
       for (int c0 = 0; c0 < p.Cout; c0 += CR) {
         const int nc = min(CR, p.Cout - c0);
         const int ssz_c = nc * P2 * H;
@@ -454,11 +551,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1) oaa_engine_kernel(const Engine
     }
 
     // item end: publish everything, then finish the deferred channels
+    if (laneB) __threadfence();
     cp_async_wait_all();
     __syncthreads();
-    if (tid == 0) st_release(p.flags + item, p.Cout);
+    if (tid == pub_tid) st_release(p.flags + item, p.Cout);
     if (laneB && has_pred) {
-      wait_flag(pred_flag, p.Cout, lane, bmask);
+      wait_flag(pred_flag, p.Cout, lane, leader, bmask, seen, inflight);
       for (int c = max(0, p.Cout - kRingDepth); c < p.Cout; ++c) {
         float pend[TR > 0 ? TR : 1];
         prefetch(c, pend);

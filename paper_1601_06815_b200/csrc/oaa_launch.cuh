@@ -14,7 +14,7 @@ namespace oaa_host {
 extern std::atomic<uint64_t> g_launches;
 
 struct EnginePlan {
-  int R, Ro, off, T, Cin, Cout, TS, BW, nthreads, CR;
+  int R, Ro, off, T, Cin, Cout, TS, BW, nthreads, ncomp, CR;
   bool S1;
   size_t smem;
 };

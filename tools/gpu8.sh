@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:oaa_engine -s 0 -c 1 -o gpurun_out/prof_fwd_r1c python tools/prof_step.py 1 fwd 2>&1 | tail -1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:oaa_engine -s 0 -c 1 -o gpurun_out/prof_bwd_r1c python tools/prof_step.py 1 bwd_data 2>&1 | tail -1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:oaa_bwd_filter -s 0 -c 1 -o gpurun_out/prof_bwf_r1c python tools/prof_step.py 1 bwd_filter 2>&1 | tail -1
