@@ -115,8 +115,9 @@ bool plan_engine(int R, int Ro, int off, int n, int Cin, int Cout, EnginePlan* e
   const int nband = e->S1 ? Cin : 2;
   const size_t band_b = sizeof(float) * (size_t)nband * n * e->BW;
   const size_t ring_b = sizeof(float) * (size_t)oaa::kRingDepth * (n - 1) * oaa::kMaxThreads;
+  // S1 runs the TMEM engine (spectra and deferred rows in tensor memory, no smem ring)
   e->smem = sizeof(float2) * 2 * ((size_t)H * P * e->TS) + sizeof(float4) * (size_t)nsb * cin_s * P2 * H +
-            (e->S1 ? std::max(band_b, ring_b) : band_b + ring_b);
+            (e->S1 ? band_b : band_b + ring_b);
   return e->smem <= 220 * 1024;
 }
 

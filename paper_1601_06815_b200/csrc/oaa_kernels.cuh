@@ -42,7 +42,7 @@ constexpr int kMaxThreads = 256;  // CTA size cap: max(TÂ·n, Ro) â‰¤ 256 â‡’ N â
 __host__ __device__ constexpr int q_stride(int n) {
   int target = (16 / n) % 16;
   if (target == 0) target = 16 % 16;
-  int ts = (kMaxThreads + n - 1) / n;
+  int ts = (kMaxThreads + n - 1) / n + 1;  // + â‰¥1 always-zero column (see col_geo)
   while ((ts % 16) != target) ++ts;
   return ts;
 }
@@ -70,6 +70,10 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
   asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// Release fence at GPU scope: prior writes of this thread become visible device-wide
+// before its later writes (MEMBAR.ALL.GPU; unlike fence_release() it is not SC and does
+// not invalidate L1).
+__device__ __forceinline__ void fence_release() { asm volatile("fence.release.gpu;" ::: "memory"); }
 __device__ __forceinline__ void st_release(int* p, int v) {
 #ifdef OAA_EXP_RELAXED_PUBLISH
   asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -183,20 +187,31 @@ __device__ __forceinline__ void stage_a_store(const float (&yr)[2 * NN - 1], con
 // Stage-B lane geometry for output column J (Full-frame coordinate): the two block
 // columns that land on it -- block tA at p2 = pA and block tAâˆ’1 at p2 = pA + n -- as
 // float2 offsets into a Q buffer, with validity flags.
+// An absent contributor reads column T of the Q buffer, which is kept zero
+// (zero_q_tail), so the loads need no predicates.
 struct ColGeo {
   int offA, offB;
-  bool vA, vB;
 };
 template <int NN>
 __device__ __forceinline__ ColGeo col_geo(int J, int T) {
   constexpr int TS = q_stride(NN);
   const int tA = J / NN, pA = J - tA * NN;
   ColGeo g;
-  g.vA = tA < T;
-  g.vB = (tA >= 1) && (pA <= NN - 2);
-  g.offA = g.vA ? pA * TS + tA : 0;
-  g.offB = g.vB ? (pA + NN) * TS + tA - 1 : 0;
+  g.offA = (tA < T) ? pA * TS + tA : pA * TS + T;
+  g.offB = (tA >= 1 && pA <= NN - 2) ? (pA + NN) * TS + tA - 1 : pA * TS + T;
   return g;
+}
+// Zero the unused tile columns [T, TS) of both Q buffers (stage A never writes them
+// with non-zero data).
+template <int NN>
+__device__ __forceinline__ void zero_q_tail(float2* Qs, int qsz, int T, int tid, int nthr) {
+  constexpr int P = 2 * NN - 1, H = NN, TS = q_stride(NN);
+  const int w = TS - T, tot = 2 * H * P * w;
+  for (int e = tid; e < tot; e += nthr) {
+    const int c = e % w, row = e / w;  // row = bufÂ·HÂ·P + f1Â·P + p2
+    const int buf = row / (H * P), rr = row - buf * (H * P);
+    Qs[buf * qsz + rr * TS + T + c] = make_float2(0.f, 0.f);
+  }
 }
 
 // Sum the two block columns and apply the Hermitian inverse along f1 (c2r): y[p1] is
@@ -210,8 +225,8 @@ __device__ __forceinline__ void stage_b_column(const float2* __restrict__ Q, con
   const float2* qb = Q + g.offB;
 #pragma unroll
   for (int f1 = 0; f1 < H; ++f1) {
-    const float2 a = g.vA ? qa[f1 * P * TS] : make_float2(0.f, 0.f);
-    const float2 b = g.vB ? qb[f1 * P * TS] : make_float2(0.f, 0.f);
+    const float2 a = qa[f1 * P * TS];
+    const float2 b = qb[f1 * P * TS];
     zr[f1] = a.x + b.x;
     zi[f1] = a.y + b.y;
   }
@@ -276,6 +291,7 @@ __global__ void __launch_bounds__(kMaxThreads, OAA_ENGINE_MINB) oaa_engine_kerne
   const int bandsz = NN * BW;                      // floats per staged channel
   // S1 reads the staged rows only at item start, when the ring is empty: they share space
   float* ring = S1 ? band : band + 2 * bandsz;     // [kRingDepth][TR][RS]
+  zero_q_tail<NN>(Qs, qsz, p.T, tid, nthr);
 
   // stage A lane = (t2, f1)
   const int a_t = tid / H, a_f1 = tid - (tid / H) * H;
@@ -356,7 +372,7 @@ __global__ void __launch_bounds__(kMaxThreads, OAA_ENGINE_MINB) oaa_engine_kerne
       // The partial rows of channels < cb+1 are published at the next barrier when
       // cb+1 is a publication point: every thread that stored them fences first
       // (bar.sync alone does not make other warps' global stores visible device-wide).
-      if (((cb + 1) % kPublishEvery) == 0 && rowsB) __threadfence();
+      if (((cb + 1) % kPublishEvery) == 0 && rowsB) fence_release();
       if (!has_pred) {
 #pragma unroll
         for (int p1 = 0; p1 < TR; ++p1)
@@ -551,7 +567,7 @@ __global__ void __launch_bounds__(kMaxThreads, OAA_ENGINE_MINB) oaa_engine_kerne
     }
 
     // item end: publish everything, then finish the deferred channels
-    if (laneB) __threadfence();
+    if (laneB) fence_release();
     cp_async_wait_all();
     __syncthreads();
     if (tid == pub_tid) st_release(p.flags + item, p.Cout);
@@ -564,6 +580,317 @@ __global__ void __launch_bounds__(kMaxThreads, OAA_ENGINE_MINB) oaa_engine_kerne
       }
     }
   }
+}
+
+// ------------------------------------------------------------------ TMEM helpers
+// Each thread owns one TMEM lane (32Â·(warp % 4) + lane) and reads / writes consecutive
+// 32-bit columns of it (shape 32x32b).  All tcgen05 ops are warp-collective.
+__device__ __forceinline__ void tmem_ld16(uint32_t ta, float* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]),
+        "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
+      : "r"(ta));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t ta, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]));
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t ta, float* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "r"(ta));
+}
+__device__ __forceinline__ void tmem_st8(uint32_t ta, const float* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta), "f"(v[0]),
+               "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// TMEM columns per thread of the S1 engine: the input row spectra (CR channels, 2P
+// floats each, in whole 16-column loads) + the deferred top rows (kTRing channels Ã— 8).
+constexpr int kTRing = 4;     // deferred channels per lane (TMEM ring)
+constexpr int kTPublish = 2;  // progress published every kTPublish channels, one channel late
+static_assert(kTRing >= kTPublish + 2, "ring must cover the publication lag");
+__host__ __device__ constexpr int s1t_xcols(int n) { return ((2 * (2 * n - 1) + 15) / 16) * 16; }
+__host__ __device__ constexpr int s1t_cols_per_thread(int n, int cr) { return cr * s1t_xcols(n) + kTRing * 8; }
+// columns allocated per CTA: two warps share every TMEM lane (8 warps / 4 quadrants)
+__host__ __device__ constexpr int s1t_alloc_cols(int n, int cr) {
+  return (2 * s1t_cols_per_thread(n, cr) <= 32) ? 32 : (2 * s1t_cols_per_thread(n, cr) <= 64) ? 64
+       : (2 * s1t_cols_per_thread(n, cr) <= 128) ? 128 : (2 * s1t_cols_per_thread(n, cr) <= 256) ? 256 : 512;
+}
+
+// ------------------------------------------------------------------ S1 engine, TMEM
+// Input-stationary engine (forward at small C) with the per-lane input row spectra and
+// the deferred overlap rows held in tensor memory instead of registers, so two CTAs
+// (16 warps) fit on an SM.  Same algorithm and protocol as oaa_engine_kernel<.., S1>.
+// Shared memory: Q[2][H][P][TS] float2 | spectra[3][Cin][P2][H] float4 | staged rows.
+template <int NN, int CR>
+__global__ void __launch_bounds__(kMaxThreads, 2) oaa_engine_s1t_kernel(const EngineParams p) {
+  constexpr int P = 2 * NN - 1, H = NN, P2 = (P + 1) / 2, TR = NN - 1;
+  constexpr int NSB = 3;
+  constexpr int TS = q_stride(NN);
+  constexpr int XC = s1t_xcols(NN);                 // TMEM columns per channel
+  constexpr int NX16 = XC / 16;
+  constexpr int RING0 = CR * XC;                    // first ring column
+  constexpr int ACOLS = s1t_alloc_cols(NN, CR);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int s_item;
+  __shared__ uint32_t s_tmem;
+  const int BW = p.BW;
+  const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int qsz = H * P * TS;
+  const int ssz = p.Cin * P2 * H;
+  float2* Qs = reinterpret_cast<float2*>(smem_raw);
+  float4* Ss = reinterpret_cast<float4*>(Qs + 2 * qsz);
+  float* band = reinterpret_cast<float*>(Ss + NSB * ssz);
+  const int bandsz = NN * BW;
+  zero_q_tail<NN>(Qs, qsz, p.T, tid, nthr);
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&s_tmem)),
+                 "n"(ACOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tbase = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) & 1) * (ACOLS / 2);
+
+  const int a_t = tid / H, a_f1 = tid - (tid / H) * H;
+  const bool comp = tid < p.ncomp;
+  const bool laneA = comp && a_t < p.T;
+  const int a_qoff = a_f1 * P * TS + a_t;
+  const int pub_tid = (nthr > p.ncomp) ? p.ncomp : 0;
+  const bool laneB = comp && tid < p.Ro;
+  const unsigned bmask = __ballot_sync(0xffffffffu, laneB);
+  const int leader = bmask ? __ffs(bmask) - 1 : 0;
+  const ColGeo cg = col_geo<NN>(tid + p.off, p.T);
+  const size_t plane_sz = (size_t)p.Ro * p.Ro;
+
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_item = atomicAdd(p.counter, 1);
+    __syncthreads();
+    const int item = s_item;
+    if (item >= p.num_items) break;
+    const int b = item / p.T, t1 = item - (item / p.T) * p.T;
+    const bool has_pred = (t1 > 0) && (TR > 0);
+    const int* pred_flag = p.flags + item - 1;
+    const float* in_b = p.in + (size_t)b * p.Cin * p.R * p.R;
+    const int I0 = t1 * NN - p.off;
+    int seen = 0, inflight = 0;
+    unsigned rows = 0;
+#pragma unroll
+    for (int p1 = 0; p1 < P; ++p1)
+      if (I0 + p1 >= 0 && I0 + p1 < p.Ro) rows |= 1u << p1;
+    const unsigned rowsB = laneB ? rows : 0u;
+    float* colp = p.out + (size_t)b * p.Cout * plane_sz + (ptrdiff_t)I0 * p.Ro + tid;
+
+    // stage input rows + the first two spectra
+    for (int c = 0; c < p.Cin; ++c)
+      stage_rows(band + c * bandsz, BW, in_b + (size_t)c * p.R * p.R, p.R, t1 * NN, NN, 0, BW, tid, nthr);
+    for (int co = 0; co < 2 && co < p.Cout; ++co)
+      for (int e = tid; e < ssz; e += nthr) cp_async16(Ss + co * ssz + e, p.spec + (size_t)co * ssz + e);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    // this lane's input row spectra â†’ TMEM (lanes past the last tile store zeros)
+    if (warp * 32 < nthr) {
+      float cf[NN], sf[NN];
+#pragma unroll
+      for (int p1 = 0; p1 < NN; ++p1) {
+        float s, c;
+        sincospif(2.0f * (float)((a_f1 * p1) % P) / (float)P, &s, &c);
+        cf[p1] = c;
+        sf[p1] = s;
+      }
+#pragma unroll
+      for (int c = 0; c < CR; ++c) {
+        float xb[XC];
+#pragma unroll
+        for (int q = 0; q < XC; ++q) xb[q] = 0.f;
+        if (laneA && c < p.Cin) {
+          float z[NN][NN], xr[P], xi[P];
+          read_block<NN>(band + c * bandsz, BW, a_t * NN, z);
+          block_row_spectrum<NN>(z, cf, sf, xr, xi);
+#pragma unroll
+          for (int f = 0; f < P; ++f) { xb[f] = xr[f]; xb[P + f] = xi[f]; }
+        }
+#pragma unroll
+        for (int q = 0; q < NX16; ++q) tmem_st16(tbase + c * XC + 16 * q, xb + 16 * q);
+      }
+      tmem_wait_st();
+    }
+
+    constexpr unsigned kAll = (1u << P) - 1u;
+    const bool fullB = rowsB == kAll;  // interior tile row: no per-row bounds checks
+    const ptrdiff_t Ro = p.Ro;
+    auto prefetch = [&](int c, float (&pend)[TR > 0 ? TR : 1]) {
+      const float* cp = colp + (size_t)c * plane_sz;
+      if (fullB) {
+#pragma unroll
+        for (int p1 = 0; p1 < TR; ++p1) { pend[p1] = __ldcg(cp); cp += Ro; }
+      } else {
+#pragma unroll
+        for (int p1 = 0; p1 < TR; ++p1)
+          pend[p1] = ((rowsB >> p1) & 1u) ? __ldcg(cp + (ptrdiff_t)p1 * Ro) : 0.f;
+      }
+    };
+    auto store_rows = [&](float* cp, const float* v, int p_lo, int p_hi, bool partial_from_n) {
+      if (fullB) {
+        float* r = cp + (ptrdiff_t)p_lo * Ro;
+#pragma unroll
+        for (int p1 = 0; p1 < P; ++p1) {
+          if (p1 >= p_lo && p1 < p_hi) {
+            if (partial_from_n && p1 >= NN) __stcg(r, v[p1]);
+            else __stcs(r, v[p1]);
+            r += Ro;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int p1 = 0; p1 < P; ++p1)
+          if (p1 >= p_lo && p1 < p_hi && ((rowsB >> p1) & 1u)) {
+            if (partial_from_n && p1 >= NN) __stcg(cp + (ptrdiff_t)p1 * Ro, v[p1]);
+            else __stcs(cp + (ptrdiff_t)p1 * Ro, v[p1]);
+          }
+      }
+    };
+    auto pre_b = [&](int cb, float (&pend)[TR > 0 ? TR : 1]) -> bool {
+      const bool fin = laneB && has_pred && cb >= kTRing;
+      if (fin) {
+        wait_flag(pred_flag, cb - kTRing + 1, lane, leader, bmask, seen, inflight);  // publication lags â‰¤ kTPublish+1
+        prefetch(cb - kTRing, pend);
+      }
+      return fin;
+    };
+    // stage B of channel cb (warp-uniform: TMEM ring accesses are collective)
+    auto do_b = [&](int cb, bool fin, const float (&pend)[TR > 0 ? TR : 1]) {
+      float y[P];
+      stage_b_column<NN>(Qs + (cb & 1) * qsz, cg, y);
+      float* cp = colp + (size_t)cb * plane_sz;
+      // Channels < cb are published at the barrier that follows when cb is a
+      // publication point.  Every thread that stored their partial rows fences first;
+      // the fence sits BEFORE this channel's stores, so the stores it waits for were
+      // issued an iteration ago and have normally landed (a cheap fence).
+      if ((cb % kTPublish) == 0 && cb > 0 && rowsB) fence_release();
+      store_rows(cp, y, TR, P, true);
+      if (!has_pred) {
+        store_rows(cp, y, 0, TR, false);
+      } else if (TR > 0) {
+        const uint32_t slot = tbase + RING0 + (cb % kTRing) * 8;
+        float old[8];
+        __syncwarp();
+        tmem_ld8(slot, old);  // channel cb âˆ’ kTRing's top rows (same slot)
+        tmem_wait_ld();
+        if (fin) {
+          float sum[P];
+#pragma unroll
+          for (int p1 = 0; p1 < P; ++p1) sum[p1] = (p1 < TR) ? pend[p1] + old[p1] : 0.f;
+          store_rows(colp + (size_t)(cb - kTRing) * plane_sz, sum, 0, TR, false);
+        }
+        float nw[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) nw[q] = (q < TR) ? y[q] : 0.f;
+        tmem_st8(slot, nw);
+        if (laneB && lane == leader && seen < cb + 2 - kTRing + kTPublish) inflight = ld_relaxed(pred_flag);
+      }
+    };
+    // barrier after stage B of channel cb: channels [0, cb) are fenced by everyone
+    auto sync_publish = [&](int cb) {
+      cp_async_wait_1();
+      tmem_wait_st();
+      __syncthreads();
+      if (tid == pub_tid && cb > 0 && (cb % kTPublish) == 0) st_release(p.flags + item, cb);
+    };
+    auto stage_a = [&](int co) {
+      float yr[P], yi[P];
+      const float4* S = Ss + (co % NSB) * ssz + a_f1;
+      __syncwarp();  // tcgen05.ld is warp-collective: reconverge after divergent code
+#pragma unroll
+      for (int c = 0; c < CR; ++c) {
+        if (c < p.Cin) {
+          float xb[XC];
+#pragma unroll
+          for (int q = 0; q < NX16; ++q) tmem_ld16(tbase + c * XC + 16 * q, xb + 16 * q);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < P2; ++q) {
+            const float4 w = S[(c * P2 + q) * H];
+            const int f = 2 * q;
+            const float x0r = xb[f], x0i = xb[P + f];
+            if (c == 0) { yr[f] = w.x * x0r; yi[f] = w.x * x0i; }
+            else { yr[f] = fmaf(w.x, x0r, yr[f]); yi[f] = fmaf(w.x, x0i, yi[f]); }
+            yr[f] = fmaf(-w.y, x0i, yr[f]);
+            yi[f] = fmaf(w.y, x0r, yi[f]);
+            if (f + 1 < P) {
+              const float x1r = xb[f + 1], x1i = xb[P + f + 1];
+              if (c == 0) { yr[f + 1] = w.z * x1r; yi[f + 1] = w.z * x1i; }
+              else { yr[f + 1] = fmaf(w.z, x1r, yr[f + 1]); yi[f + 1] = fmaf(w.z, x1i, yi[f + 1]); }
+              yr[f + 1] = fmaf(-w.w, x1i, yr[f + 1]);
+              yi[f + 1] = fmaf(w.w, x1r, yi[f + 1]);
+            }
+          }
+        }
+      }
+      stage_a_store<NN>(yr, yi, Qs + (co & 1) * qsz + a_qoff);
+    };
+    auto prefetch_spec = [&](int co) {
+      if (co + 2 < p.Cout)
+        for (int e = tid; e < ssz; e += nthr)
+          cp_async16(Ss + ((co + 2) % NSB) * ssz + e, p.spec + (size_t)(co + 2) * ssz + e);
+      cp_async_commit();
+    };
+
+    if (comp) stage_a(0);
+    prefetch_spec(0);
+    sync_publish(0);
+    for (int it = 1; it < p.Cout; ++it) {
+      if (comp) {
+        float pend[TR > 0 ? TR : 1];
+        const bool fin = pre_b(it - 1, pend);
+        stage_a(it);
+        do_b(it - 1, fin, pend);
+      }
+      prefetch_spec(it);
+      sync_publish(it - 1);
+    }
+    if (comp) {
+      float pend[TR > 0 ? TR : 1];
+      const bool fin = pre_b(p.Cout - 1, pend);
+      do_b(p.Cout - 1, fin, pend);
+    }
+    // item end: fence + publish, then finish the deferred channels
+    if (laneB) fence_release();
+    cp_async_wait_all();
+    tmem_wait_st();
+    __syncthreads();
+    if (tid == pub_tid) st_release(p.flags + item, p.Cout);
+    if (comp && has_pred && TR > 0) {
+      if (laneB) wait_flag(pred_flag, p.Cout, lane, leader, bmask, seen, inflight);
+      for (int c = max(0, p.Cout - kTRing); c < p.Cout; ++c) {
+        float pend[TR > 0 ? TR : 1];
+        prefetch(c, pend);
+        float old[8];
+        __syncwarp();
+        tmem_ld8(tbase + RING0 + (c % kTRing) * 8, old);
+        tmem_wait_ld();
+        float sum[P];
+#pragma unroll
+        for (int p1 = 0; p1 < P; ++p1) sum[p1] = (p1 < TR) ? pend[p1] + old[p1] : 0.f;
+        store_rows(colp + (size_t)c * plane_sz, sum, 0, TR, false);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "n"(ACOLS));
 }
 
 // ------------------------------------------------------------------ bwd_filter

@@ -6,6 +6,8 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "oaa_kernels.cuh"
 
@@ -40,14 +42,39 @@ cudaError_t launch_engine_t(const oaa::EngineParams& p, const EnginePlan& e, cud
   return cudaGetLastError();
 }
 
+// S1 engine with TMEM-resident input spectra: occupancy is also bounded by tensor
+// memory (512 columns per SM).
+template <int NN, int CR>
+cudaError_t launch_engine_s1t_t(const oaa::EngineParams& p, const EnginePlan& e, cudaStream_t s) {
+  auto k = oaa::oaa_engine_s1t_kernel<NN, CR>;
+  cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem);
+  if (err != cudaSuccess) return err;
+  err = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (err != cudaSuccess) return err;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, e.nthreads, e.smem);
+  // (the occupancy query under-reports here; over-subscribing a persistent grid is
+  // harmless: surplus CTAs find no work item and exit)
+  per_sm = std::max(1, std::max(per_sm, 2));
+  per_sm = std::min(per_sm, 512 / oaa::s1t_alloc_cols(NN, CR));
+  const int grid = std::max(1, std::min(p.num_items, sms * per_sm));
+  if (std::getenv("OAA_DEBUG"))
+    std::fprintf(stderr, "oaa s1t<%d,%d>: threads %d smem %zu per_sm %d grid %d\n", NN, CR, e.nthreads, e.smem, per_sm, grid);
+  k<<<grid, e.nthreads, e.smem, s>>>(p);
+  g_launches++;
+  return cudaGetLastError();
+}
+
 template <int NN>
 cudaError_t launch_engine_n(const oaa::EngineParams& p, const EnginePlan& e, cudaStream_t s) {
   if (e.S1) {
     switch (e.CR) {
-      case 1: return launch_engine_t<NN, 1, true>(p, e, s);
-      case 2: return launch_engine_t<NN, 2, true>(p, e, s);
-      case 3: return launch_engine_t<NN, 3, true>(p, e, s);
-      default: return launch_engine_t<NN, 4, true>(p, e, s);
+      case 1: return launch_engine_s1t_t<NN, 1>(p, e, s);
+      case 2: return launch_engine_s1t_t<NN, 2>(p, e, s);
+      case 3: return launch_engine_s1t_t<NN, 3>(p, e, s);
+      default: return launch_engine_s1t_t<NN, 4>(p, e, s);
     }
   } else {
     switch (e.CR) {
