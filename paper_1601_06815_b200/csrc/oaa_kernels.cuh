@@ -119,10 +119,14 @@ __device__ __forceinline__ void stage_rows(float* dst, int ld, const float* __re
     for (int cc = tid; cc < ncols; cc += nthr) {
       const int q = c0 + cc;
       const bool qok = q >= 0 && q < R;
+      const float* src = plane + (size_t)r0 * R + q;  // only dereferenced when in range
+      float* d = dst + cc;
       for (int rr = 0; rr < nrows; ++rr) {
         const int r = r0 + rr;
         const bool ok = qok && r >= 0 && r < R;
-        cp_async4(dst + rr * ld + cc, ok ? plane + (size_t)r * R + q : plane, ok);
+        cp_async4(d, ok ? src : plane, ok);
+        src += R;
+        d += ld;
       }
     }
   }
@@ -166,6 +170,41 @@ __device__ __forceinline__ void block_row_spectrum(const float (&z)[NN][NN], con
     }
     rr[p2] = a;
     ri[p2] = b;
+  }
+#pragma unroll
+  for (int p2 = NN; p2 < P; ++p2) { rr[p2] = 0.f; ri[p2] = 0.f; }
+  dft<P, -1, lead_mask(NN)>(rr, ri, xr, xi);
+}
+
+// Same as block_row_spectrum, reading the block row by row from staged shared memory
+// (row stride ld, block column origin c) so the n×n block is never held in registers.
+template <int NN>
+__device__ __forceinline__ void block_row_spectrum_smem(const float* src, int ld, int c, const float (&cf)[NN],
+                                                        const float (&sf)[NN], float (&xr)[2 * NN - 1],
+                                                        float (&xi)[2 * NN - 1]) {
+  constexpr int P = 2 * NN - 1;
+  float rr[P], ri[P];
+#pragma unroll
+  for (int p1 = 0; p1 < NN; ++p1) {
+    float z[NN];
+    if constexpr (NN % 4 == 0) {
+#pragma unroll
+      for (int q = 0; q < NN; q += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(src + p1 * ld + c + q);
+        z[q] = v.x; z[q + 1] = v.y; z[q + 2] = v.z; z[q + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < NN; ++q) z[q] = src[p1 * ld + c + q];
+    }
+#pragma unroll
+    for (int p2 = 0; p2 < NN; ++p2) {
+      if (p1 == 0) { rr[p2] = z[p2]; ri[p2] = 0.f; }
+      else {
+        rr[p2] = fmaf(z[p2], cf[p1], rr[p2]);
+        ri[p2] = fmaf(-z[p2], sf[p1], ri[p2]);
+      }
+    }
   }
 #pragma unroll
   for (int p2 = NN; p2 < P; ++p2) { rr[p2] = 0.f; ri[p2] = 0.f; }
@@ -894,23 +933,30 @@ __global__ void __launch_bounds__(kMaxThreads, 2) oaa_engine_s1t_kernel(const En
 }
 
 // ------------------------------------------------------------------ bwd_filter
-// Stage rows r0..r0+nrows of `nplanes` consecutive R×R planes (plane stride R·R), columns
-// [c0, c0+ncols), into dst[plane][row][ld] (zero outside).  Threads own (row-group,
-// column) pairs, so all threads issue copies even when ncols is small.
+// Stage rows r0..r0+NROWS of `nplanes` consecutive R×R planes (plane stride R·R),
+// columns [c0, c0+ncols), into dst[plane][row][ld] (zero outside).  Warps own rows,
+// lanes own columns, and the plane loop only bumps pointers, so a copy costs a handful
+// of instructions (the rows are not 16-byte aligned in general: M = N−n+1 is odd).
+template <int NROWS>
 __device__ __forceinline__ void stage_planes_rows(float* dst, int ld, const float* __restrict__ base,
-                                                  int nplanes, int R, int r0, int nrows, int c0,
-                                                  int ncols, int tid, int nthr) {
-  const int groups = max(1, nthr / ncols);
-  const int cc = tid % ncols, grp = tid / ncols;
-  if (grp >= groups) return;
-  const int q = c0 + cc;
-  const bool qok = q >= 0 && q < R;
-  const int total = nplanes * nrows;
-  for (int row = grp; row < total; row += groups) {
-    const int pl = row / nrows, rr = row - (row / nrows) * nrows;
+                                                  int nplanes, int R, int r0, int c0, int ncols, int tid,
+                                                  int nthr) {
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
+  const size_t pstride = (size_t)R * R;
+  for (int rr = warp; rr < NROWS; rr += nwarps) {
     const int r = r0 + rr;
-    const bool ok = qok && r >= 0 && r < R;
-    cp_async4(dst + row * ld + cc, ok ? base + ((size_t)pl * R + r) * R + q : base, ok);
+    const bool rok = r >= 0 && r < R;
+    for (int cc = lane; cc < ncols; cc += 32) {
+      const int q = c0 + cc;
+      const bool ok = rok && q >= 0 && q < R;
+      const float* src = ok ? base + (size_t)r * R + q : base;
+      float* d = dst + rr * ld + cc;
+      for (int pl = 0; pl < nplanes; ++pl) {
+        cp_async4(d, src, ok);
+        if (ok) src += pstride;
+        d += NROWS * ld;
+      }
+    }
   }
 }
 
@@ -960,10 +1006,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1) oaa_bwd_filter_kernel(const Fi
       const float* dyk = p.dy + ((size_t)b * p.K + k0) * p.M * p.M;
       __syncthreads();  // previous item done with xwin / xs / dyb
       // x rows of this item's windows (zero outside x) and the first dy chunk
-      for (int cc = 0; cc < nc; ++cc)
-        stage_rows(xwin + cc * P * XW, XW, p.x + ((size_t)b * p.C + c0 + cc) * p.N * p.N, p.N,
-                   t1 * NN + w0, P, w0, XW, tid, nthr);
-      stage_planes_rows(dyb, DW, dyk, nk, p.M, t1 * NN, NN, 0, min(p.TCH, p.Td) * NN, tid, nthr);
+      stage_planes_rows<P>(xwin, XW, p.x + ((size_t)b * p.C + c0) * p.N * p.N, nc, p.N, t1 * NN + w0, w0, XW,
+                           tid, nthr);
+      stage_planes_rows<NN>(dyb, DW, dyk, nk, p.M, t1 * NN, 0, min(p.TCH, p.Td) * NN, tid, nthr);
       cp_async_commit();
       cp_async_wait_all();
       __syncthreads();
@@ -1008,17 +1053,14 @@ __global__ void __launch_bounds__(kMaxThreads, 1) oaa_bwd_filter_kernel(const Fi
         __syncthreads();  // chunk ch landed, Ξ̂ written, chunk ch−1's buffer free
         if (ch + 1 < nchunks) {
           const int t0n = tc0 + p.TCH;
-          stage_planes_rows(dyb + ((ch + 1) & 1) * dysz, DW, dyk, nk, p.M, t1 * NN, NN, t0n * NN,
-                            min(p.TCH, p.Td - t0n) * NN, tid, nthr);
+          stage_planes_rows<NN>(dyb + ((ch + 1) & 1) * dysz, DW, dyk, nk, p.M, t1 * NN, t0n * NN,
+                                min(p.TCH, p.Td - t0n) * NN, tid, nthr);
           cp_async_commit();
         }
         if (laneK) {
           const float* db = dyb + (ch & 1) * dysz + kk * NN * DW;
-          for (int tt = 0; tt < ntc; ++tt) {
-            float z[NN][NN];
-            read_block<NN>(db, DW, tt * NN, z);
-            float gr[P], gi[P];
-            block_row_spectrum<NN>(z, cf, sf, gr, gi);
+          // accumulate conj(Ĝ)·Ξ̂ of one block into the lane's dŴ row
+          auto accum = [&](int tt, const float (&gr)[P], const float (&gi)[P]) {
             const float2* src = xs + ((size_t)((tc0 + tt) * CR) * P) * H + f1;
 #pragma unroll
             for (int cc = 0; cc < CR; ++cc) {
@@ -1026,7 +1068,6 @@ __global__ void __launch_bounds__(kMaxThreads, 1) oaa_bwd_filter_kernel(const Fi
 #pragma unroll
                 for (int f2 = 0; f2 < P; ++f2) {
                   const float2 X = src[(cc * P + f2) * H];
-                  // conj(G)·X
                   ar[cc][f2] = fmaf(gr[f2], X.x, ar[cc][f2]);
                   ar[cc][f2] = fmaf(gi[f2], X.y, ar[cc][f2]);
                   ai[cc][f2] = fmaf(gr[f2], X.y, ai[cc][f2]);
@@ -1034,6 +1075,19 @@ __global__ void __launch_bounds__(kMaxThreads, 1) oaa_bwd_filter_kernel(const Fi
                 }
               }
             }
+          };
+          int tt = 0;
+          for (; tt + 1 < ntc; tt += 2) {  // two independent block transforms per step (ILP)
+            float g0r[P], g0i[P], g1r[P], g1i[P];
+            block_row_spectrum_smem<NN>(db, DW, tt * NN, cf, sf, g0r, g0i);
+            block_row_spectrum_smem<NN>(db, DW, (tt + 1) * NN, cf, sf, g1r, g1i);
+            accum(tt, g0r, g0i);
+            accum(tt + 1, g1r, g1i);
+          }
+          if (tt < ntc) {
+            float gr[P], gi[P];
+            block_row_spectrum_smem<NN>(db, DW, tt * NN, cf, sf, gr, gi);
+            accum(tt, gr, gi);
           }
         }
       }
