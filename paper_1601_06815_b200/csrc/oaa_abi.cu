@@ -110,14 +110,19 @@ bool plan_engine(int R, int Ro, int off, int n, int Cin, int Cout, EnginePlan* e
     e->S1 = false;
     e->CR = std::min(Cout, kCRMax);
   }
-  const int nsb = e->S1 ? 3 : 2;
-  const int cin_s = e->S1 ? Cin : e->CR;
-  const int nband = e->S1 ? Cin : 2;
-  const size_t band_b = sizeof(float) * (size_t)nband * n * e->BW;
-  const size_t ring_b = sizeof(float) * (size_t)oaa::kRingDepth * (n - 1) * oaa::kMaxThreads;
-  // S1 runs the TMEM engine (spectra and deferred rows in tensor memory, no smem ring)
-  e->smem = sizeof(float2) * 2 * ((size_t)H * P * e->TS) + sizeof(float4) * (size_t)nsb * cin_s * P2 * H +
-            (e->S1 ? band_b : band_b + ring_b);
+  const size_t q_b = sizeof(float2) * 2 * ((size_t)H * P * e->TS);
+  if (e->S1) {
+    // S1 runs the TMEM engine (spectra and deferred rows in tensor memory, no smem ring)
+    e->CIG = 1;
+    e->smem = q_b + sizeof(float4) * (size_t)3 * Cin * P2 * H + sizeof(float) * (size_t)Cin * n * e->BW;
+  } else {
+    const size_t ring_b = sizeof(float) * (size_t)std::min(oaa::kRingDepth, Cout) * (n - 1) * oaa::kMaxThreads;
+    for (e->CIG = 4; e->CIG >= 1; e->CIG /= 2) {
+      e->smem = q_b + ring_b + 2 * (size_t)e->CIG * (sizeof(float4) * (size_t)e->CR * P2 * H + sizeof(float) * (size_t)n * e->BW);
+      if (e->smem <= 220 * 1024) break;
+    }
+    if (e->CIG < 1) e->CIG = 1;
+  }
   return e->smem <= 220 * 1024;
 }
 
@@ -269,6 +274,7 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
   p.BW = e.BW;
   p.num_items = B * e.T;
   p.ncomp = e.ncomp;
+  p.CIG = e.CIG;
   ProfScope prof(is_fwd ? OAA_OP_FWD : OAA_OP_BWD_DATA, s);
   prof.start();
   cudaError_t err = launch_engine(n, p, e, s);

@@ -55,6 +55,7 @@ struct EngineParams {
   int* counter;         // dynamic work-item counter
   int B, Cin, Cout, R, T, Ro, off, TS, BW, num_items;
   int ncomp;            // compute threads; a trailing extra warp (if any) only publishes flags
+  int CIG;              // S2: input channels staged per barrier
 };
 
 struct FilterParams {
@@ -326,10 +327,10 @@ __global__ void __launch_bounds__(kMaxThreads, OAA_ENGINE_MINB) oaa_engine_kerne
   const int ssz = CIN_S * P2 * H;                  // float4 per spectrum buffer
   float2* Qs = reinterpret_cast<float2*>(smem_raw);
   float4* Ss = reinterpret_cast<float4*>(Qs + 2 * qsz);
-  float* band = reinterpret_cast<float*>(Ss + NSB * ssz);
+  float* band = reinterpret_cast<float*>(Ss + (S1 ? NSB : 2 * p.CIG) * ssz);
   const int bandsz = NN * BW;                      // floats per staged channel
   // S1 reads the staged rows only at item start, when the ring is empty: they share space
-  float* ring = S1 ? band : band + 2 * bandsz;     // [kRingDepth][TR][RS]
+  float* ring = S1 ? band : band + 2 * p.CIG * bandsz;  // [min(kRingDepth, Cout)][TR][RS]
   zero_q_tail<NN>(Qs, qsz, p.T, tid, nthr);
 
   // stage A lane = (t2, f1)
@@ -546,54 +547,75 @@ __global__ void __launch_bounds__(kMaxThreads, OAA_ENGINE_MINB) oaa_engine_kerne
         cf[p1] = c;
         sf[p1] = s;
       }
+      // Input channels are staged CIG at a time (one barrier per group), double buffered:
+      // band[2][CIG][n][BW], spectra[2][CIG][CR][P2][H].
+      const int CIG = p.CIG;
+      const int ngrp = (p.Cin + CIG - 1) / CIG;
       for (int c0 = 0; c0 < p.Cout; c0 += CR) {
         const int nc = min(CR, p.Cout - c0);
-        const int ssz_c = nc * P2 * H;
+        const int ssz_c = nc * P2 * H;  // float4 of one input channel's chunk spectra
         float ar[CR][P], ai[CR][P];
 #pragma unroll
         for (int cc = 0; cc < CR; ++cc)
 #pragma unroll
           for (int f2 = 0; f2 < P; ++f2) { ar[cc][f2] = 0.f; ai[cc][f2] = 0.f; }
-        // prologue: stage input channel 0
-        stage_rows(band, BW, in_b, p.R, t1 * NN, NN, 0, BW, tid, nthr);
-        for (int e = tid; e < ssz_c; e += nthr) cp_async16(Ss + e, p.spec + (size_t)c0 * P2 * H + e);
-        cp_async_commit();
-        for (int ci = 0; ci < p.Cin; ++ci) {
-          cp_async_wait_all();
-          __syncthreads();
-          if (ci + 1 < p.Cin) {  // stage the next input channel while this one computes
-            const int nb = (ci + 1) & 1;
-            stage_rows(band + nb * bandsz, BW, in_b + (size_t)(ci + 1) * p.R * p.R, p.R, t1 * NN, NN, 0,
+        auto stage_group = [&](int g) {
+          const int slot = g & 1;
+          for (int j = 0; j < CIG; ++j) {
+            const int ci = g * CIG + j;
+            if (ci >= p.Cin) break;
+            stage_rows(band + (slot * CIG + j) * bandsz, BW, in_b + (size_t)ci * p.R * p.R, p.R, t1 * NN, NN, 0,
                        BW, tid, nthr);
             for (int e = tid; e < ssz_c; e += nthr)
-              cp_async16(Ss + nb * ssz + e, p.spec + ((size_t)(ci + 1) * p.Cout + c0) * P2 * H + e);
-            cp_async_commit();
+              cp_async16(Ss + (slot * CIG + j) * ssz + e, p.spec + ((size_t)ci * p.Cout + c0) * P2 * H + e);
           }
+          cp_async_commit();
+        };
+        stage_group(0);
+        for (int g = 0; g < ngrp; ++g) {
+          cp_async_wait_all();
+          __syncthreads();
+          if (g + 1 < ngrp) stage_group(g + 1);  // overlaps this group's compute
           if (laneA) {
-            float z[NN][NN];
-            read_block<NN>(band + (ci & 1) * bandsz, BW, a_t * NN, z);
-            float gr[P], gi[P];
-            block_row_spectrum<NN>(z, cf, sf, gr, gi);
-            const float4* S = Ss + (ci & 1) * ssz + a_f1;
+            const int nci = min(CIG, p.Cin - g * CIG);
+            // accumulate one input channel's row spectrum into the output accumulators
+            auto accum = [&](int slot, const float (&gr)[P], const float (&gi)[P]) {
+              const float4* S = Ss + slot * ssz + a_f1;
 #pragma unroll
-            for (int cc = 0; cc < CR; ++cc) {
-              if (cc < nc) {
+              for (int cc = 0; cc < CR; ++cc) {
+                if (cc < nc) {
 #pragma unroll
-                for (int q = 0; q < P2; ++q) {
-                  const float4 w = S[(cc * P2 + q) * H];
-                  const int f = 2 * q;
-                  ar[cc][f] = fmaf(w.x, gr[f], ar[cc][f]);
-                  ar[cc][f] = fmaf(-w.y, gi[f], ar[cc][f]);
-                  ai[cc][f] = fmaf(w.x, gi[f], ai[cc][f]);
-                  ai[cc][f] = fmaf(w.y, gr[f], ai[cc][f]);
-                  if (f + 1 < P) {
-                    ar[cc][f + 1] = fmaf(w.z, gr[f + 1], ar[cc][f + 1]);
-                    ar[cc][f + 1] = fmaf(-w.w, gi[f + 1], ar[cc][f + 1]);
-                    ai[cc][f + 1] = fmaf(w.z, gi[f + 1], ai[cc][f + 1]);
-                    ai[cc][f + 1] = fmaf(w.w, gr[f + 1], ai[cc][f + 1]);
+                  for (int q = 0; q < P2; ++q) {
+                    const float4 w = S[(cc * P2 + q) * H];
+                    const int f = 2 * q;
+                    ar[cc][f] = fmaf(w.x, gr[f], ar[cc][f]);
+                    ar[cc][f] = fmaf(-w.y, gi[f], ar[cc][f]);
+                    ai[cc][f] = fmaf(w.x, gi[f], ai[cc][f]);
+                    ai[cc][f] = fmaf(w.y, gr[f], ai[cc][f]);
+                    if (f + 1 < P) {
+                      ar[cc][f + 1] = fmaf(w.z, gr[f + 1], ar[cc][f + 1]);
+                      ar[cc][f + 1] = fmaf(-w.w, gi[f + 1], ar[cc][f + 1]);
+                      ai[cc][f + 1] = fmaf(w.z, gi[f + 1], ai[cc][f + 1]);
+                      ai[cc][f + 1] = fmaf(w.w, gr[f + 1], ai[cc][f + 1]);
+                    }
                   }
                 }
               }
+            };
+            int j = 0;
+            for (; j + 1 < nci; j += 2) {  // two independent block transforms per step (ILP)
+              const int s0 = (g & 1) * CIG + j;
+              float g0r[P], g0i[P], g1r[P], g1i[P];
+              block_row_spectrum_smem<NN>(band + s0 * bandsz, BW, a_t * NN, cf, sf, g0r, g0i);
+              block_row_spectrum_smem<NN>(band + (s0 + 1) * bandsz, BW, a_t * NN, cf, sf, g1r, g1i);
+              accum(s0, g0r, g0i);
+              accum(s0 + 1, g1r, g1i);
+            }
+            if (j < nci) {
+              const int s0 = (g & 1) * CIG + j;
+              float gr[P], gi[P];
+              block_row_spectrum_smem<NN>(band + s0 * bandsz, BW, a_t * NN, cf, sf, gr, gi);
+              accum(s0, gr, gi);
             }
           }
         }

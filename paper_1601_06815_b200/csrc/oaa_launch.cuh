@@ -16,7 +16,7 @@ namespace oaa_host {
 extern std::atomic<uint64_t> g_launches;
 
 struct EnginePlan {
-  int R, Ro, off, T, Cin, Cout, TS, BW, nthreads, ncomp, CR;
+  int R, Ro, off, T, Cin, Cout, TS, BW, nthreads, ncomp, CR, CIG;
   bool S1;
   size_t smem;
 };
