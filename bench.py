@@ -86,7 +86,7 @@ def measured_peaks():
 
 # ------------------------------------------------------------------ clocks sampler
 class ClockSampler:
-    def __init__(self, index=0, period_ms=200):
+    def __init__(self, index=0, period_ms=50):
         self.index, self.period_ms = index, period_ms
         self.proc = None
         self.lines = []
@@ -139,7 +139,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU oracle timing
-def cpu_oracle_rate(w, budget_s=15.0, max_images=64):
+def cpu_oracle_rate(w, budget_s=15.0, max_images=512):
     """Time the float64 direct oracle (fwd + bwd_data + bwd_filter) on a sub-batch of
     the workload on all host cores; returns (images/s, cores, sample description)."""
     import numpy as np
@@ -258,18 +258,21 @@ def run_ours(args, w):
     ms_step = ms_total / args.steps
     value = world * B * args.steps / (ms_total / 1e3)
 
-    # e2e through the public API from pinned host buffers
+    # e2e through the public API from pinned host buffers (paper_1601_06815_b200.pipeline:
+    # chunked H2D / compute / D2H on three streams; bwd_filter over the whole batch)
     e2e = None
     if not args.no_e2e:
+        from paper_1601_06815_b200.pipeline import HostStep
+        hs = HostStep(B, C, K, N, n, crop, dev, chunks=args.e2e_chunks)
         hx = x.cpu().pin_memory(); hw = wt.cpu().pin_memory(); hdy = dy.cpu().pin_memory()
         hy = torch.empty((B, K, M, M)).pin_memory()
         hdx = torch.empty((B, C, N, N)).pin_memory()
         hdw = torch.empty((K, C, n, n)).pin_memory()
 
         def e2e_step():
-            x.copy_(hx, non_blocking=True); wt.copy_(hw, non_blocking=True); dy.copy_(hdy, non_blocking=True)
-            step()
-            hy.copy_(y, non_blocking=True); hdx.copy_(dx, non_blocking=True); hdw.copy_(dw, non_blocking=True)
+            hs(hx, hw, hdy, hy, hdx, hdw, stream=stream)
+            if world > 1:
+                dist.all_reduce(hs.dw)
 
         for _ in range(2):
             e2e_step()
@@ -288,10 +291,8 @@ def run_ours(args, w):
             t = torch.tensor([ems], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
-        h2d = 4 * (x.numel() + wt.numel() + dy.numel())
-        d2h = 4 * (y.numel() + dx.numel() + dw.numel())
-        e2e = {"value": world * B * ne / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h}
+        e2e = {"value": world * B * ne / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": hs.h2d_bytes,
+               "d2h_bytes_per_step": hs.d2h_bytes, "chunks": len(hs.chunks)}
 
     # roofline of the dominant kernel
     terms = algorithmic_terms(w)
@@ -334,13 +335,14 @@ def run_ours(args, w):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-images", type=int, default=1)
+    ap.add_argument("--e2e-chunks", type=int, default=8)
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

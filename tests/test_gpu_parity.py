@@ -261,3 +261,23 @@ def test_sharded_config_one_gpu_shard():
     c = CONFIGS["sharded"]
     from workloads import Workload
     _full_size(Workload("sharded_shard", B=128, C=c.C, K=c.K, N=c.N, n=c.n), n_samples=400, n_dw=64, seed=4)
+
+
+def test_host_pipeline_matches_device_calls():
+    """pipeline.HostStep (chunked H2D/compute/D2H) gives the same results as the plain
+    device calls, bitwise (same kernels, same per-image work)."""
+    from paper_1601_06815_b200.pipeline import HostStep
+    B, C, K, N, n, crop = 6, 3, 5, 30, 5, "valid"
+    d = make_inputs(B, C, K, N, n, crop, seed=13)
+    hx = torch.from_numpy(d["x"]).pin_memory(); hw = torch.from_numpy(d["w"]).pin_memory()
+    hdy = torch.from_numpy(d["dy"]).pin_memory()
+    M = out_size(N, n, crop)
+    hy = torch.empty((B, K, M, M)).pin_memory(); hdx = torch.empty((B, C, N, N)).pin_memory()
+    hdw = torch.empty((K, C, n, n)).pin_memory()
+    hs = HostStep(B, C, K, N, n, crop, chunks=3)
+    hs(hx, hw, hdy, hy, hdx, hdw)
+    torch.cuda.synchronize()
+    x, w, dy = hx.cuda(), hw.cuda(), hdy.cuda()
+    assert torch.equal(hy, oaa.conv_fwd(x, w, crop).cpu())
+    assert torch.equal(hdx, oaa.conv_bwd_data(dy, w, N, crop).cpu())
+    assert torch.equal(hdw, oaa.conv_bwd_filter(x, dy, n, crop).cpu())
