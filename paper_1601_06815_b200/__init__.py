@@ -61,6 +61,8 @@ def lib():
                 f = getattr(L, name)
                 f.argtypes = [F, F, F, I, I, I, I, I, I, V, Z, V]
                 f.restype = I
+            L.oaa_debug_bin_gemm.argtypes = [F, F, F, I, I, I, I, V]
+            L.oaa_debug_bin_gemm.restype = I
             L.oaa_status_string.argtypes = [I]
             L.oaa_status_string.restype = ctypes.c_char_p
             L.oaa_version.argtypes = []
@@ -205,6 +207,22 @@ def conv_bwd_filter(x: torch.Tensor, dy: torch.Tensor, n: int, crop="valid",
         if tuple(out.shape) != (K, C, n, n):
             raise ValueError(f"out must have shape {(K, C, n, n)}")
     return _call(lib().oaa_conv_bwd_filter, x, dy, out, (B, C, K, N, n), crop, OP_BWD_FILTER, stream)
+
+
+def debug_bin_gemm(A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:
+    """D[f] = A[f] @ B[f].T with the tcgen05 3×TF32 contraction kernel (diagnostics)."""
+    _check(A, "A", 3); _check(B, "B", 3)
+    F, M, Kd = A.shape
+    F2, N, Kd2 = B.shape
+    if F != F2 or Kd != Kd2 or Kd % 4:
+        raise ValueError("shape mismatch or Kd % 4 != 0")
+    D = torch.empty((F, M, N), dtype=torch.float32, device=A.device)
+    s = torch.cuda.current_stream(A.device)
+    st = lib().oaa_debug_bin_gemm(ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
+                                  ctypes.c_void_p(D.data_ptr()), F, M, N, Kd, ctypes.c_void_p(s.cuda_stream))
+    if st != 0:
+        raise OaAError(lib().oaa_status_string(st).decode())
+    return D
 
 
 def launch_count() -> int:

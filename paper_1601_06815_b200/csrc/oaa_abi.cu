@@ -12,6 +12,7 @@
 #include "../../include/oaa.h"
 #define OAA_DEFINE_AUX_KERNELS
 #include "oaa_launch.cuh"
+#include "oaa_tc.cuh"
 
 namespace oaa_host {
 std::atomic<uint64_t> g_launches{0};
@@ -387,6 +388,22 @@ const char* oaa_status_string(oaa_status_t s) {
     case OAA_ERR_CUDA: return "OAA_ERR_CUDA: CUDA launch failure";
   }
   return "unknown oaa_status_t";
+}
+
+oaa_status_t oaa_debug_bin_gemm(const float* A, const float* B, float* D, int F, int M, int N, int Kd,
+                                void* stream) {
+  if (!A || !B || !D || F < 1 || M < 1 || N < 1 || Kd < 1 || (Kd & 3)) return OAA_ERR_INVALID_VALUE;
+  oaa::BinGemmParams p;
+  p.A = A; p.B = B; p.D = D; p.F = F; p.M = M; p.N = N; p.Kd = Kd; p.ldd = N;
+  p.strideA = (long long)M * Kd; p.strideB = (long long)N * Kd; p.strideD = (long long)M * N;
+  const size_t smem = 2 * 4 * 4096 * sizeof(float);
+  if (cudaFuncSetAttribute(oaa::oaa_bin_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return OAA_ERR_CUDA;
+  dim3 grid(cdiv(N, oaa::kTcN), cdiv(M, oaa::kTcM), F);
+  oaa::oaa_bin_gemm_kernel<<<grid, 128, smem, static_cast<cudaStream_t>(stream)>>>(p);
+  g_launches++;
+  return cudaGetLastError() == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
 }
 
 const char* oaa_version(void) { return "oaa-b200 0.1.0 sm_100a"; }

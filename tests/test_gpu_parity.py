@@ -281,3 +281,15 @@ def test_host_pipeline_matches_device_calls():
     assert torch.equal(hy, oaa.conv_fwd(x, w, crop).cpu())
     assert torch.equal(hdx, oaa.conv_bwd_data(dy, w, N, crop).cpu())
     assert torch.equal(hdw, oaa.conv_bwd_filter(x, dy, n, crop).cpu())
+
+
+@pytest.mark.parametrize("F,M,N,Kd", [(1, 128, 128, 32), (3, 256, 384, 192), (2, 200, 130, 68), (5, 512, 256, 128)])
+def test_tcgen05_bin_gemm_3xtf32(F, M, N, Kd):
+    """The tensor-core contraction kernel alone vs a float64 matmul: fp32-level accuracy
+    (3×TF32), ragged M/N/K tails."""
+    g = torch.Generator(device="cuda").manual_seed(F * 1000 + M + N + Kd)
+    A = torch.rand((F, M, Kd), generator=g, device="cuda") * 2 - 1
+    B = torch.rand((F, N, Kd), generator=g, device="cuda") * 2 - 1
+    D = oaa.debug_bin_gemm(A, B)
+    ref = torch.matmul(A.double(), B.double().transpose(1, 2))
+    check(D.cpu().numpy(), ref.cpu().numpy(), "bin_gemm")
