@@ -89,7 +89,8 @@ bool make_geo(int N, int n, oaa_crop_t crop, Geo* g) {
 constexpr int kCRMax = 4;
 
 
-bool plan_engine(int R, int Ro, int off, int n, int Cin, int Cout, EnginePlan* e) {
+bool plan_engine(int R, int Ro, int off, int n, int Cin, int Cout, EnginePlan* e, bool ly = false) {
+  e->LY = ly;
   e->R = R;
   e->Ro = Ro;
   e->off = off;
@@ -112,7 +113,13 @@ bool plan_engine(int R, int Ro, int off, int n, int Cin, int Cout, EnginePlan* e
     e->CR = std::min(Cout, kCRMax);
   }
   const size_t q_b = sizeof(float2) * 2 * ((size_t)H * P * e->TS);
-  if (e->S1) {
+  if (ly) {
+    // the engine only inverts Ŷ (bin GEMM output) and overlap-adds: no inputs, no spectra
+    e->S1 = true;
+    e->CR = 1;
+    e->CIG = 1;
+    e->smem = q_b;
+  } else if (e->S1) {
     // S1 runs the TMEM engine (spectra and deferred rows in tensor memory, no smem ring)
     e->CIG = 1;
     e->smem = q_b + sizeof(float4) * (size_t)3 * Cin * P2 * H + sizeof(float) * (size_t)Cin * n * e->BW;
@@ -134,12 +141,16 @@ bool plan_filter(int B, int C, int K, int M, int n, FilterPlan* f) {
   f->KG = std::min(f->KG, K);
   f->nkg = cdiv(K, f->KG);
   f->nthreads = cdiv(f->KG * H, 32) * 32;
-  f->CR = std::min(C, kCRMax);
   f->TCH = std::max(1, std::min(f->Td, 32 / n));
   f->XW = cdiv(f->Td * n + n - 1, 4) * 4;
   f->DW = cdiv(f->TCH * n, 4) * 4;
-  f->smem = sizeof(float) * (size_t)f->CR * P * f->XW + sizeof(float2) * (size_t)f->Td * f->CR * P * H +
-            2 * sizeof(float) * (size_t)f->KG * n * f->DW + sizeof(float2) * 16;
+  // channels per pass: as many as fit (the Ξ̂ of a whole tile row grows with Td·CR)
+  for (f->CR = std::min(C, kCRMax); f->CR >= 1; --f->CR) {
+    f->smem = sizeof(float) * (size_t)f->CR * P * f->XW + sizeof(float2) * (size_t)f->Td * f->CR * P * H +
+              2 * sizeof(float) * (size_t)f->KG * n * f->DW + sizeof(float2) * 16;
+    if (f->smem <= 220 * 1024) break;
+  }
+  if (f->CR < 1) f->CR = 1;
   const int items = std::max(1, B * f->Td);
   // one persistent wave: ~148 SMs on B200 (fixed so results do not depend on the device)
   f->G = std::max(1, std::min(items, 148 / f->nkg));
@@ -204,17 +215,160 @@ oaa_status_t validate(int B, int C, int K, int N, int n, oaa_crop_t crop, Geo* g
   return OAA_OK;
 }
 
+// tensor-core path ----------------------------------------------
+// Layers with many input AND output channels evaluate the per-bin contraction as a
+// real-ified GEMM on the tensor cores (oaa_tc.cuh): tile spectra Xg → D = Ag·Xgᵀ → the
+// engine in LY mode inverts and overlap-adds.  Xg and D hold one batch chunk at a time.
+constexpr int kTcMinChannels = 16;
+constexpr size_t kTcChunkBytes = size_t(1) << 31;  // Xg + D per chunk
+
+struct TcPlan {
+  bool use;
+  int F, T, Kdp, bc, nchunks;
+  size_t ag_b, xg_b, d_b;
+};
+TcPlan plan_tc(int B, int Cin, int Cout, int R, int n) {
+  TcPlan t{};
+  t.use = Cin >= kTcMinChannels && Cout >= kTcMinChannels;
+  if (!t.use || B < 1) return t;
+  const int P = 2 * n - 1;
+  t.F = n * P;
+  t.T = cdiv(R, n);
+  t.Kdp = cdiv(2 * Cin, 4) * 4;
+  const size_t per_img = sizeof(float) * (size_t)t.F * t.T * t.T * (t.Kdp + 2 * (size_t)Cout);
+  t.nchunks = (int)std::max<size_t>(1, (B * per_img + kTcChunkBytes - 1) / kTcChunkBytes);
+  t.bc = cdiv(B, t.nchunks);
+  t.nchunks = cdiv(B, t.bc);
+  t.ag_b = sizeof(float) * (size_t)t.F * 2 * Cout * t.Kdp;
+  t.xg_b = sizeof(float) * (size_t)t.F * t.bc * t.T * t.T * t.Kdp;
+  t.d_b = sizeof(float) * (size_t)t.F * 2 * Cout * t.bc * t.T * t.T;
+  return t;
+}
+
 // workspace layouts ------------------------------------------------------------
 struct EngineWs {
-  size_t spec_off, flags_off, counter_off, total;
+  size_t spec_off, flags_off, counter_off, xg_off, d_off, total;
 };
-EngineWs engine_ws(int B, int C, int K, int Tr, const Geo& g) {
+EngineWs engine_ws(int B, int C, int K, int Tr, const Geo& g, const TcPlan& tc) {
   EngineWs w{};
   w.spec_off = 0;
+  if (tc.use) {
+    w.flags_off = align_up(tc.ag_b);
+    w.counter_off = align_up(w.flags_off + sizeof(int) * (size_t)std::max(1, tc.bc * Tr));
+    w.xg_off = align_up(w.counter_off + sizeof(int));
+    w.d_off = align_up(w.xg_off + tc.xg_b);
+    w.total = align_up(w.d_off + tc.d_b);
+    return w;
+  }
   w.flags_off = align_up(sizeof(float4) * (size_t)K * C * ((g.P + 1) / 2) * g.H);
   w.counter_off = align_up(w.flags_off + sizeof(int) * (size_t)std::max(1, B * Tr));
   w.total = align_up(w.counter_off + sizeof(int));
   return w;
+}
+
+cudaError_t launch_tile_spectra(int n, const oaa::TileSpecParams& p, size_t smem, cudaStream_t s) {
+  switch (n) {
+    case 1: return launch_tile_spectra_n<1>(p, smem, s);
+    case 2: return launch_tile_spectra_n<2>(p, smem, s);
+    case 3: return launch_tile_spectra_n<3>(p, smem, s);
+    case 4: return launch_tile_spectra_n<4>(p, smem, s);
+    case 5: return launch_tile_spectra_n<5>(p, smem, s);
+    case 6: return launch_tile_spectra_n<6>(p, smem, s);
+    case 7: return launch_tile_spectra_n<7>(p, smem, s);
+    case 8: return launch_tile_spectra_n<8>(p, smem, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_bin_gemm(const oaa::BinGemmParams& p, cudaStream_t s) {
+  const size_t smem = 2 * 4 * 4096 * sizeof(float);
+  cudaError_t err = cudaFuncSetAttribute(oaa::oaa_bin_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+  if (err != cudaSuccess) return err;
+  dim3 grid(cdiv(p.N, oaa::kTcN), cdiv(p.M, oaa::kTcM), p.F);
+  oaa::oaa_bin_gemm_kernel<<<grid, 128, smem, s>>>(p);
+  g_launches++;
+  return cudaGetLastError();
+}
+
+// Tensor-core evaluation of fwd / bwd_data: per batch chunk, T1 (tile spectra) → bin
+// GEMM (3×TF32 tcgen05) → engine in LY mode (inverse DFT + overlap-add + crop).
+oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* out, int B, int C, int K, int n,
+                           const Geo& g, const EnginePlan& e, const TcPlan& tc, const EngineWs& L, char* base,
+                           cudaStream_t s) {
+  const int Cin = e.Cin, Cout = e.Cout, T = e.T, T2 = T * T;
+  float* Ag = reinterpret_cast<float*>(base + L.spec_off);
+  int* flags = reinterpret_cast<int*>(base + L.flags_off);
+  int* counter = reinterpret_cast<int*>(base + L.counter_off);
+  float* Xg = reinterpret_cast<float*>(base + L.xg_off);
+  float* D = reinterpret_cast<float*>(base + L.d_off);
+  if (tc.Kdp > 2 * Cin && cudaMemsetAsync(Ag, 0, tc.ag_b, s) != cudaSuccess) return OAA_ERR_CUDA;
+  {
+    const long long total = (long long)tc.F * Cin * Cout;
+    const int thr = 256;
+    const int blocks = (int)std::min<long long>((total + thr - 1) / thr, 8192);
+    oaa::oaa_realified_spectrum_kernel<<<blocks, thr, 0, s>>>(w, Ag, K, C, n, is_fwd ? 0 : 1, tc.Kdp);
+    g_launches++;
+    if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
+  }
+  oaa::TileSpecParams tp;
+  tp.in = in;
+  tp.Xg = Xg;
+  tp.Cin = Cin;
+  tp.R = e.R;
+  tp.T = T;
+  tp.Kdp = tc.Kdp;
+  tp.BW = e.BW;
+  tp.CSTR = n * e.BW + 4;
+  const size_t t1_smem = sizeof(float) * 16 * (size_t)tp.CSTR;
+  oaa::BinGemmParams gp;
+  gp.A = Ag;
+  gp.B = Xg;
+  gp.D = D;
+  gp.F = tc.F;
+  gp.M = 2 * Cout;
+  gp.Kd = tc.Kdp;
+  gp.strideA = (long long)2 * Cout * tc.Kdp;
+  oaa::EngineParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.out = out;
+  p.flags = flags;
+  p.counter = counter;
+  p.D = D;
+  p.Cin = 0;
+  p.Cout = Cout;
+  p.R = e.R;
+  p.T = T;
+  p.Ro = e.Ro;
+  p.off = e.off;
+  p.TS = e.TS;
+  p.BW = e.BW;
+  p.ncomp = e.ncomp;
+  p.CIG = 1;
+  ProfScope prof(is_fwd ? OAA_OP_FWD : OAA_OP_BWD_DATA, s);
+  prof.start();
+  for (int b0 = 0; b0 < B; b0 += tc.bc) {
+    const int bc = std::min(tc.bc, B - b0);
+    const long long btc = (long long)bc * T2;
+    tp.b0 = b0;
+    tp.bc = bc;
+    tp.BTc = btc;
+    if (launch_tile_spectra(n, tp, t1_smem, s) != cudaSuccess) return OAA_ERR_CUDA;
+    gp.N = (int)btc;
+    gp.ldd = (int)btc;
+    gp.strideB = btc * tc.Kdp;
+    gp.strideD = (long long)2 * Cout * btc;
+    if (launch_bin_gemm(gp, s) != cudaSuccess) return OAA_ERR_CUDA;
+    if (cudaMemsetAsync(flags, 0, L.xg_off - L.flags_off, s) != cudaSuccess) return OAA_ERR_CUDA;
+    p.B = bc;
+    p.b0 = b0;
+    p.BTc = (int)btc;
+    p.num_items = bc * T;
+    if (launch_engine(n, p, e, s) != cudaSuccess) return OAA_ERR_CUDA;
+  }
+  prof.stop();
+  (void)g;
+  return OAA_OK;
 }
 
 oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out, int B, int C,
@@ -232,10 +386,11 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
   const size_t w_bytes = sizeof(float) * (size_t)K * C * n * n;
   if (B > 0 && (overlaps(in, in_bytes, out, out_bytes) || overlaps(w, w_bytes, out, out_bytes)))
     return OAA_ERR_INVALID_VALUE;
+  const TcPlan tc = plan_tc(B, Cin, Cout, R, n);
   EnginePlan e;
-  if (!plan_engine(R, Ro, off, n, Cin, Cout, &e)) return OAA_ERR_UNSUPPORTED;
+  if (!plan_engine(R, Ro, off, n, Cin, Cout, &e, tc.use)) return OAA_ERR_UNSUPPORTED;
   if (B == 0) return OAA_OK;
-  EngineWs L = engine_ws(B, C, K, e.T, g);
+  EngineWs L = engine_ws(B, C, K, e.T, g, tc);
   if (!ws || ws_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0)
     return OAA_ERR_WORKSPACE;
   if (overlaps(ws, L.total, out, out_bytes) || overlaps(ws, L.total, in, in_bytes))
@@ -246,6 +401,7 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
   int* flags = reinterpret_cast<int*>(base + L.flags_off);
   int* counter = reinterpret_cast<int*>(base + L.counter_off);
 
+  if (tc.use) return run_engine_tc(is_fwd, in, w, out, B, C, K, n, g, e, tc, L, base, s);
   // kernel spectra: loop-major layout [Cloop][Cinner][P][H]
   const int loop_is_k = (is_fwd == e.S1) ? 1 : 0;  // fwd S1 / bwd_data S2 loop over k
   {
@@ -302,8 +458,9 @@ size_t oaa_conv_workspace_bytes(oaa_op_t op, int B, int C, int K, int N, int n, 
   if (validate(B, C, K, N, n, crop, &g) != OAA_OK) return 0;
   if (B == 0) return 0;
   if (op == OAA_OP_FWD || op == OAA_OP_BWD_DATA) {
-    const int R = op == OAA_OP_FWD ? N : g.M;
-    return engine_ws(B, C, K, cdiv(R, n), g).total;
+    const bool fwd = op == OAA_OP_FWD;
+    const int R = fwd ? N : g.M;
+    return engine_ws(B, C, K, cdiv(R, n), g, plan_tc(B, fwd ? C : K, fwd ? K : C, R, n)).total;
   }
   if (op == OAA_OP_BWD_FILTER) {
     FilterPlan f;
@@ -396,14 +553,7 @@ oaa_status_t oaa_debug_bin_gemm(const float* A, const float* B, float* D, int F,
   oaa::BinGemmParams p;
   p.A = A; p.B = B; p.D = D; p.F = F; p.M = M; p.N = N; p.Kd = Kd; p.ldd = N;
   p.strideA = (long long)M * Kd; p.strideB = (long long)N * Kd; p.strideD = (long long)M * N;
-  const size_t smem = 2 * 4 * 4096 * sizeof(float);
-  if (cudaFuncSetAttribute(oaa::oaa_bin_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
-    return OAA_ERR_CUDA;
-  dim3 grid(cdiv(N, oaa::kTcN), cdiv(M, oaa::kTcM), F);
-  oaa::oaa_bin_gemm_kernel<<<grid, 128, smem, static_cast<cudaStream_t>(stream)>>>(p);
-  g_launches++;
-  return cudaGetLastError() == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
+  return launch_bin_gemm(p, static_cast<cudaStream_t>(stream)) == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
 }
 
 const char* oaa_version(void) { return "oaa-b200 0.1.0 sm_100a"; }

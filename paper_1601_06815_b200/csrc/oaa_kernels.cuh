@@ -56,6 +56,10 @@ struct EngineParams {
   int B, Cin, Cout, R, T, Ro, off, TS, BW, num_items;
   int ncomp;            // compute threads; a trailing extra warp (if any) only publishes flags
   int CIG;              // S2: input channels staged per barrier
+  // tensor-core path (LY engine): Ŷ = D[f][m][bt] from the bin GEMM, items of the batch
+  // chunk starting at image b0 (item = (b − b0)·T + t1), BTc = tiles in the chunk
+  const float* D;
+  int BTc, b0;
 };
 
 struct FilterParams {
@@ -689,15 +693,20 @@ __host__ __device__ constexpr int s1t_alloc_cols(int n, int cr) {
 // the deferred overlap rows held in tensor memory instead of registers, so two CTAs
 // (16 warps) fit on an SM.  Same algorithm and protocol as oaa_engine_kernel<.., S1>.
 // Shared memory: Q[2][H][P][TS] float2 | spectra[3][Cin][P2][H] float4 | staged rows.
-template <int NN, int CR>
+//
+// LY = true: the "load-Ŷ" variant used after the tensor-core contraction (oaa_tc.cuh):
+// stage A reads this lane's spectrum row of Ŷ for output channel co from D instead of
+// contracting register / TMEM spectra; everything after (row IDFT, stage B, overlap-add
+// protocol) is shared.  TMEM then only holds the ring.
+template <int NN, int CR, bool LY>
 __global__ void __launch_bounds__(kMaxThreads, 2) oaa_engine_s1t_kernel(const EngineParams p) {
   constexpr int P = 2 * NN - 1, H = NN, P2 = (P + 1) / 2, TR = NN - 1;
   constexpr int NSB = 3;
   constexpr int TS = q_stride(NN);
   constexpr int XC = s1t_xcols(NN);                 // TMEM columns per channel
   constexpr int NX16 = XC / 16;
-  constexpr int RING0 = CR * XC;                    // first ring column
-  constexpr int ACOLS = s1t_alloc_cols(NN, CR);
+  constexpr int RING0 = LY ? 0 : CR * XC;           // first ring column
+  constexpr int ACOLS = s1t_alloc_cols(NN, LY ? 0 : CR);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_item;
   __shared__ uint32_t s_tmem;
@@ -739,10 +748,11 @@ __global__ void __launch_bounds__(kMaxThreads, 2) oaa_engine_s1t_kernel(const En
     __syncthreads();
     const int item = s_item;
     if (item >= p.num_items) break;
-    const int b = item / p.T, t1 = item - (item / p.T) * p.T;
+    const int bl = item / p.T, t1 = item - (item / p.T) * p.T;
+    const int b = bl + (LY ? p.b0 : 0);
     const bool has_pred = (t1 > 0) && (TR > 0);
     const int* pred_flag = p.flags + item - 1;
-    const float* in_b = p.in + (size_t)b * p.Cin * p.R * p.R;
+    const float* in_b = LY ? nullptr : p.in + (size_t)b * p.Cin * p.R * p.R;
     const int I0 = t1 * NN - p.off;
     int seen = 0, inflight = 0;
     unsigned rows = 0;
@@ -753,15 +763,17 @@ __global__ void __launch_bounds__(kMaxThreads, 2) oaa_engine_s1t_kernel(const En
     float* colp = p.out + (size_t)b * p.Cout * plane_sz + (ptrdiff_t)I0 * p.Ro + tid;
 
     // stage input rows + the first two spectra
-    for (int c = 0; c < p.Cin; ++c)
-      stage_rows(band + c * bandsz, BW, in_b + (size_t)c * p.R * p.R, p.R, t1 * NN, NN, 0, BW, tid, nthr);
-    for (int co = 0; co < 2 && co < p.Cout; ++co)
-      for (int e = tid; e < ssz; e += nthr) cp_async16(Ss + co * ssz + e, p.spec + (size_t)co * ssz + e);
+    if (!LY) {
+      for (int c = 0; c < p.Cin; ++c)
+        stage_rows(band + c * bandsz, BW, in_b + (size_t)c * p.R * p.R, p.R, t1 * NN, NN, 0, BW, tid, nthr);
+      for (int co = 0; co < 2 && co < p.Cout; ++co)
+        for (int e = tid; e < ssz; e += nthr) cp_async16(Ss + co * ssz + e, p.spec + (size_t)co * ssz + e);
+    }
     cp_async_commit();
     cp_async_wait_all();
     __syncthreads();
     // this lane's input row spectra → TMEM (lanes past the last tile store zeros)
-    if (warp * 32 < nthr) {
+    if (!LY) {
       float cf[NN], sf[NN];
 #pragma unroll
       for (int p1 = 0; p1 < NN; ++p1) {
@@ -869,8 +881,21 @@ __global__ void __launch_bounds__(kMaxThreads, 2) oaa_engine_s1t_kernel(const En
       __syncthreads();
       if (tid == pub_tid && cb > 0 && (cb % kTPublish) == 0) st_release(p.flags + item, cb);
     };
+    // LY: this lane's Ŷ row for output channel co (bins f = f1·P + f2, zero past the tiles)
+    const float* dlane = LY ? p.D + (size_t)(a_f1 * P) * 2 * p.Cout * p.BTc + (size_t)(bl * p.T + t1) * p.T + a_t
+                            : nullptr;
     auto stage_a = [&](int co) {
       float yr[P], yi[P];
+      if constexpr (LY) {
+#pragma unroll
+        for (int f2 = 0; f2 < P; ++f2) {
+          const float* d = dlane + ((size_t)f2 * 2 * p.Cout + co) * p.BTc;
+          yr[f2] = laneA ? __ldg(d) : 0.f;
+          yi[f2] = laneA ? __ldg(d + (size_t)p.Cout * p.BTc) : 0.f;
+        }
+        stage_a_store<NN>(yr, yi, Qs + (co & 1) * qsz + a_qoff);
+        return;
+      }
       const float4* S = Ss + (co % NSB) * ssz + a_f1;
       __syncwarp();  // tcgen05.ld is warp-collective: reconverge after divergent code
 #pragma unroll
@@ -902,7 +927,7 @@ __global__ void __launch_bounds__(kMaxThreads, 2) oaa_engine_s1t_kernel(const En
       stage_a_store<NN>(yr, yi, Qs + (co & 1) * qsz + a_qoff);
     };
     auto prefetch_spec = [&](int co) {
-      if (co + 2 < p.Cout)
+      if (!LY && co + 2 < p.Cout)
         for (int e = tid; e < ssz; e += nthr)
           cp_async16(Ss + ((co + 2) % NSB) * ssz + e, p.spec + (size_t)(co + 2) * ssz + e);
       cp_async_commit();
@@ -1203,3 +1228,85 @@ __global__ void oaa_spectrum_kernel(const float* __restrict__ w, float4* __restr
 #endif  // OAA_DEFINE_AUX_KERNELS
 
 }  // namespace oaa
+
+namespace oaa {
+
+// ------------------------------------------------------------------ operand producers
+// B operand of the bin GEMM: the forward spectra of every input block of a batch chunk,
+//   Xg[f][bt][kk],  f = f1·P + f2 (half spectrum, f1 < n), bt = (b−b0)·T² + t1·T + t2,
+//   kk < Cin: Re X̂_c, Cin ≤ kk < 2Cin: Im X̂_c, zero up to Kdp (a multiple of 4).
+struct TileSpecParams {
+  const float* in;  // [B][Cin][R][R]
+  float* Xg;        // [F][BTc][Kdp]
+  int Cin, R, T, b0, bc, Kdp, BW, CSTR;
+  long long BTc;
+};
+
+// One CTA per (image, tile row) of the chunk; lanes (channel cl of a group of 16, row
+// f1), channel fastest so the spectrum stores are coalesced along kk.
+template <int NN>
+__global__ void __launch_bounds__(128) oaa_tile_spectra_kernel(const TileSpecParams p) {
+  constexpr int P = 2 * NN - 1, CG = 16;
+  extern __shared__ __align__(16) float band[];  // [CG][NN][BW] (channel stride CSTR)
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int cl = tid % CG, f1 = tid / CG;
+  const int item = blockIdx.x;
+  const int bl = item / p.T, t1 = item - (item / p.T) * p.T;
+  const int b = p.b0 + bl;
+  float cf[NN], sf[NN];
+#pragma unroll
+  for (int p1 = 0; p1 < NN; ++p1) {
+    float s, c;
+    sincospif(2.0f * (float)((f1 * p1) % P) / (float)P, &s, &c);
+    cf[p1] = c;
+    sf[p1] = s;
+  }
+  const float* in_b = p.in + (size_t)b * p.Cin * p.R * p.R;
+  for (int c0 = 0; c0 < p.Cin; c0 += CG) {
+    const int ncg = min(CG, p.Cin - c0);
+    __syncthreads();
+    // stage rows t1·n .. +n of channels c0.. (warps own (channel,row) segments)
+    const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
+    for (int sgm = warp; sgm < ncg * NN; sgm += nwarps) {
+      const int ch = sgm / NN, rr = sgm - (sgm / NN) * NN;
+      const int r = t1 * NN + rr;
+      const bool rok = r < p.R;
+      const float* src = in_b + ((size_t)(c0 + ch) * p.R + (rok ? r : 0)) * p.R;
+      float* d = band + ch * p.CSTR + rr * p.BW;
+      for (int q = lane; q < p.BW; q += 32) {
+        const bool ok = rok && q < p.R;
+        cp_async4(d + q, ok ? src + q : in_b, ok);
+      }
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    if (f1 < NN && cl < ncg) {
+      const float* bsrc = band + cl * p.CSTR;
+      for (int t2 = 0; t2 < p.T; ++t2) {
+        float xr[P], xi[P];
+        block_row_spectrum_smem<NN>(bsrc, p.BW, t2 * NN, cf, sf, xr, xi);
+        const long long bt = (long long)(bl * p.T + t1) * p.T + t2;
+        float* dst = p.Xg + ((long long)(f1 * P) * p.BTc + bt) * p.Kdp + c0 + cl;
+#pragma unroll
+        for (int f2 = 0; f2 < P; ++f2) {
+          dst[(long long)f2 * p.BTc * p.Kdp] = xr[f2];
+          dst[(long long)f2 * p.BTc * p.Kdp + p.Cin] = xi[f2];
+        }
+      }
+    }
+  }
+  // zero the K padding columns (2Cin ≤ kk < Kdp) of this item's rows
+  const int pad = p.Kdp - 2 * p.Cin;
+  if (pad > 0) {
+    for (int e = tid; e < NN * P * p.T * pad; e += nthr) {
+      const int kk = e % pad, rest = e / pad;
+      const int t2 = rest % p.T, f = rest / p.T;
+      const long long bt = (long long)(bl * p.T + t1) * p.T + t2;
+      p.Xg[((long long)f * p.BTc + bt) * p.Kdp + 2 * p.Cin + kk] = 0.f;
+    }
+  }
+}
+
+}  // namespace oaa
+

@@ -18,6 +18,7 @@ extern std::atomic<uint64_t> g_launches;
 struct EnginePlan {
   int R, Ro, off, T, Cin, Cout, TS, BW, nthreads, ncomp, CR, CIG;
   bool S1;
+  bool LY;  // tensor-core path: the engine loads Ŷ computed by the bin GEMM
   size_t smem;
 };
 
@@ -44,9 +45,9 @@ cudaError_t launch_engine_t(const oaa::EngineParams& p, const EnginePlan& e, cud
 
 // S1 engine with TMEM-resident input spectra: occupancy is also bounded by tensor
 // memory (512 columns per SM).
-template <int NN, int CR>
+template <int NN, int CR, bool LY>
 cudaError_t launch_engine_s1t_t(const oaa::EngineParams& p, const EnginePlan& e, cudaStream_t s) {
-  auto k = oaa::oaa_engine_s1t_kernel<NN, CR>;
+  auto k = oaa::oaa_engine_s1t_kernel<NN, CR, LY>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem);
   if (err != cudaSuccess) return err;
   err = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -58,10 +59,10 @@ cudaError_t launch_engine_s1t_t(const oaa::EngineParams& p, const EnginePlan& e,
   // (the occupancy query under-reports here; over-subscribing a persistent grid is
   // harmless: surplus CTAs find no work item and exit)
   per_sm = std::max(1, std::max(per_sm, 2));
-  per_sm = std::min(per_sm, 512 / oaa::s1t_alloc_cols(NN, CR));
+  per_sm = std::min(per_sm, 512 / oaa::s1t_alloc_cols(NN, LY ? 0 : CR));
   const int grid = std::max(1, std::min(p.num_items, sms * per_sm));
   if (std::getenv("OAA_DEBUG"))
-    std::fprintf(stderr, "oaa s1t<%d,%d>: threads %d smem %zu per_sm %d grid %d\n", NN, CR, e.nthreads, e.smem, per_sm, grid);
+    std::fprintf(stderr, "oaa s1t<%d,%d,%d>: threads %d smem %zu per_sm %d grid %d\n", NN, CR, (int)LY, e.nthreads, e.smem, per_sm, grid);
   k<<<grid, e.nthreads, e.smem, s>>>(p);
   g_launches++;
   return cudaGetLastError();
@@ -69,12 +70,13 @@ cudaError_t launch_engine_s1t_t(const oaa::EngineParams& p, const EnginePlan& e,
 
 template <int NN>
 cudaError_t launch_engine_n(const oaa::EngineParams& p, const EnginePlan& e, cudaStream_t s) {
+  if (e.LY) return launch_engine_s1t_t<NN, 1, true>(p, e, s);
   if (e.S1) {
     switch (e.CR) {
-      case 1: return launch_engine_s1t_t<NN, 1>(p, e, s);
-      case 2: return launch_engine_s1t_t<NN, 2>(p, e, s);
-      case 3: return launch_engine_s1t_t<NN, 3>(p, e, s);
-      default: return launch_engine_s1t_t<NN, 4>(p, e, s);
+      case 1: return launch_engine_s1t_t<NN, 1, false>(p, e, s);
+      case 2: return launch_engine_s1t_t<NN, 2, false>(p, e, s);
+      case 3: return launch_engine_s1t_t<NN, 3, false>(p, e, s);
+      default: return launch_engine_s1t_t<NN, 4, false>(p, e, s);
     }
   } else {
     switch (e.CR) {
@@ -107,15 +109,27 @@ cudaError_t launch_filter_n(const oaa::FilterParams& p, const FilterPlan& f, cud
   }
 }
 
+template <int NN>
+cudaError_t launch_tile_spectra_n(const oaa::TileSpecParams& p, size_t smem, cudaStream_t s) {
+  auto k = oaa::oaa_tile_spectra_kernel<NN>;
+  cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  k<<<p.bc * p.T, 128, smem, s>>>(p);
+  g_launches++;
+  return cudaGetLastError();
+}
+
 #define OAA_DECLARE_N(NN)                                                                      \
   extern template cudaError_t launch_engine_n<NN>(const oaa::EngineParams&, const EnginePlan&, \
                                                   cudaStream_t);                              \
   extern template cudaError_t launch_filter_n<NN>(const oaa::FilterParams&, const FilterPlan&, \
-                                                  cudaStream_t);
+                                                  cudaStream_t);                              \
+  extern template cudaError_t launch_tile_spectra_n<NN>(const oaa::TileSpecParams&, size_t, cudaStream_t);
 #define OAA_INSTANTIATE_N(NN)                                                                 \
   template cudaError_t launch_engine_n<NN>(const oaa::EngineParams&, const EnginePlan&,       \
                                            cudaStream_t);                                     \
   template cudaError_t launch_filter_n<NN>(const oaa::FilterParams&, const FilterPlan&,       \
-                                           cudaStream_t);
+                                           cudaStream_t);                                     \
+  template cudaError_t launch_tile_spectra_n<NN>(const oaa::TileSpecParams&, size_t, cudaStream_t);
 
 }  // namespace oaa_host

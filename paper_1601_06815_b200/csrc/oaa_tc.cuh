@@ -217,3 +217,47 @@ __global__ void __launch_bounds__(128, 1) oaa_bin_gemm_kernel(const BinGemmParam
 }
 
 }  // namespace oaa
+
+#ifdef OAA_DEFINE_AUX_KERNELS
+namespace oaa {
+// A operand of the bin GEMM, the real-ified kernel spectra
+//   Ag[f][m][kk] = [[Wr, −Wi], [Wi, Wr]]  (rows m < Co | m ≥ Co, columns kk < Ci | kk ≥ Ci),
+// with W_{o,i}[f] = DFT_P(w_{o,i})[f1][f2] / P² (fwd: o = k, i = c) or of flip180(w_{k,c})
+// with o = c, i = k (bwd_data).  The K padding columns (2Ci ≤ kk < Kdp) are zeroed by the
+// caller.  One thread per (f, o, i), twiddles from a per-block fp64 table.
+__global__ void oaa_realified_spectrum_kernel(const float* __restrict__ w, float* __restrict__ Ag, int K, int C,
+                                              int n, int flip_bwd, int Kdp) {
+  const int P = 2 * n - 1, H = n, F = H * P;
+  const int Co = flip_bwd ? C : K, Ci = flip_bwd ? K : C;
+  __shared__ double tc[16], ts[16];
+  if (threadIdx.x < P) sincospi(2.0 * (double)threadIdx.x / (double)P, &ts[threadIdx.x], &tc[threadIdx.x]);
+  __syncthreads();
+  const long long total = (long long)F * Co * Ci;
+  const double inv = 1.0 / ((double)P * (double)P);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % Ci);
+    const int o = (int)((t / Ci) % Co);
+    const int f = (int)(t / ((long long)Ci * Co));
+    const int f1 = f / P, f2 = f - (f / P) * P;
+    const int k = flip_bwd ? i : o, c = flip_bwd ? o : i;
+    const float* wk = w + ((size_t)k * C + c) * n * n;
+    double sr = 0.0, si = 0.0;
+    for (int p1 = 0; p1 < n; ++p1)
+      for (int p2 = 0; p2 < n; ++p2) {
+        const float v = flip_bwd ? wk[(n - 1 - p1) * n + (n - 1 - p2)] : wk[p1 * n + p2];
+        const int mm = (f1 * p1 + f2 * p2) % P;
+        sr += (double)v * tc[mm];
+        si -= (double)v * ts[mm];
+      }
+    const float re = (float)(sr * inv), im = (float)(si * inv);
+    float* row_r = Ag + ((long long)f * 2 * Co + o) * Kdp;
+    float* row_i = row_r + (long long)Co * Kdp;
+    row_r[i] = re;
+    row_r[Ci + i] = -im;
+    row_i[i] = im;
+    row_i[Ci + i] = re;
+  }
+}
+}  // namespace oaa
+#endif

@@ -87,6 +87,21 @@ def test_channel_regimes(B, C, K, crop):
 
 
 @pytest.mark.parametrize("crop", CROPS)
+@pytest.mark.parametrize("B,C,K,N,n", [(2, 16, 20, 17, 3), (1, 17, 33, 29, 5), (3, 24, 16, 20, 8),
+                                       (2, 16, 16, 9, 1), (1, 20, 18, 40, 7), (2, 33, 17, 23, 2)])
+def test_tensor_core_path(B, C, K, N, n, crop):
+    """C ≥ 16 and K ≥ 16: fwd and bwd_data run tile spectra → tcgen05 bin GEMM (3×TF32)
+    → engine (LY mode); ragged 2C (K padding), ragged GEMM tiles, ragged spatial tails."""
+    if crop == "valid" and n > N:
+        pytest.skip("Valid needs n <= N")
+    d = make_inputs(B, C, K, N, n, crop, seed=B * 131 + C * 17 + K * 3 + n)
+    y, dx, dw = run_all(d, N, n, crop)
+    check(y, oracle.conv_fwd(d["x"], d["w"], crop), f"fwd tc {B,C,K,N,n}")
+    check(dx, oracle.conv_bwd_data(d["dy"], d["w"], N, crop), f"bwd_data tc {B,C,K,N,n}")
+    check(dw, oracle.conv_bwd_filter(d["x"], d["dy"], n, crop), "bwd_filter")
+
+
+@pytest.mark.parametrize("crop", CROPS)
 def test_config1_parity(crop):
     """BASELINE config 1: N=32, n=3, C=K=B=1, forward, vs CPU float64 direct."""
     c = CONFIGS["parity"]
