@@ -61,7 +61,9 @@ def lib():
                 f = getattr(L, name)
                 f.argtypes = [F, F, F, I, I, I, I, I, I, V, Z, V]
                 f.restype = I
-            L.oaa_debug_bin_gemm.argtypes = [F, F, F, I, I, I, I, V]
+            L.oaa_debug_bin_gemm_workspace_bytes.argtypes = [I, I, I, I]
+            L.oaa_debug_bin_gemm_workspace_bytes.restype = Z
+            L.oaa_debug_bin_gemm.argtypes = [F, F, F, I, I, I, I, V, Z, V]
             L.oaa_debug_bin_gemm.restype = I
             L.oaa_status_string.argtypes = [I]
             L.oaa_status_string.restype = ctypes.c_char_p
@@ -214,12 +216,15 @@ def debug_bin_gemm(A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:
     _check(A, "A", 3); _check(B, "B", 3)
     F, M, Kd = A.shape
     F2, N, Kd2 = B.shape
-    if F != F2 or Kd != Kd2 or Kd % 4:
-        raise ValueError("shape mismatch or Kd % 4 != 0")
+    if F != F2 or Kd != Kd2:
+        raise ValueError("shape mismatch")
     D = torch.empty((F, M, N), dtype=torch.float32, device=A.device)
     s = torch.cuda.current_stream(A.device)
+    nbytes = int(lib().oaa_debug_bin_gemm_workspace_bytes(F, M, N, Kd))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=A.device)
     st = lib().oaa_debug_bin_gemm(ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
-                                  ctypes.c_void_p(D.data_ptr()), F, M, N, Kd, ctypes.c_void_p(s.cuda_stream))
+                                  ctypes.c_void_p(D.data_ptr()), F, M, N, Kd, ctypes.c_void_p(ws.data_ptr()),
+                                  nbytes, ctypes.c_void_p(s.cuda_stream))
     if st != 0:
         raise OaAError(lib().oaa_status_string(st).decode())
     return D

@@ -224,7 +224,7 @@ constexpr size_t kTcChunkBytes = size_t(1) << 31;  // Xg + D per chunk
 
 struct TcPlan {
   bool use;
-  int F, T, Kdp, bc, nchunks;
+  int F, T, Kc, RTA, RTB, NB, bc, nchunks;  // K chunks of 32, row tiles of A and B, B tiles per CTA
   size_t ag_b, xg_b, d_b;
 };
 TcPlan plan_tc(int B, int Cin, int Cout, int R, int n) {
@@ -234,13 +234,16 @@ TcPlan plan_tc(int B, int Cin, int Cout, int R, int n) {
   const int P = 2 * n - 1;
   t.F = n * P;
   t.T = cdiv(R, n);
-  t.Kdp = cdiv(2 * Cin, 4) * 4;
-  const size_t per_img = sizeof(float) * (size_t)t.F * t.T * t.T * (t.Kdp + 2 * (size_t)Cout);
+  t.Kc = cdiv(2 * ((Cin + 3) & ~3), oaa::kTcK);
+  t.RTA = cdiv(2 * Cout, oaa::kTcM);
+  const size_t per_img = sizeof(float) * (size_t)t.F * t.T * t.T * (2 * (size_t)t.Kc * oaa::kTcK + 2 * (size_t)Cout);
   t.nchunks = (int)std::max<size_t>(1, (B * per_img + kTcChunkBytes - 1) / kTcChunkBytes);
   t.bc = cdiv(B, t.nchunks);
   t.nchunks = cdiv(B, t.bc);
-  t.ag_b = sizeof(float) * (size_t)t.F * 2 * Cout * t.Kdp;
-  t.xg_b = sizeof(float) * (size_t)t.F * t.bc * t.T * t.T * t.Kdp;
+  t.NB = t.bc * t.T * t.T > oaa::kTcM ? 2 : 1;
+  t.RTB = cdiv(cdiv(t.bc * t.T * t.T, oaa::kTcM), t.NB) * t.NB;
+  t.ag_b = sizeof(float) * (size_t)t.F * t.Kc * 2 * t.RTA * 4096;
+  t.xg_b = sizeof(float) * (size_t)t.F * t.Kc * 2 * t.RTB * 4096;
   t.d_b = sizeof(float) * (size_t)t.F * 2 * Cout * t.bc * t.T * t.T;
   return t;
 }
@@ -280,13 +283,66 @@ cudaError_t launch_tile_spectra(int n, const oaa::TileSpecParams& p, size_t smem
   return cudaErrorInvalidValue;
 }
 
+// tensor-core weight gradient: Ĝ / Ξ̂ spectra of a batch chunk →
+// split-K bin GEMM writing per-split partial dŴ → the fp64 finalize of the FFMA path.
+struct TcFiltPlan {
+  bool use;
+  int F, Td, T2, RTA, RTB, NB, bc, nchunks, Kc, S, kps, G, SWg, SWx;
+  size_t a_b, b_b, part_b;
+};
+TcFiltPlan plan_tc_filter(int B, int C, int K, int N, int M, int n) {
+  TcFiltPlan t{};
+  t.use = C >= kTcMinChannels && K >= kTcMinChannels;
+  if (!t.use || B < 1) return t;
+  const int P = 2 * n - 1;
+  t.F = n * P;
+  t.Td = cdiv(M, n);
+  t.T2 = t.Td * t.Td;
+  t.RTA = cdiv(K, oaa::kTcM);
+  t.NB = 2 * C > oaa::kTcM ? 2 : 1;
+  t.RTB = cdiv(cdiv(2 * C, oaa::kTcM), t.NB) * t.NB;
+  const size_t per_img = sizeof(float) * (size_t)t.F * 2 * t.T2 * 2 * 128 * (size_t)(t.RTA + t.RTB);
+  t.nchunks = (int)std::max<size_t>(1, (B * per_img + kTcChunkBytes - 1) / kTcChunkBytes);
+  t.bc = cdiv(B, t.nchunks);
+  t.nchunks = cdiv(B, t.bc);
+  t.Kc = cdiv(2 * t.bc * t.T2, oaa::kTcK);
+  // split-K for parallelism (≥ ~4 CTAs per SM); the splits are summed in fp64 by the
+  // finalize kernel, and inside a split the GEMM drains its TMEM accumulator every
+  // kTcDrain K chunks (oaa_tc.cuh).
+  const int tiles = t.F * t.RTA * cdiv(2 * C, oaa::kTcM * t.NB);
+  t.S = std::max(1, std::min(t.Kc, cdiv(4 * 148, tiles)));
+  t.kps = cdiv(t.Kc, t.S);
+  t.S = cdiv(t.Kc, t.kps);
+  t.G = t.S;  // chunks accumulate into the same per-split slabs, in stream order
+  t.SWg = cdiv(t.Td * n, 4) * 4;
+  t.SWx = cdiv(t.Td * n + n - 1, 4) * 4;
+  t.a_b = align_up(sizeof(float) * (size_t)t.F * t.Kc * 2 * t.RTA * 4096);
+  t.b_b = align_up(sizeof(float) * (size_t)t.F * t.Kc * 2 * t.RTB * 4096);
+  t.part_b = align_up(sizeof(float2) * (size_t)t.G * K * C * t.F);
+  return t;
+}
+
+cudaError_t launch_filter_spectra(int n, const oaa::FiltSpecParams& p, bool xwin, int items, size_t smem,
+                                  cudaStream_t s) {
+  switch (n) {
+    case 1: return launch_filter_spectra_n<1>(p, xwin, items, smem, s);
+    case 2: return launch_filter_spectra_n<2>(p, xwin, items, smem, s);
+    case 3: return launch_filter_spectra_n<3>(p, xwin, items, smem, s);
+    case 4: return launch_filter_spectra_n<4>(p, xwin, items, smem, s);
+    case 5: return launch_filter_spectra_n<5>(p, xwin, items, smem, s);
+    case 6: return launch_filter_spectra_n<6>(p, xwin, items, smem, s);
+    case 7: return launch_filter_spectra_n<7>(p, xwin, items, smem, s);
+    case 8: return launch_filter_spectra_n<8>(p, xwin, items, smem, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_bin_gemm(const oaa::BinGemmParams& p, cudaStream_t s) {
-  const size_t smem = 2 * 4 * 4096 * sizeof(float);
   cudaError_t err = cudaFuncSetAttribute(oaa::oaa_bin_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+                                         (int)oaa::kTcSmem);
   if (err != cudaSuccess) return err;
-  dim3 grid(cdiv(p.N, oaa::kTcN), cdiv(p.M, oaa::kTcM), p.F);
-  oaa::oaa_bin_gemm_kernel<<<grid, 128, smem, s>>>(p);
+  dim3 grid(cdiv(p.N, oaa::kTcM * p.NB), cdiv(p.M, oaa::kTcM), p.F * p.S);
+  oaa::oaa_bin_gemm_kernel<<<grid, oaa::kTcThreads, oaa::kTcSmem, s>>>(p);
   g_launches++;
   return cudaGetLastError();
 }
@@ -302,12 +358,12 @@ oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* 
   int* counter = reinterpret_cast<int*>(base + L.counter_off);
   float* Xg = reinterpret_cast<float*>(base + L.xg_off);
   float* D = reinterpret_cast<float*>(base + L.d_off);
-  if (tc.Kdp > 2 * Cin && cudaMemsetAsync(Ag, 0, tc.ag_b, s) != cudaSuccess) return OAA_ERR_CUDA;
+  if (cudaMemsetAsync(Ag, 0, tc.ag_b, s) != cudaSuccess) return OAA_ERR_CUDA;
   {
     const long long total = (long long)tc.F * Cin * Cout;
     const int thr = 256;
     const int blocks = (int)std::min<long long>((total + thr - 1) / thr, 8192);
-    oaa::oaa_realified_spectrum_kernel<<<blocks, thr, 0, s>>>(w, Ag, K, C, n, is_fwd ? 0 : 1, tc.Kdp);
+    oaa::oaa_realified_spectrum_kernel<<<blocks, thr, 0, s>>>(w, Ag, K, C, n, is_fwd ? 0 : 1, tc.Kc, tc.RTA);
     g_launches++;
     if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
   }
@@ -317,18 +373,25 @@ oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* 
   tp.Cin = Cin;
   tp.R = e.R;
   tp.T = T;
-  tp.Kdp = tc.Kdp;
+  tp.Kc = tc.Kc;
+  tp.RTB = tc.RTB;
   tp.BW = e.BW;
   tp.CSTR = n * e.BW + 4;
   const size_t t1_smem = sizeof(float) * 16 * (size_t)tp.CSTR;
-  oaa::BinGemmParams gp;
+  oaa::BinGemmParams gp{};
   gp.A = Ag;
   gp.B = Xg;
   gp.D = D;
   gp.F = tc.F;
   gp.M = 2 * Cout;
-  gp.Kd = tc.Kdp;
-  gp.strideA = (long long)2 * Cout * tc.Kdp;
+  gp.Kc = tc.Kc;
+  gp.RTA = tc.RTA;
+  gp.RTB = tc.RTB;
+  gp.S = 1;
+  gp.kps = tc.Kc;
+  gp.mode = 0;
+  gp.partial = nullptr;
+  gp.NB = tc.NB;
   oaa::EngineParams p;
   std::memset(&p, 0, sizeof(p));
   p.out = out;
@@ -352,11 +415,9 @@ oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* 
     const long long btc = (long long)bc * T2;
     tp.b0 = b0;
     tp.bc = bc;
-    tp.BTc = btc;
     if (launch_tile_spectra(n, tp, t1_smem, s) != cudaSuccess) return OAA_ERR_CUDA;
     gp.N = (int)btc;
     gp.ldd = (int)btc;
-    gp.strideB = btc * tc.Kdp;
     gp.strideD = (long long)2 * Cout * btc;
     if (launch_bin_gemm(gp, s) != cudaSuccess) return OAA_ERR_CUDA;
     if (cudaMemsetAsync(flags, 0, L.xg_off - L.flags_off, s) != cudaSuccess) return OAA_ERR_CUDA;
@@ -439,6 +500,56 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
   return err == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
 }
 
+oaa_status_t run_filter_tc(const float* x, const float* dy, float* dw, int B, int C, int K, int N, int n,
+                           const Geo& g, const TcFiltPlan& t, void* ws, size_t ws_bytes, cudaStream_t s,
+                           size_t x_bytes, size_t dy_bytes, size_t dw_bytes) {
+  const size_t need = t.a_b + t.b_b + t.part_b;
+  if (!ws || ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0) return OAA_ERR_WORKSPACE;
+  if (overlaps(ws, need, dw, dw_bytes) || overlaps(ws, need, x, x_bytes) || overlaps(ws, need, dy, dy_bytes))
+    return OAA_ERR_INVALID_VALUE;
+  char* base = static_cast<char*>(ws);
+  float* Ga = reinterpret_cast<float*>(base);
+  float* Xb = reinterpret_cast<float*>(base + t.a_b);
+  float* part = reinterpret_cast<float*>(base + t.a_b + t.b_b);
+  oaa::FiltSpecParams gs{};
+  gs.src = dy; gs.Op = Ga; gs.nch = K; gs.R = g.M; gs.Td = t.Td; gs.org = 0; gs.Kc = t.Kc; gs.RT = t.RTA;
+  gs.SW = t.SWg;
+  oaa::FiltSpecParams xs{};
+  xs.src = x; xs.Op = Xb; xs.nch = C; xs.R = N; xs.Td = t.Td; xs.org = g.o - (n - 1); xs.Kc = t.Kc;
+  xs.RT = t.RTB; xs.SW = t.SWx;
+  const size_t smem_g = sizeof(float) * 8 * n * (size_t)t.SWg;
+  const size_t smem_x = sizeof(float) * 8 * (2 * n - 1) * (size_t)t.SWx;
+  oaa::BinGemmParams gp{};
+  gp.A = Ga; gp.B = Xb; gp.D = nullptr; gp.F = t.F; gp.M = K; gp.N = 2 * C; gp.Kc = t.Kc; gp.RTA = t.RTA;
+  gp.RTB = t.RTB; gp.ldd = 0; gp.strideD = 0; gp.S = t.S; gp.kps = t.kps; gp.mode = 1; gp.Cf = C; gp.H = n;
+  gp.P = 2 * n - 1; gp.partial = part; gp.NB = t.NB;
+  ProfScope prof(OAA_OP_BWD_FILTER, s);
+  prof.start();
+  for (int ci = 0; ci < t.nchunks; ++ci) {
+    const int b0 = ci * t.bc, bc = std::min(t.bc, B - b0);
+    gs.b0 = b0;
+    xs.b0 = b0;
+    if (launch_filter_spectra(n, gs, false, bc * t.Td, smem_g, s) != cudaSuccess) return OAA_ERR_CUDA;
+    if (launch_filter_spectra(n, xs, true, bc * t.Td, smem_x, s) != cudaSuccess) return OAA_ERR_CUDA;
+    const int j0 = 2 * bc * t.T2;
+    if (j0 < 32 * t.Kc) {
+      oaa::oaa_tc_zero_tail_kernel<<<512, 256, 0, s>>>(Ga, t.F, t.Kc, t.RTA, j0);
+      oaa::oaa_tc_zero_tail_kernel<<<512, 256, 0, s>>>(Xb, t.F, t.Kc, t.RTB, j0);
+      g_launches += 2;
+      if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
+    }
+    gp.g0 = 0;
+    gp.accumulate = ci > 0;
+    if (launch_bin_gemm(gp, s) != cudaSuccess) return OAA_ERR_CUDA;
+  }
+  prof.stop();
+  const int bins = g.P * g.H;
+  oaa::oaa_filter_finalize_kernel<<<K * C, 128, sizeof(double2) * bins, s>>>(
+      reinterpret_cast<const float2*>(part), dw, t.G, K, C, n);
+  g_launches++;
+  return cudaGetLastError() == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
+}
+
 }  // namespace
 
 extern "C" {
@@ -463,6 +574,8 @@ size_t oaa_conv_workspace_bytes(oaa_op_t op, int B, int C, int K, int N, int n, 
     return engine_ws(B, C, K, cdiv(R, n), g, plan_tc(B, fwd ? C : K, fwd ? K : C, R, n)).total;
   }
   if (op == OAA_OP_BWD_FILTER) {
+    const TcFiltPlan t = plan_tc_filter(B, C, K, N, g.M, n);
+    if (t.use) return t.a_b + t.b_b + t.part_b;
     FilterPlan f;
     if (!plan_filter(B, C, K, g.M, n, &f)) return 0;
     return align_up(sizeof(float2) * (size_t)f.G * K * C * g.P * g.H);
@@ -499,6 +612,8 @@ oaa_status_t oaa_conv_bwd_filter(const float* x, const float* dy, float* dw, int
     if (cudaMemsetAsync(dw, 0, dw_bytes, s) != cudaSuccess) return OAA_ERR_CUDA;
     return OAA_OK;
   }
+  const TcFiltPlan tcf = plan_tc_filter(B, C, K, N, g.M, n);
+  if (tcf.use) return run_filter_tc(x, dy, dw, B, C, K, N, n, g, tcf, ws, ws_bytes, s, x_bytes, dy_bytes, dw_bytes);
   FilterPlan f;
   if (!plan_filter(B, C, K, g.M, n, &f)) return OAA_ERR_UNSUPPORTED;
   const size_t need = align_up(sizeof(float2) * (size_t)f.G * K * C * g.P * g.H);
@@ -547,13 +662,34 @@ const char* oaa_status_string(oaa_status_t s) {
   return "unknown oaa_status_t";
 }
 
-oaa_status_t oaa_debug_bin_gemm(const float* A, const float* B, float* D, int F, int M, int N, int Kd,
-                                void* stream) {
-  if (!A || !B || !D || F < 1 || M < 1 || N < 1 || Kd < 1 || (Kd & 3)) return OAA_ERR_INVALID_VALUE;
+size_t oaa_debug_bin_gemm_workspace_bytes(int F, int M, int N, int Kd) {
+  if (F < 1 || M < 1 || N < 1 || Kd < 1) return 0;
+  const size_t NB = N > oaa::kTcM ? 2 : 1;
+  const size_t Kc = cdiv(Kd, oaa::kTcK), RTA = cdiv(M, oaa::kTcM), RTB = (cdiv(cdiv(N, oaa::kTcM), (int)NB)) * NB;
+  return align_up(sizeof(float) * (size_t)F * Kc * 2 * RTA * 4096) + align_up(sizeof(float) * (size_t)F * Kc * 2 * RTB * 4096);
+}
+
+oaa_status_t oaa_debug_bin_gemm(const float* A, const float* B, float* D, int F, int M, int N, int Kd, void* ws,
+                                size_t ws_bytes, void* stream) {
+  if (!A || !B || !D || F < 1 || M < 1 || N < 1 || Kd < 1) return OAA_ERR_INVALID_VALUE;
+  const size_t need = oaa_debug_bin_gemm_workspace_bytes(F, M, N, Kd);
+  if (!ws || ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0) return OAA_ERR_WORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
   oaa::BinGemmParams p;
-  p.A = A; p.B = B; p.D = D; p.F = F; p.M = M; p.N = N; p.Kd = Kd; p.ldd = N;
-  p.strideA = (long long)M * Kd; p.strideB = (long long)N * Kd; p.strideD = (long long)M * N;
-  return launch_bin_gemm(p, static_cast<cudaStream_t>(stream)) == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
+  p.F = F; p.M = M; p.N = N; p.ldd = N;
+  p.NB = N > oaa::kTcM ? 2 : 1;
+  p.Kc = cdiv(Kd, oaa::kTcK); p.RTA = cdiv(M, oaa::kTcM); p.RTB = cdiv(cdiv(N, oaa::kTcM), p.NB) * p.NB;
+  p.strideD = (long long)M * N;
+  p.S = 1; p.kps = p.Kc; p.mode = 0; p.partial = nullptr; p.accumulate = 0;
+  float* Ap = static_cast<float*>(ws);
+  float* Bp = reinterpret_cast<float*>(static_cast<char*>(ws) + align_up(sizeof(float) * (size_t)F * p.Kc * 2 * p.RTA * 4096));
+  oaa::oaa_tc_pack_kernel<<<1024, 256, 0, s>>>(A, Ap, F, M, Kd, p.Kc, p.RTA);
+  g_launches++;
+  oaa::oaa_tc_pack_kernel<<<1024, 256, 0, s>>>(B, Bp, F, N, Kd, p.Kc, p.RTB);
+  g_launches++;
+  if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
+  p.A = Ap; p.B = Bp; p.D = D;
+  return launch_bin_gemm(p, s) == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
 }
 
 const char* oaa_version(void) { return "oaa-b200 0.1.0 sm_100a"; }

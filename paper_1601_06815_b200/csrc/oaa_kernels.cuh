@@ -882,17 +882,27 @@ __global__ void __launch_bounds__(kMaxThreads, 2) oaa_engine_s1t_kernel(const En
       if (tid == pub_tid && cb > 0 && (cb % kTPublish) == 0) st_release(p.flags + item, cb);
     };
     // LY: this lane's Ŷ row for output channel co (bins f = f1·P + f2, zero past the tiles)
+    // LY: this lane's Ŷ row (bins f1·P + f2) of the next output channel, loaded one
+    // channel ahead into registers so the loads fly during the previous channel's work
     const float* dlane = LY ? p.D + (size_t)(a_f1 * P) * 2 * p.Cout * p.BTc + (size_t)(bl * p.T + t1) * p.T + a_t
                             : nullptr;
-    auto stage_a = [&](int co) {
-      float yr[P], yi[P];
+    float yrn[LY ? P : 1], yin[LY ? P : 1];
+    auto load_y = [&](int co) {
       if constexpr (LY) {
 #pragma unroll
         for (int f2 = 0; f2 < P; ++f2) {
           const float* d = dlane + ((size_t)f2 * 2 * p.Cout + co) * p.BTc;
-          yr[f2] = laneA ? __ldg(d) : 0.f;
-          yi[f2] = laneA ? __ldg(d + (size_t)p.Cout * p.BTc) : 0.f;
+          yrn[f2] = laneA ? __ldg(d) : 0.f;
+          yin[f2] = laneA ? __ldg(d + (size_t)p.Cout * p.BTc) : 0.f;
         }
+      }
+    };
+    auto stage_a = [&](int co) {
+      float yr[P], yi[P];
+      if constexpr (LY) {
+#pragma unroll
+        for (int f2 = 0; f2 < P; ++f2) { yr[f2] = yrn[f2]; yi[f2] = yin[f2]; }
+        if (co + 1 < p.Cout) load_y(co + 1);
         stage_a_store<NN>(yr, yi, Qs + (co & 1) * qsz + a_qoff);
         return;
       }
@@ -933,6 +943,7 @@ __global__ void __launch_bounds__(kMaxThreads, 2) oaa_engine_s1t_kernel(const En
       cp_async_commit();
     };
 
+    if (LY && comp) load_y(0);
     if (comp) stage_a(0);
     prefetch_spec(0);
     sync_publish(0);
@@ -1232,40 +1243,58 @@ __global__ void oaa_spectrum_kernel(const float* __restrict__ w, float4* __restr
 namespace oaa {
 
 // ------------------------------------------------------------------ operand producers
-// B operand of the bin GEMM: the forward spectra of every input block of a batch chunk,
-//   Xg[f][bt][kk],  f = f1·P + f2 (half spectrum, f1 < n), bt = (b−b0)·T² + t1·T + t2,
-//   kk < Cin: Re X̂_c, Cin ≤ kk < 2Cin: Im X̂_c, zero up to Kdp (a multiple of 4).
+// Operands of the tensor-core bin GEMM (oaa_tc.cuh) are written pre-split (3×TF32:
+// x = hi + lo, hi = x with the low 13 mantissa bits cleared) in the UMMA-blocked layout
+//   Op[f][kc][h][rt][4096 floats],  kc = k/32, h = hi|lo, rt = r/128,
+// each block a 128-row × 32-k tile in canonical no-swizzle K-major order.
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+  hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  lo = x - hi;
+}
+__device__ __forceinline__ size_t tc_idx(int f, int Kc, int RT, int h, int r, int k) {
+  return ((((size_t)f * Kc + (k >> 5)) * 2 + h) * RT + (r >> 7)) * 4096 + ((r & 127) >> 3) * 256 +
+         ((k & 31) >> 2) * 32 + (r & 7) * 4 + (k & 3);
+}
+__device__ __forceinline__ void tc_put(float* Op, int f, int Kc, int RT, int r, int k, float v) {
+  float hi, lo;
+  split_tf32(v, hi, lo);
+  Op[tc_idx(f, Kc, RT, 0, r, k)] = hi;
+  Op[tc_idx(f, Kc, RT, 1, r, k)] = lo;
+}
+
+// B operand: the forward spectra of every input block of a batch chunk, row
+// bt = (b−b0)·T² + t1·T + t2, column c < Cin: Re X̂_c, Cinp + c: Im X̂_c (Cinp = Cin
+// rounded up to 4), zero elsewhere up to 32·Kc; bin f = f1·P + f2 (half spectrum, f1 < n).
 struct TileSpecParams {
   const float* in;  // [B][Cin][R][R]
-  float* Xg;        // [F][BTc][Kdp]
-  int Cin, R, T, b0, bc, Kdp, BW, CSTR;
-  long long BTc;
+  float* Xg;        // blocked [F][Kc][2][RTB][4096]
+  int Cin, R, T, b0, bc, Kc, RTB, BW, CSTR;
 };
 
-// One CTA per (image, tile row) of the chunk; lanes (channel cl of a group of 16, row
-// f1), channel fastest so the spectrum stores are coalesced along kk.
+// One CTA per (image, tile row) of the chunk.  A task is (f1, tile t2, quad of 4
+// channels): its spectra go out as float4 (4 consecutive columns of one row), and the 8
+// lanes of consecutive tiles of a warp fill whole 128-byte lines of the blocked layout.
 template <int NN>
 __global__ void __launch_bounds__(128) oaa_tile_spectra_kernel(const TileSpecParams p) {
   constexpr int P = 2 * NN - 1, CG = 16;
   extern __shared__ __align__(16) float band[];  // [CG][NN][BW] (channel stride CSTR)
+  __shared__ float2 tw[16];
   const int tid = threadIdx.x, nthr = blockDim.x;
-  const int cl = tid % CG, f1 = tid / CG;
+  if (tid < P) {
+    float sn, cs;
+    sincospif(2.0f * (float)tid / (float)P, &sn, &cs);
+    tw[tid] = make_float2(cs, sn);
+  }
   const int item = blockIdx.x;
   const int bl = item / p.T, t1 = item - (item / p.T) * p.T;
   const int b = p.b0 + bl;
-  float cf[NN], sf[NN];
-#pragma unroll
-  for (int p1 = 0; p1 < NN; ++p1) {
-    float s, c;
-    sincospif(2.0f * (float)((f1 * p1) % P) / (float)P, &s, &c);
-    cf[p1] = c;
-    sf[p1] = s;
-  }
+  const int bt0 = (bl * p.T + t1) * p.T;
+  const int Cinp = (p.Cin + 3) & ~3;
+  const int TH8 = (p.T + 7) >> 3;
   const float* in_b = p.in + (size_t)b * p.Cin * p.R * p.R;
-  for (int c0 = 0; c0 < p.Cin; c0 += CG) {
+  for (int c0 = 0; c0 < Cinp; c0 += CG) {
     const int ncg = min(CG, p.Cin - c0);
     __syncthreads();
-    // stage rows t1·n .. +n of channels c0.. (warps own (channel,row) segments)
     const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
     for (int sgm = warp; sgm < ncg * NN; sgm += nwarps) {
       const int ch = sgm / NN, rr = sgm - (sgm / NN) * NN;
@@ -1281,32 +1310,197 @@ __global__ void __launch_bounds__(128) oaa_tile_spectra_kernel(const TileSpecPar
     cp_async_commit();
     cp_async_wait_all();
     __syncthreads();
-    if (f1 < NN && cl < ncg) {
-      const float* bsrc = band + cl * p.CSTR;
-      for (int t2 = 0; t2 < p.T; ++t2) {
-        float xr[P], xi[P];
-        block_row_spectrum_smem<NN>(bsrc, p.BW, t2 * NN, cf, sf, xr, xi);
-        const long long bt = (long long)(bl * p.T + t1) * p.T + t2;
-        float* dst = p.Xg + ((long long)(f1 * P) * p.BTc + bt) * p.Kdp + c0 + cl;
+    const int ntask = NN * TH8 * 32;
+    for (int u = tid; u < ntask; u += nthr) {
+      const int t2 = ((u >> 5) % TH8) * 8 + (u & 7), cq = (u >> 3) & 3, f1 = (u >> 5) / TH8;
+      const int cb = c0 + 4 * cq;
+      if (t2 >= p.T || cb >= Cinp) continue;
+      float cf[NN], sf[NN];
 #pragma unroll
-        for (int f2 = 0; f2 < P; ++f2) {
-          dst[(long long)f2 * p.BTc * p.Kdp] = xr[f2];
-          dst[(long long)f2 * p.BTc * p.Kdp + p.Cin] = xi[f2];
+      for (int p1 = 0; p1 < NN; ++p1) {
+        const float2 t = tw[(f1 * p1) % P];
+        cf[p1] = t.x;
+        sf[p1] = t.y;
+      }
+      float xr[4][P], xi[4][P];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (cb + i < p.Cin) {
+          block_row_spectrum_smem<NN>(band + (cb + i - c0) * p.CSTR, p.BW, t2 * NN, cf, sf, xr[i], xi[i]);
+        } else {
+#pragma unroll
+          for (int f2 = 0; f2 < P; ++f2) { xr[i][f2] = 0.f; xi[i][f2] = 0.f; }
+        }
+      }
+      const int bt = bt0 + t2;
+#pragma unroll
+      for (int f2 = 0; f2 < P; ++f2) {
+        const int f = f1 * P + f2;
+        float h[4], l[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) split_tf32(xr[i][f2], h[i], l[i]);
+        *reinterpret_cast<float4*>(p.Xg + tc_idx(f, p.Kc, p.RTB, 0, bt, cb)) = make_float4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<float4*>(p.Xg + tc_idx(f, p.Kc, p.RTB, 1, bt, cb)) = make_float4(l[0], l[1], l[2], l[3]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) split_tf32(xi[i][f2], h[i], l[i]);
+        *reinterpret_cast<float4*>(p.Xg + tc_idx(f, p.Kc, p.RTB, 0, bt, Cinp + cb)) = make_float4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<float4*>(p.Xg + tc_idx(f, p.Kc, p.RTB, 1, bt, Cinp + cb)) = make_float4(l[0], l[1], l[2], l[3]);
+      }
+    }
+  }
+  // zero the K padding columns (2·Cinp ≤ kk < 32·Kc) of this item's rows
+  const int padq = (32 * p.Kc - 2 * Cinp) >> 2;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int e = tid; e < NN * P * p.T * padq; e += nthr) {
+    const int qq = e % padq, rest = e / padq;
+    const int t2 = rest % p.T, f = rest / p.T;
+    *reinterpret_cast<float4*>(p.Xg + tc_idx(f, p.Kc, p.RTB, 0, bt0 + t2, 2 * Cinp + 4 * qq)) = z;
+    *reinterpret_cast<float4*>(p.Xg + tc_idx(f, p.Kc, p.RTB, 1, bt0 + t2, 2 * Cinp + 4 * qq)) = z;
+  }
+}
+
+// Operands of the tensor-core weight gradient:
+//   dŴ[f][k][c] = Σ_bt conj(Ĝ[f][k][bt])·Ξ̂[f][c][bt]
+// as one real GEMM per bin with the reduction index j = 2·bt + {0: re, 1: im}:
+//   A rows k      : (Gr, Gi)                       (G mode: n×n dy blocks)
+//   B rows c      : (Xr, Xi)  → D[k][c]   = Re dŴ   (X mode: (2n−1)² x windows)
+//   B rows C + c  : (Xi, −Xr) → D[k][C+c] = Im dŴ
+// bt = (b − b0)·Td² + t1·Td + t2 over the dy blocks of a batch chunk; the x window of
+// block (t1, t2) starts at (t1·n + org, t2·n + org), org = o − (n−1) (zero outside x).
+struct FiltSpecParams {
+  const float* src;  // dy [B][K][M][M] (G) or x [B][C][N][N] (X)
+  float* Op;         // blocked [F][Kc][2][RT][4096]
+  int nch, R, Td, org, b0, Kc, RT, SW;
+};
+
+template <int NN, bool XWIN>
+__global__ void __launch_bounds__(256) oaa_filter_spectra_kernel(const FiltSpecParams p) {
+  constexpr int P = 2 * NN - 1, H = NN, ROWS = XWIN ? P : NN, CG = 8;
+  extern __shared__ __align__(16) float band[];  // [CG][ROWS][SW]
+  const int tid = threadIdx.x;
+  const int kl = tid & 7, grp = tid >> 3;        // channel within group, lane group
+  const int f1 = grp % H, tsub = grp / H, nsub = 32 / H;
+  const int item = blockIdx.x;
+  const int bl = item / p.Td, t1 = item - (item / p.Td) * p.Td;
+  const int b = p.b0 + bl;
+  const int bt0 = (bl * p.Td + t1) * p.Td;
+  float tcx[ROWS], tsx[ROWS];  // e^{−2πi f1 p1 / P} for the column stage
+#pragma unroll
+  for (int p1 = 0; p1 < ROWS; ++p1) {
+    float sn, cs;
+    sincospif(2.0f * (float)((f1 * p1) % P) / (float)P, &sn, &cs);
+    tcx[p1] = cs;
+    tsx[p1] = sn;
+  }
+  const size_t plane = (size_t)p.R * p.R;
+  const int r0 = t1 * NN + p.org;
+  const int q_lo = bt0 >> 1, q_hi = (bt0 + p.Td - 1) >> 1;
+  for (int c0 = 0; c0 < p.nch; c0 += CG) {
+    const int ncg = min(CG, p.nch - c0);
+    __syncthreads();
+    {
+      const int lane = tid & 31, warp = tid >> 5;
+      const float* base = p.src + ((size_t)b * p.nch + c0) * plane;
+      for (int sg = warp; sg < ncg * ROWS; sg += 8) {
+        const int ch = sg / ROWS, rr = sg - (sg / ROWS) * ROWS;
+        const int r = r0 + rr;
+        const bool rok = r >= 0 && r < p.R;
+        const float* srow = base + ch * plane + (size_t)(rok ? r : 0) * p.R;
+        float* d = band + (ch * ROWS + rr) * p.SW;
+        for (int q = lane; q < p.SW; q += 32) {
+          const int col = q + p.org;
+          const bool ok = rok && col >= 0 && col < p.R;
+          cp_async4(d + q, ok ? srow + col : base, ok);
+        }
+      }
+      cp_async_commit();
+      cp_async_wait_all();
+      __syncthreads();
+    }
+    if (kl >= ncg || tsub >= nsub) continue;
+    const float* bsrc = band + kl * ROWS * p.SW;
+    const int ch = c0 + kl;
+    for (int q = q_lo + tsub; q <= q_hi; q += nsub) {
+      float sr[2][P], si[2][P];
+      bool have[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int bt = 2 * q + h;
+        have[h] = bt >= bt0 && bt < bt0 + p.Td;
+        const int t2 = have[h] ? bt - bt0 : 0;
+        if constexpr (!XWIN) {
+          float cf[NN], sf[NN];
+#pragma unroll
+          for (int p1 = 0; p1 < NN; ++p1) { cf[p1] = tcx[p1]; sf[p1] = tsx[p1]; }
+          block_row_spectrum_smem<NN>(bsrc, p.SW, t2 * NN, cf, sf, sr[h], si[h]);
+        } else {
+          const float* w = bsrc + t2 * NN;
+          float rr[P], ri[P];
+#pragma unroll
+          for (int p2 = 0; p2 < P; ++p2) {
+            float a = w[p2], bb = 0.f;
+#pragma unroll
+            for (int p1 = 1; p1 < P; ++p1) {
+              const float v = w[p1 * p.SW + p2];
+              a = fmaf(v, tcx[p1], a);
+              bb = fmaf(-v, tsx[p1], bb);
+            }
+            rr[p2] = a;
+            ri[p2] = bb;
+          }
+          dft<P, -1>(rr, ri, sr[h], si[h]);
+        }
+      }
+#pragma unroll
+      for (int f2 = 0; f2 < P; ++f2) {
+        const int f = f1 * P + f2;
+        // row ch: (re, im) pairs; X mode also row nch + ch: (im, −re)
+#pragma unroll
+        for (int rowk = 0; rowk < (XWIN ? 2 : 1); ++rowk) {
+          float v[4];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            v[2 * h] = rowk == 0 ? sr[h][f2] : si[h][f2];
+            v[2 * h + 1] = rowk == 0 ? si[h][f2] : -sr[h][f2];
+          }
+          const int row = ch + rowk * p.nch;
+          float hi[4], lo[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) split_tf32(v[e], hi[e], lo[e]);
+          float* dh = p.Op + tc_idx(f, p.Kc, p.RT, 0, row, 4 * q);
+          float* dl = p.Op + tc_idx(f, p.Kc, p.RT, 1, row, 4 * q);
+          if (have[0] && have[1]) {
+            *reinterpret_cast<float4*>(dh) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+            *reinterpret_cast<float4*>(dl) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+          } else if (have[0]) {
+            *reinterpret_cast<float2*>(dh) = make_float2(hi[0], hi[1]);
+            *reinterpret_cast<float2*>(dl) = make_float2(lo[0], lo[1]);
+          } else {
+            *reinterpret_cast<float2*>(dh + 2) = make_float2(hi[2], hi[3]);
+            *reinterpret_cast<float2*>(dl + 2) = make_float2(lo[2], lo[3]);
+          }
         }
       }
     }
   }
-  // zero the K padding columns (2Cin ≤ kk < Kdp) of this item's rows
-  const int pad = p.Kdp - 2 * p.Cin;
-  if (pad > 0) {
-    for (int e = tid; e < NN * P * p.T * pad; e += nthr) {
-      const int kk = e % pad, rest = e / pad;
-      const int t2 = rest % p.T, f = rest / p.T;
-      const long long bt = (long long)(bl * p.T + t1) * p.T + t2;
-      p.Xg[((long long)f * p.BTc + bt) * p.Kdp + 2 * p.Cin + kk] = 0.f;
-    }
+}
+
+#ifdef OAA_DEFINE_AUX_KERNELS
+// Zero the reduction tail j ∈ [j0, 32·Kc) of every row of a blocked operand.
+__global__ void oaa_tc_zero_tail_kernel(float* Op, int F, int Kc, int RT, int j0) {
+  const int tail = 32 * Kc - j0;
+  if (tail <= 0) return;
+  const long long total = (long long)F * 2 * RT * 128 * tail;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int j = j0 + (int)(t % tail);
+    const int r = (int)((t / tail) % (RT * 128));
+    const int h = (int)((t / ((long long)tail * RT * 128)) % 2);
+    const int f = (int)(t / ((long long)tail * RT * 128 * 2));
+    Op[tc_idx(f, Kc, RT, h, r, j)] = 0.f;
   }
 }
 
-}  // namespace oaa
+#endif  // OAA_DEFINE_AUX_KERNELS
 
+}  // namespace oaa

@@ -119,17 +119,29 @@ cudaError_t launch_tile_spectra_n(const oaa::TileSpecParams& p, size_t smem, cud
   return cudaGetLastError();
 }
 
+template <int NN>
+cudaError_t launch_filter_spectra_n(const oaa::FiltSpecParams& p, bool xwin, int items, size_t smem, cudaStream_t s) {
+  auto k = xwin ? oaa::oaa_filter_spectra_kernel<NN, true> : oaa::oaa_filter_spectra_kernel<NN, false>;
+  cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  k<<<items, 256, smem, s>>>(p);
+  g_launches++;
+  return cudaGetLastError();
+}
+
 #define OAA_DECLARE_N(NN)                                                                      \
   extern template cudaError_t launch_engine_n<NN>(const oaa::EngineParams&, const EnginePlan&, \
                                                   cudaStream_t);                              \
   extern template cudaError_t launch_filter_n<NN>(const oaa::FilterParams&, const FilterPlan&, \
                                                   cudaStream_t);                              \
-  extern template cudaError_t launch_tile_spectra_n<NN>(const oaa::TileSpecParams&, size_t, cudaStream_t);
+  extern template cudaError_t launch_tile_spectra_n<NN>(const oaa::TileSpecParams&, size_t, cudaStream_t); \
+  extern template cudaError_t launch_filter_spectra_n<NN>(const oaa::FiltSpecParams&, bool, int, size_t, cudaStream_t);
 #define OAA_INSTANTIATE_N(NN)                                                                 \
   template cudaError_t launch_engine_n<NN>(const oaa::EngineParams&, const EnginePlan&,       \
                                            cudaStream_t);                                     \
   template cudaError_t launch_filter_n<NN>(const oaa::FilterParams&, const FilterPlan&,       \
                                            cudaStream_t);                                     \
-  template cudaError_t launch_tile_spectra_n<NN>(const oaa::TileSpecParams&, size_t, cudaStream_t);
+  template cudaError_t launch_tile_spectra_n<NN>(const oaa::TileSpecParams&, size_t, cudaStream_t); \
+  template cudaError_t launch_filter_spectra_n<NN>(const oaa::FiltSpecParams&, bool, int, size_t, cudaStream_t);
 
 }  // namespace oaa_host

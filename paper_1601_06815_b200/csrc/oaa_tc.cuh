@@ -5,33 +5,51 @@
 // For every bin f the contraction Ŷ_f = Ŵ_f · X̂_f (K×C complex by C×B·T complex) is
 // real-ified,
 //      [Yr; Yi] (2K × N) = [[Wr, −Wi], [Wi, Wr]] (2K × 2C) · [Xr; Xi] (2C × N),
-// and evaluated as D[f] = A[f] · B[f]ᵀ with A[f] = M×Kd, B[f] = N×Kd (both K-major, fp32
-// in global memory).  fp32 accuracy (rel-L2 ≤ 1e-5, R9) needs 3×TF32: every
-// operand is split x = hi + lo (hi = x with the low 13 mantissa bits cleared, lo = x − hi)
-// and D = A_hi·B_hi + A_hi·B_lo + A_lo·B_hi accumulates in tensor memory.
+// and evaluated as D[f] = A[f] · B[f]ᵀ (A[f] M×Kd, B[f] N×Kd, both K-major).  fp32
+// accuracy (rel-L2 ≤ 1e-5, R9) needs 3×TF32: every operand is split
+// x = hi + lo (hi = x with the low 13 mantissa bits cleared, lo = x − hi) and
+// D = A_lo·B_hi + A_hi·B_lo + A_hi·B_hi accumulates in tensor memory.
 //
-// Kernel structure (one CTA = one 128×128 output tile of one bin, 128 threads):
-//   * all threads load a 128×32 chunk of A and of B, split hi/lo and store them into shared
-//     memory in the canonical no-swizzle K-major UMMA layout (8-row × 16-byte core
-//     matrices; LBO = 128 B between the two K halves of an MMA, SBO = 1 KB between 8-row
-//     groups), double buffered so the next chunk loads while the MMAs of this one run;
-//   * one elected thread issues 4 k-steps × 3 tcgen05.mma.kind::tf32 (M=128, N=128, K=8)
-//     per chunk and commits them to an mbarrier;
-//   * epilogue: tcgen05.ld of the 128×128 fp32 accumulator (thread = row) → global.
+// Operands arrive pre-split in the UMMA-blocked layout written by their producers
+// (tile spectra / real-ified weights, oaa_kernels.cuh): for each (bin, 32-wide K chunk,
+// hi|lo) the row tiles of 128 rows are consecutive 16 KB blocks in the canonical
+// no-swizzle K-major order (8-row × 16-byte core matrices: LBO = 128 B between the two K
+// halves of an MMA, SBO = 1 KB between 8-row groups).  So every pipeline stage is four
+// plain bulk copies (cp.async.bulk, TMA engine) and no thread touches operand data.
+//
+// Kernel (one CTA = one 128 × 256 output tile of one bin, 128 threads, 1 CTA/SM):
+//   * warp 0 lane 0: producer -- per K chunk waits for the stage to be free, posts the
+//     byte count on the stage's "full" mbarrier and issues the bulk copies;
+//   * warp 1 lane 0: MMA issuer -- waits "full", issues 4 k-steps × 3 tcgen05.mma
+//     .kind::tf32 (M=128, N=256, K=8) and commits them to the stage's "empty" mbarrier;
+//   * all 4 warps: epilogue, tcgen05.ld of the 128 × 256 fp32 accumulator (thread = row).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "oaa_kernels.cuh"
+
 namespace oaa {
 
-constexpr int kTcM = 128, kTcN = 128, kTcK = 32;  // CTA tile and K chunk (fp32 elements)
+constexpr int kTcM = 128, kTcN = 256, kTcK = 32;  // CTA tile and K chunk (fp32 elements)
+constexpr int kTcStages = 2;
+constexpr size_t kTcStageBytes = (size_t)(2 * kTcM + 2 * kTcN) * kTcK * sizeof(float);  // 96 KB
+constexpr size_t kTcSmem = kTcStages * kTcStageBytes;
 
 struct BinGemmParams {
-  const float* A;  // [F][M][Kd]
-  const float* B;  // [F][N][Kd]
+  const float* A;  // blocked [F][Kc][2][RTA][4096]
+  const float* B;  // blocked [F][Kc][2][RTB][4096]  (RTB even)
   float* D;        // [F][M][ldd] (row m, column n)
-  int F, M, N, Kd, ldd;
-  long long strideA, strideB, strideD;  // per-bin strides (elements)
+  int F, M, N, Kc, RTA, RTB, ldd;
+  long long strideD;  // per-bin stride of D (elements)
+  // split-K: grid.z = F·S, split s reduces K chunks [s·kps, min(Kc, (s+1)·kps))
+  int S, kps;
+  // mode 1 (weight gradient): instead of D, write the split's partial dŴ in the layout of
+  // oaa_filter_finalize_kernel, partial[g0+s][k=m][c][f2·H+f1] (float2), columns
+  // n < Cf → real part of c = n, n ≥ Cf → imaginary part of c = n − Cf.
+  int mode, Cf, H, P, g0, accumulate;
+  float* partial;
+  int NB;  // B row tiles per CTA (1: N tile 128, 2: N tile 256); RTB is a multiple of NB
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -47,7 +65,7 @@ __device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr, uint32_t lb
   return d;
 }
 
-// Instruction descriptor: D f32, A/B tf32, both K-major, M=128, N=128.
+// Instruction descriptor: D f32, A/B tf32, both K-major.
 __host__ __device__ constexpr uint32_t umma_idesc_tf32(int M, int N) {
   return (1u << 4)                 // c_format = F32
          | (2u << 7)               // a_format = TF32
@@ -68,6 +86,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// 1-D bulk copy global → shared (TMA engine), completion counted on `bar` in bytes.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void umma_tf32(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                           uint32_t accumulate) {
   asm volatile(
@@ -82,153 +112,192 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
-// Split fp32 → (tf32 hi, fp32 remainder).  The tensor core reads the top 19 bits of each
-// fp32 operand, so hi is exact and lo carries the next 11+ bits.
-__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-  hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-  lo = x - hi;
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t ta, float (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]),
+        "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15]),
+        "=f"(v[16]), "=f"(v[17]), "=f"(v[18]), "=f"(v[19]), "=f"(v[20]), "=f"(v[21]), "=f"(v[22]), "=f"(v[23]),
+        "=f"(v[24]), "=f"(v[25]), "=f"(v[26]), "=f"(v[27]), "=f"(v[28]), "=f"(v[29]), "=f"(v[30]), "=f"(v[31])
+      : "r"(ta));
 }
 
-// Store a 128-row × 32-element fp32 chunk (row stride ld elements in global, rows r0..)
-// as hi and lo tiles in the canonical K-major no-swizzle layout:
-//   byte offset of (row r, k) = (r/8)·1024 + (k/4)·128 + (r%8)·16 + (k%4)·4
-// Rows ≥ nrows and columns ≥ kvalid are zero.
-__device__ __forceinline__ void load_split_tile(const float* __restrict__ g, long long ld, int nrows, int kvalid,
-                                                float* hi, float* lo, int tid) {
-  // 128 rows × 8 chunks of 4 → 1024 float4 slots, 128 threads → 8 each
-#pragma unroll
-  for (int it = 0; it < 8; ++it) {
-    const int slot = it * 128 + tid;
-    const int r = slot >> 3, c = slot & 7;  // row, k-chunk
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (r < nrows) {
-      const float* src = g + (long long)r * ld + 4 * c;
-      if (4 * c + 3 < kvalid) {
-        v = *reinterpret_cast<const float4*>(src);
-      } else {
-        if (4 * c + 0 < kvalid) v.x = src[0];
-        if (4 * c + 1 < kvalid) v.y = src[1];
-        if (4 * c + 2 < kvalid) v.z = src[2];
-      }
-    }
-    float4 h, l;
-    split_tf32(v.x, h.x, l.x);
-    split_tf32(v.y, h.y, l.y);
-    split_tf32(v.z, h.z, l.z);
-    split_tf32(v.w, h.w, l.w);
-    const int off = (r >> 3) * 256 + c * 32 + (r & 7) * 4;  // in floats
-    *reinterpret_cast<float4*>(hi + off) = h;
-    *reinterpret_cast<float4*>(lo + off) = l;
-  }
-}
+// K chunks accumulated in one TMEM accumulator before it is drained into registers.  The
+// tensor core's fp32 accumulation truncates, so its error grows with the number of
+// accumulate steps; draining every kTcDrain chunks and summing the drained values with
+// round-to-nearest FADDs keeps long reductions (the weight gradient's B·T′) at fp32
+// accuracy.
+constexpr int kTcDrain = 8;
+constexpr int kTcThreads = 320;  // warp 0 TMA producer, warp 1 MMA issuer, warps 2..9 drain/epilogue
 
-// D[f][m][n] = Σ_k A[f][m][k] · B[f][n][k]  (3×TF32).  grid = (ceil(N/128), ceil(M/128), F)
-__global__ void __launch_bounds__(128, 1) oaa_bin_gemm_kernel(const BinGemmParams p) {
+// D[f][m][n] = Σ_k A[f][m][k] · B[f][n][k]  (3×TF32).  grid = (ceil(N/(128·NB)), ceil(M/128), F·S)
+// Two TMEM accumulators of 256 columns alternate per group of kTcDrain K chunks, so the
+// MMAs of group g+1 run while the epilogue warps drain group g.
+__global__ void __launch_bounds__(kTcThreads, 1) oaa_bin_gemm_kernel(const BinGemmParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // [2 buffers][A_hi, A_lo, B_hi, B_lo] × 16 KB
-  float* sm = reinterpret_cast<float*>(smem_raw);
-  __shared__ uint64_t mbar[2];
+  // stage s: [A_hi 16K][A_lo 16K][B_hi 32K][B_lo 32K]
+  __shared__ uint64_t full[kTcStages], empty[kTcStages], accf[2], acce[2];
   __shared__ uint32_t s_tmem;
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int f = blockIdx.z, m0 = blockIdx.y * kTcM, n0 = blockIdx.x * kTcN;
-  const float* A = p.A + (long long)f * p.strideA + (long long)m0 * p.Kd;
-  const float* Bm = p.B + (long long)f * p.strideB + (long long)n0 * p.Kd;
-  const int mrows = min(kTcM, p.M - m0), nrows = min(kTcN, p.N - n0);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int f = blockIdx.z / p.S, split = blockIdx.z - (blockIdx.z / p.S) * p.S;
+  const int kbeg = split * p.kps, nk = min(p.Kc, kbeg + p.kps) - kbeg;
+  const int mt = blockIdx.y, nt = blockIdx.x;
+  const int NB = p.NB, ntile = kTcM * NB;
+  const int m0 = mt * kTcM, n0 = nt * ntile;
+  const int mrows = min(kTcM, p.M - m0), ncols = min(ntile, p.N - n0);
+  const int nb = min(NB, p.RTB - NB * nt);  // B row tiles present
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&s_tmem)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
+  if (tid == 32) {
+    for (int s = 0; s < kTcStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&accf[b], 1);
+      mbar_init(&acce[b], 8);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = s_tmem;
-  constexpr uint32_t idesc = umma_idesc_tf32(kTcM, kTcN);
-  const int nchunks = (p.Kd + kTcK - 1) / kTcK;
-  uint32_t phase[2] = {0u, 0u};
-  for (int ch = 0; ch < nchunks; ++ch) {
-    const int buf = ch & 1;
-    float* base = sm + buf * 4 * 4096;
-    // the MMAs that read this buffer two chunks ago must be done
-    if (ch >= 2) {
-      mbar_wait(&mbar[buf], phase[buf]);
-      phase[buf] ^= 1u;
-    }
-    const int k0 = ch * kTcK, kvalid = min(kTcK, p.Kd - k0);
-    load_split_tile(A + k0, p.Kd, mrows, kvalid, base, base + 4096, tid);
-    load_split_tile(Bm + k0, p.Kd, nrows, kvalid, base + 2 * 4096, base + 3 * 4096, tid);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t a_hi = smem_u32(base), a_lo = smem_u32(base + 4096);
-      const uint32_t b_hi = smem_u32(base + 2 * 4096), b_lo = smem_u32(base + 3 * 4096);
-#pragma unroll
-      for (int ks = 0; ks < kTcK / 8; ++ks) {  // K = 8 tf32 per MMA = 2 core-matrix columns
-        const uint32_t koff = ks * 256;        // 2 × 128 B
-        const uint64_t dah = umma_desc_kmajor(a_hi + koff, 128, 1024);
-        const uint64_t dal = umma_desc_kmajor(a_lo + koff, 128, 1024);
-        const uint64_t dbh = umma_desc_kmajor(b_hi + koff, 128, 1024);
-        const uint64_t dbl = umma_desc_kmajor(b_lo + koff, 128, 1024);
-        const uint32_t acc = (ch > 0 || ks > 0) ? 1u : 0u;
-        umma_tf32(tmem, dal, dbh, idesc, acc);
-        umma_tf32(tmem, dah, dbl, idesc, 1u);
-        umma_tf32(tmem, dah, dbh, idesc, 1u);
+  const int ngroups = (nk + kTcDrain - 1) / kTcDrain;
+  constexpr uint32_t kBlk = 4096 * sizeof(float);
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      for (int ch = 0; ch < nk; ++ch) {
+        const int s = ch % kTcStages;
+        if (ch >= kTcStages) mbar_wait(&empty[s], ((ch / kTcStages) - 1) & 1);
+        unsigned char* st = smem_raw + s * kTcStageBytes;
+        mbar_expect_tx(&full[s], 2 * kBlk + 2 * nb * kBlk);
+        const float* a = p.A + ((((size_t)f * p.Kc + kbeg + ch) * 2) * p.RTA + mt) * 4096;
+        const float* b = p.B + ((((size_t)f * p.Kc + kbeg + ch) * 2) * p.RTB + NB * nt) * 4096;
+        bulk_g2s(st, a, kBlk, &full[s]);
+        bulk_g2s(st + kBlk, a + (size_t)p.RTA * 4096, kBlk, &full[s]);
+        bulk_g2s(st + 2 * kBlk, b, nb * kBlk, &full[s]);
+        bulk_g2s(st + 4 * kBlk, b + (size_t)p.RTB * 4096, nb * kBlk, &full[s]);
       }
-      umma_commit(&mbar[buf]);
     }
-  }
-  // wait for the last chunk's MMAs (all earlier ones complete in order)
-  {
-    const int last = (nchunks - 1) & 1;
-    // each buffer's barrier has completed floor(uses) phases already consumed above
-    mbar_wait(&mbar[last], phase[last]);
-  }
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  // epilogue: thread tid owns accumulator row m0 + tid (TMEM lane = 32·warp + lane)
-  const int row = tid;
-  float* drow = p.D + (long long)f * p.strideD + (long long)(m0 + row) * p.ldd + n0;
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      const uint32_t idesc = NB == 2 ? umma_idesc_tf32(kTcM, 256) : umma_idesc_tf32(kTcM, 128);
+      for (int ch = 0; ch < nk; ++ch) {
+        const int g = ch / kTcDrain, buf = g & 1;
+        const bool first = (ch % kTcDrain) == 0;
+        if (first && g >= 2) mbar_wait(&acce[buf], ((g >> 1) - 1) & 1);
+        const int s = ch % kTcStages;
+        mbar_wait(&full[s], (ch / kTcStages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t base = smem_u32(smem_raw + s * kTcStageBytes);
+        const uint32_t a_hi = base, a_lo = base + kBlk, b_hi = base + 2 * kBlk, b_lo = base + 4 * kBlk;
+        const uint32_t acc_t = tmem + buf * 256;
 #pragma unroll
-  for (int c0 = 0; c0 < kTcN; c0 += 32) {
-    float v[32];
-    const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + c0;
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]),
-          "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15]),
-          "=f"(v[16]), "=f"(v[17]), "=f"(v[18]), "=f"(v[19]), "=f"(v[20]), "=f"(v[21]), "=f"(v[22]), "=f"(v[23]),
-          "=f"(v[24]), "=f"(v[25]), "=f"(v[26]), "=f"(v[27]), "=f"(v[28]), "=f"(v[29]), "=f"(v[30]), "=f"(v[31])
-        : "r"(ta));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (row < mrows) {
+        for (int ks = 0; ks < kTcK / 8; ++ks) {  // K = 8 tf32 per MMA = 2 core-matrix columns
+          const uint32_t koff = ks * 256;        // 2 × 128 B
+          const uint64_t dah = umma_desc_kmajor(a_hi + koff, 128, 1024);
+          const uint64_t dal = umma_desc_kmajor(a_lo + koff, 128, 1024);
+          const uint64_t dbh = umma_desc_kmajor(b_hi + koff, 128, 1024);
+          const uint64_t dbl = umma_desc_kmajor(b_lo + koff, 128, 1024);
+          umma_tf32(acc_t, dal, dbh, idesc, (first && ks == 0) ? 0u : 1u);
+          umma_tf32(acc_t, dah, dbl, idesc, 1u);
+          umma_tf32(acc_t, dah, dbh, idesc, 1u);
+        }
+        umma_commit(&empty[s]);
+        if ((ch % kTcDrain) == kTcDrain - 1 || ch == nk - 1) umma_commit(&accf[buf]);
+      }
+    }
+  } else {
+    // drain / epilogue: warp w reads TMEM lanes 32·(w%4).., column half (w−2)/4
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    const int row = 32 * q + lane, cb = 128 * half;
+    const bool active = cb < ncols;
+    float acc[128];
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (c0 + j < nrows) drow[c0 + j] = v[j];
+    for (int j = 0; j < 128; ++j) acc[j] = 0.f;
+    for (int g = 0; g < ngroups; ++g) {
+      const int buf = g & 1;
+      mbar_wait(&accf[buf], (g >> 1) & 1);
+      __syncwarp();
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (active) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float v[32];
+          tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + buf * 256 + cb + 32 * c, v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[32 * c + j] += v[j];
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[buf]);
+    }
+    if (active && row < mrows) {
+      if (p.mode == 1) {
+        const int k = m0 + row, f1 = f / p.P, f2 = f - (f / p.P) * p.P;
+        const int bins = p.H * p.P;
+        float* pk = p.partial + ((size_t)(p.g0 + split) * p.M + k) * p.Cf * bins * 2 + (size_t)(f2 * p.H + f1) * 2;
+#pragma unroll
+        for (int j = 0; j < 128; ++j) {
+          const int nn = cb + j;
+          if (nn < ncols) {
+            const int n = n0 + nn;
+            const int im = n >= p.Cf, c = im ? n - p.Cf : n;
+            float* d = pk + (size_t)c * bins * 2 + im;
+            *d = p.accumulate ? *d + acc[j] : acc[j];
+          }
+        }
+      }
+    }
+    if (p.mode == 0 && active) {
+      // transpose through shared memory (the pipeline stages are idle now: every bulk copy
+      // was consumed by an MMA that has completed) so each store instruction writes 128
+      // contiguous bytes of one D row
+      float* tile = reinterpret_cast<float*>(smem_raw) + (warp - 2) * 32 * 129;
+#pragma unroll
+      for (int j = 0; j < 128; ++j) tile[lane * 129 + j] = acc[j];
+      __syncwarp();
+      const int nc = min(128, ncols - cb);
+      for (int r = 0; r < 32; ++r) {
+        const int m = 32 * q + r;
+        if (m >= mrows) break;
+        float* drow = p.D + (long long)f * p.strideD + (long long)(m0 + m) * p.ldd + n0 + cb;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int j = lane + 32 * i;
+          if (j < nc) __stcg(drow + j, tile[r * 129 + j]);
+        }
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 }  // namespace oaa
 
 #ifdef OAA_DEFINE_AUX_KERNELS
 namespace oaa {
-// A operand of the bin GEMM, the real-ified kernel spectra
-//   Ag[f][m][kk] = [[Wr, −Wi], [Wi, Wr]]  (rows m < Co | m ≥ Co, columns kk < Ci | kk ≥ Ci),
-// with W_{o,i}[f] = DFT_P(w_{o,i})[f1][f2] / P² (fwd: o = k, i = c) or of flip180(w_{k,c})
-// with o = c, i = k (bwd_data).  The K padding columns (2Ci ≤ kk < Kdp) are zeroed by the
-// caller.  One thread per (f, o, i), twiddles from a per-block fp64 table.
+// A operand of the bin GEMM, the real-ified kernel spectra, pre-split and blocked:
+//   rows m < Co: (Wr at column i, −Wi at column Cip + i); rows Co + m: (Wi, Wr),
+// Cip = Ci rounded up to 4 (the column layout of oaa_tile_spectra_kernel), with
+// W_{o,i}[f] = DFT_P(w_{o,i})[f1][f2] / P² (fwd: o = k, i = c) or of flip180(w_{k,c})
+// with o = c, i = k (bwd_data).  All other columns are zeroed by the caller.  One thread
+// per (f, o, i), twiddles from a per-block fp64 table.
 __global__ void oaa_realified_spectrum_kernel(const float* __restrict__ w, float* __restrict__ Ag, int K, int C,
-                                              int n, int flip_bwd, int Kdp) {
+                                              int n, int flip_bwd, int Kc, int RTA) {
   const int P = 2 * n - 1, H = n, F = H * P;
-  const int Co = flip_bwd ? C : K, Ci = flip_bwd ? K : C;
+  const int Co = flip_bwd ? C : K, Ci = flip_bwd ? K : C, Cip = (Ci + 3) & ~3;
   __shared__ double tc[16], ts[16];
   if (threadIdx.x < P) sincospi(2.0 * (double)threadIdx.x / (double)P, &ts[threadIdx.x], &tc[threadIdx.x]);
   __syncthreads();
@@ -251,12 +320,25 @@ __global__ void oaa_realified_spectrum_kernel(const float* __restrict__ w, float
         si -= (double)v * ts[mm];
       }
     const float re = (float)(sr * inv), im = (float)(si * inv);
-    float* row_r = Ag + ((long long)f * 2 * Co + o) * Kdp;
-    float* row_i = row_r + (long long)Co * Kdp;
-    row_r[i] = re;
-    row_r[Ci + i] = -im;
-    row_i[i] = im;
-    row_i[Ci + i] = re;
+    tc_put(Ag, f, Kc, RTA, o, i, re);
+    tc_put(Ag, f, Kc, RTA, o, Cip + i, -im);
+    tc_put(Ag, f, Kc, RTA, Co + o, i, im);
+    tc_put(Ag, f, Kc, RTA, Co + o, Cip + i, re);
+  }
+}
+
+// Row-major X[F][rows][Kd] → pre-split blocked layout (debug entry point only).  Padding
+// rows and columns are written as zeros.
+__global__ void oaa_tc_pack_kernel(const float* __restrict__ X, float* __restrict__ Op, int F, int rows, int Kd,
+                                   int Kc, int RT) {
+  const long long total = (long long)F * RT * 128 * Kc * 32;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(t % (Kc * 32));
+    const int r = (int)((t / (Kc * 32)) % (RT * 128));
+    const int f = (int)(t / ((long long)Kc * 32 * RT * 128));
+    const float v = (r < rows && k < Kd) ? X[((size_t)f * rows + r) * Kd + k] : 0.f;
+    tc_put(Op, f, Kc, RT, r, k, v);
   }
 }
 }  // namespace oaa

@@ -298,7 +298,8 @@ def test_host_pipeline_matches_device_calls():
     assert torch.equal(hdw, oaa.conv_bwd_filter(x, dy, n, crop).cpu())
 
 
-@pytest.mark.parametrize("F,M,N,Kd", [(1, 128, 128, 32), (3, 256, 384, 192), (2, 200, 130, 68), (5, 512, 256, 128)])
+@pytest.mark.parametrize("F,M,N,Kd", [(1, 128, 128, 32), (3, 256, 384, 192), (2, 200, 130, 68), (5, 512, 256, 128),
+                                      (3, 300, 700, 50), (1, 16, 1000, 7), (2, 130, 257, 96)])
 def test_tcgen05_bin_gemm_3xtf32(F, M, N, Kd):
     """The tensor-core contraction kernel alone vs a float64 matmul: fp32-level accuracy
     (3×TF32), ragged M/N/K tails."""
