@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -185,6 +186,21 @@ cudaError_t launch_engine(int n, const oaa::EngineParams& p, const EnginePlan& e
   return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_walk(int n, const oaa::XSpecParams& xp, const oaa::WalkParams& wp, const WalkPlan& w, int cr,
+                        cudaStream_t s) {
+  switch (n) {
+    case 1: return launch_walk_n<1>(xp, wp, w, cr, s);
+    case 2: return launch_walk_n<2>(xp, wp, w, cr, s);
+    case 3: return launch_walk_n<3>(xp, wp, w, cr, s);
+    case 4: return launch_walk_n<4>(xp, wp, w, cr, s);
+    case 5: return launch_walk_n<5>(xp, wp, w, cr, s);
+    case 6: return launch_walk_n<6>(xp, wp, w, cr, s);
+    case 7: return launch_walk_n<7>(xp, wp, w, cr, s);
+    case 8: return launch_walk_n<8>(xp, wp, w, cr, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_filter(int n, const oaa::FilterParams& p, const FilterPlan& f, cudaStream_t s) {
   switch (n) {
     case 1: return launch_filter_n<1>(p, f, s);
@@ -248,13 +264,42 @@ TcPlan plan_tc(int B, int Cin, int Cout, int R, int n) {
   return t;
 }
 
+// walker forward (oaa_walk.cuh): small input-channel counts, forward only -------------
+constexpr int kWalkMaxCin = 4;
+struct WalkHostGeo {
+  bool use;
+  int TPW, CW, RS4, CH4, NCH, KG, ngrp;
+  size_t spec_b, xs_b;
+};
+WalkHostGeo plan_walk(bool is_fwd, int B, int Cin, int Cout, int T, int Ro, int off, int n, const TcPlan& tc) {
+  WalkHostGeo w{};
+  w.use = is_fwd && !tc.use && Cin <= kWalkMaxCin && std::getenv("OAA_NO_WALK") == nullptr;
+  const int H = n;
+  w.TPW = 32 / H;
+  w.CW = w.TPW * n;
+  w.RS4 = n | 1;
+  w.CH4 = w.TPW * H * w.RS4;
+  w.NCH = cdiv(off + Ro, w.CW);
+  w.KG = std::min(8, Cout);
+  w.ngrp = cdiv(Cout, w.KG);
+  w.spec_b = align_up(sizeof(float4) * (size_t)Cin * Cout * n * H);
+  w.xs_b = align_up(sizeof(float4) * (size_t)B * T * w.NCH * Cin * w.CH4);
+  return w;
+}
+
 // workspace layouts ------------------------------------------------------------
 struct EngineWs {
   size_t spec_off, flags_off, counter_off, xg_off, d_off, total;
 };
-EngineWs engine_ws(int B, int C, int K, int Tr, const Geo& g, const TcPlan& tc) {
+EngineWs engine_ws(int B, int C, int K, int Tr, const Geo& g, const TcPlan& tc, const WalkHostGeo* wk = nullptr) {
   EngineWs w{};
   w.spec_off = 0;
+  if (wk && wk->use) {
+    w.xg_off = wk->spec_b;  // X̂ chunks
+    w.flags_off = w.counter_off = w.d_off = 0;
+    w.total = wk->spec_b + wk->xs_b;
+    return w;
+  }
   if (tc.use) {
     w.flags_off = align_up(tc.ag_b);
     w.counter_off = align_up(w.flags_off + sizeof(int) * (size_t)std::max(1, tc.bc * Tr));
@@ -451,7 +496,8 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
   EnginePlan e;
   if (!plan_engine(R, Ro, off, n, Cin, Cout, &e, tc.use)) return OAA_ERR_UNSUPPORTED;
   if (B == 0) return OAA_OK;
-  EngineWs L = engine_ws(B, C, K, e.T, g, tc);
+  const WalkHostGeo wk = plan_walk(is_fwd, B, Cin, Cout, e.T, Ro, off, n, tc);
+  EngineWs L = engine_ws(B, C, K, e.T, g, tc, &wk);
   if (!ws || ws_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0)
     return OAA_ERR_WORKSPACE;
   if (overlaps(ws, L.total, out, out_bytes) || overlaps(ws, L.total, in, in_bytes))
@@ -463,6 +509,52 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
   int* counter = reinterpret_cast<int*>(base + L.counter_off);
 
   if (tc.use) return run_engine_tc(is_fwd, in, w, out, B, C, K, n, g, e, tc, L, base, s);
+  if (wk.use) {
+    {
+      const long total = (long)K * C * ((g.P + 1) / 2) * g.H;
+      const int thr = 256;
+      const int blocks = (int)std::min<long>((total + thr - 1) / thr, 4096);
+      oaa::oaa_spectrum_kernel<<<blocks, thr, 0, s>>>(w, spec, K, C, n, 0, 1);
+      g_launches++;
+      if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
+    }
+    oaa::XSpecParams xp;
+    xp.in = in;
+    xp.S = reinterpret_cast<float4*>(base + L.xg_off);
+    xp.Cin = Cin;
+    xp.R = R;
+    xp.T = e.T;
+    xp.NCH = wk.NCH;
+    xp.SW = wk.NCH * wk.CW;
+    oaa::WalkParams wp;
+    wp.S = xp.S;
+    wp.spec = spec;
+    wp.out = out;
+    wp.B = B;
+    wp.Cin = Cin;
+    wp.Cout = Cout;
+    wp.T = e.T;
+    wp.Ro = Ro;
+    wp.off = off;
+    wp.NCH = wk.NCH;
+    wp.KG = wk.KG;
+    wp.ngrp = wk.ngrp;
+    WalkPlan wpl;
+    wpl.KG = wk.KG;
+    wpl.ngrp = wk.ngrp;
+    wpl.NCH = wk.NCH;
+    wpl.SW = xp.SW;
+    wpl.xspec_smem = sizeof(float) * (size_t)Cin * n * xp.SW;
+    const int QSZ = (2 * wk.TPW + 1) * n * g.P;
+    wpl.walk_smem = sizeof(float4) * (size_t)oaa::kWalkRing * Cin * wk.CH4 + sizeof(float2) * (size_t)wk.KG * QSZ +
+                    sizeof(float) * (size_t)wk.KG * (n - 1) * wk.NCH * wk.CW;
+    if (wpl.walk_smem > 220 * 1024 || wpl.xspec_smem > 220 * 1024) return OAA_ERR_UNSUPPORTED;
+    ProfScope prof(OAA_OP_FWD, s);
+    prof.start();
+    cudaError_t err = launch_walk(n, xp, wp, wpl, Cin, s);
+    prof.stop();
+    return err == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
+  }
   // kernel spectra: loop-major layout [Cloop][Cinner][P][H]
   const int loop_is_k = (is_fwd == e.S1) ? 1 : 0;  // fwd S1 / bwd_data S2 loop over k
   {
@@ -571,7 +663,10 @@ size_t oaa_conv_workspace_bytes(oaa_op_t op, int B, int C, int K, int N, int n, 
   if (op == OAA_OP_FWD || op == OAA_OP_BWD_DATA) {
     const bool fwd = op == OAA_OP_FWD;
     const int R = fwd ? N : g.M;
-    return engine_ws(B, C, K, cdiv(R, n), g, plan_tc(B, fwd ? C : K, fwd ? K : C, R, n)).total;
+    const TcPlan tc = plan_tc(B, fwd ? C : K, fwd ? K : C, R, n);
+    const int Ro = fwd ? g.M : N, off = fwd ? g.o : (n - 1 - g.o);
+    const WalkHostGeo wk = plan_walk(fwd, B, fwd ? C : K, fwd ? K : C, cdiv(R, n), Ro, off, n, tc);
+    return engine_ws(B, C, K, cdiv(R, n), g, tc, &wk).total;
   }
   if (op == OAA_OP_BWD_FILTER) {
     const TcFiltPlan t = plan_tc_filter(B, C, K, N, g.M, n);

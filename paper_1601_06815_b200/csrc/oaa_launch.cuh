@@ -10,6 +10,7 @@
 #include <cstdlib>
 
 #include "oaa_kernels.cuh"
+#include "oaa_walk.cuh"
 
 namespace oaa_host {
 
@@ -129,19 +130,47 @@ cudaError_t launch_filter_spectra_n(const oaa::FiltSpecParams& p, bool xwin, int
   return cudaGetLastError();
 }
 
+// Walker forward (small Cin): block spectra X̂ of the input, then the walker.
+struct WalkPlan {
+  int KG, ngrp, NCH, SW;
+  size_t xspec_smem, walk_smem;
+};
+
+template <int NN>
+cudaError_t launch_walk_n(const oaa::XSpecParams& xp, const oaa::WalkParams& wp, const WalkPlan& w, int cr,
+                          cudaStream_t s) {
+  {
+    auto k = oaa::oaa_xspec_kernel<NN>;
+    cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w.xspec_smem);
+    if (err != cudaSuccess) return err;
+    k<<<wp.B * wp.T, 256, w.xspec_smem, s>>>(xp);
+    g_launches++;
+    if ((err = cudaGetLastError()) != cudaSuccess) return err;
+  }
+  auto k = cr <= 1 ? oaa::oaa_walk_kernel<NN, 1> : cr == 2 ? oaa::oaa_walk_kernel<NN, 2>
+         : cr == 3 ? oaa::oaa_walk_kernel<NN, 3> : oaa::oaa_walk_kernel<NN, 4>;
+  cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w.walk_smem);
+  if (err != cudaSuccess) return err;
+  k<<<wp.B * w.ngrp, 32 * w.KG, w.walk_smem, s>>>(wp);
+  g_launches++;
+  return cudaGetLastError();
+}
+
 #define OAA_DECLARE_N(NN)                                                                      \
   extern template cudaError_t launch_engine_n<NN>(const oaa::EngineParams&, const EnginePlan&, \
                                                   cudaStream_t);                              \
   extern template cudaError_t launch_filter_n<NN>(const oaa::FilterParams&, const FilterPlan&, \
                                                   cudaStream_t);                              \
   extern template cudaError_t launch_tile_spectra_n<NN>(const oaa::TileSpecParams&, size_t, cudaStream_t); \
-  extern template cudaError_t launch_filter_spectra_n<NN>(const oaa::FiltSpecParams&, bool, int, size_t, cudaStream_t);
+  extern template cudaError_t launch_filter_spectra_n<NN>(const oaa::FiltSpecParams&, bool, int, size_t, cudaStream_t); \
+  extern template cudaError_t launch_walk_n<NN>(const oaa::XSpecParams&, const oaa::WalkParams&, const WalkPlan&, int, cudaStream_t);
 #define OAA_INSTANTIATE_N(NN)                                                                 \
   template cudaError_t launch_engine_n<NN>(const oaa::EngineParams&, const EnginePlan&,       \
                                            cudaStream_t);                                     \
   template cudaError_t launch_filter_n<NN>(const oaa::FilterParams&, const FilterPlan&,       \
                                            cudaStream_t);                                     \
   template cudaError_t launch_tile_spectra_n<NN>(const oaa::TileSpecParams&, size_t, cudaStream_t); \
-  template cudaError_t launch_filter_spectra_n<NN>(const oaa::FiltSpecParams&, bool, int, size_t, cudaStream_t);
+  template cudaError_t launch_filter_spectra_n<NN>(const oaa::FiltSpecParams&, bool, int, size_t, cudaStream_t); \
+  template cudaError_t launch_walk_n<NN>(const oaa::XSpecParams&, const oaa::WalkParams&, const WalkPlan&, int, cudaStream_t);
 
 }  // namespace oaa_host

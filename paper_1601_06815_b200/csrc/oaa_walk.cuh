@@ -1,0 +1,297 @@
+// oaa_walk.cuh -- the "walker" engine: contraction + inverse DFT + overlap-add of one
+// output channel per warp, walking the tile rows of an image top to bottom.
+//
+// PAPER.md:18 (§2, Fig. 1): the blocks' inverse transforms "are then added with an
+// overlap of n−1" to rebuild the linear convolution.  In the fused engines of
+// oaa_kernels.cuh one CTA owns one tile row, so the vertical overlap (n−1 rows shared
+// with the next tile row) crosses CTAs and needs progress flags, fences and a
+// read-modify-write through L2.  Here one warp owns one (image, output channel) plane and
+// produces its tile rows in order, so the vertical overlap never leaves the SM: the n−1
+// bottom rows of tile row t1 wait in a per-warp carry buffer and are added to the top
+// rows of tile row t1+1.  Every output element is written exactly once, with a plain
+// streaming store, and no warp ever waits for another.
+//
+// A tile row is processed in chunks of TPW = ⌊32/H⌋ tiles (one warp: lanes (tt, f1)):
+//   stage A  lane (tt, f1): Ŷ row f1 of tile tt = Σ_c Ŵ_c[f1,:]·X̂_c[f1,:]  (PAPER.md:15,
+//            the K·C frequency-domain products summed over c; Ŵ lives in registers),
+//            inverse DFT along f2 → Q[f1][p2] in the warp's shared Q ring;
+//   stage B  lane = output column J of the chunk: the two block columns that land on J
+//            (tile J/n at p2 = J mod n, tile J/n − 1 at p2 + n) are summed BEFORE the last
+//            transform (linearity -- the horizontal overlap-add), Hermitian
+//            c2r along f1 gives the column's 2n−1 rows; rows [0, n−1) add the carry, rows
+//            [0, n) are final and stored, rows [n, 2n−1) become the carry.
+// The forward spectra X̂ of the input blocks (one per (image, channel, block), computed
+// once by oaa_xspec_kernel) stream through a ring of shared-memory chunk slots filled by
+// bulk copies (TMA engine); the last warp to release a slot issues the copy that refills
+// it, so there is no producer warp and no CTA barrier in the steady state.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dft.cuh"
+#include "oaa_kernels.cuh"
+
+namespace oaa {
+
+template <int NN>
+struct WalkGeo {
+  static constexpr int P = 2 * NN - 1, H = NN, P2 = NN;  // f2 pairs (the last one half zero)
+  static constexpr int TPW = 32 / H;                     // tiles per chunk
+  static constexpr int CW = TPW * NN;                    // output columns per chunk
+  static constexpr int RS4 = P2 | 1;                     // float4 per spectrum row (odd: LDS.128 conflict free)
+  static constexpr int CH4 = TPW * H * RS4;              // float4 per channel in a chunk
+  static constexpr int QT = H * P;                       // float2 per tile in Q
+  static constexpr int QS = 2 * TPW;                     // Q ring slots (tiles)
+  static constexpr int QSZ = (QS + 1) * QT;              // + one always-zero tile
+};
+
+// Chunked spectrum layout (X̂ for fwd): S[b][t1][i][c][lane][RS4] float4, lane = tt·H + f1,
+// float4 q = (Re f, Im f, Re f+1, Im f+1) for f = 2q (f2 = P is zero).  Tiles past the
+// last real tile (padding to NCH·TPW) are zero.
+struct XSpecParams {
+  const float* in;  // [B][Cin][R][R]
+  float4* S;        // chunked spectra
+  int Cin, R, T, NCH, SW;  // SW = staged row width (NCH·CW)
+};
+
+// One CTA per (image, tile row): the n input rows of every channel are staged (zero
+// padded), then each task (chunk i, channel c, lane) computes its block-row spectrum.
+template <int NN>
+__global__ void __launch_bounds__(256) oaa_xspec_kernel(const XSpecParams p) {
+  using G = WalkGeo<NN>;
+  constexpr int P = G::P, H = G::H, RS4 = G::RS4;
+  extern __shared__ __align__(16) float rows_s[];  // [Cin][NN][SW]
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int item = blockIdx.x;
+  const int b = item / p.T, t1 = item - (item / p.T) * p.T;
+  const float* in_b = p.in + (size_t)b * p.Cin * p.R * p.R;
+  {
+    const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
+    for (int sg = warp; sg < p.Cin * NN; sg += nw) {
+      const int c = sg / NN, rr = sg - (sg / NN) * NN;
+      const int r = t1 * NN + rr;
+      const bool rok = r < p.R;
+      const float* src = in_b + ((size_t)c * p.R + (rok ? r : 0)) * p.R;
+      float* d = rows_s + (c * NN + rr) * p.SW;
+      for (int q = lane; q < p.SW; q += 32) {
+        const bool ok = rok && q < p.R;
+        cp_async4(d + q, ok ? src + q : in_b, ok);
+      }
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+  }
+  float4* out = p.S + (size_t)item * p.NCH * p.Cin * G::CH4;
+  const int ntask = p.NCH * p.Cin * 32;
+  for (int task = tid; task < ntask; task += nthr) {
+    const int lane = task & 31, ic = task >> 5;
+    const int tt = lane / H, f1 = lane - (lane / H) * H;
+    if (tt >= G::TPW) continue;
+    const int i = ic / p.Cin, c = ic - (ic / p.Cin) * p.Cin;
+    float cf[NN], sf[NN];
+#pragma unroll
+    for (int p1 = 0; p1 < NN; ++p1) {
+      float s, co;
+      sincospif(2.0f * (float)((f1 * p1) % P) / (float)P, &s, &co);
+      cf[p1] = co;
+      sf[p1] = s;
+    }
+    float xr[P], xi[P];
+    block_row_spectrum_smem<NN>(rows_s + c * NN * p.SW, p.SW, (i * G::TPW + tt) * NN, cf, sf, xr, xi);
+    float4* d = out + (size_t)ic * G::CH4 + lane * RS4;
+#pragma unroll
+    for (int q = 0; q < RS4; ++q) {
+      const int f = 2 * q;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (f < P) { v.x = xr[f]; v.y = xi[f]; }
+      if (f + 1 < P) { v.z = xr[f + 1]; v.w = xi[f + 1]; }
+      d[q] = v;
+    }
+  }
+}
+
+struct WalkParams {
+  const float4* S;     // chunked spectra (X̂: Cin channels per chunk)
+  const float4* spec;  // kernel spectra [Cout][Cin][P2][H] float4 (already scaled by 1/P²)
+  float* out;          // [B][Cout][Ro][Ro]
+  int B, Cin, Cout, T, Ro, off, NCH;
+  int KG;              // output channels (warps) per CTA
+  int ngrp;            // channel groups per image = ceil(Cout / KG)
+};
+
+constexpr int kWalkRing = 4;  // spectrum chunk slots per CTA
+
+// grid = B·ngrp CTAs (image-major: the groups of one image run side by side and share
+// its spectra through L2), KG warps each.
+// Shared memory: ring[kWalkRing][Cin·CH4] float4 | Q[KG][QSZ] float2 | carry[KG][n−1][NCH·CW].
+template <int NN, int CR>
+__global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
+  using G = WalkGeo<NN>;
+  constexpr int P = G::P, H = G::H, P2 = G::P2, TPW = G::TPW, CW = G::CW, RS4 = G::RS4, QT = G::QT;
+  constexpr int TR = NN - 1;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint64_t full[kWalkRing];
+  __shared__ int rel[kWalkRing];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int b = blockIdx.x / p.ngrp, grp = blockIdx.x - (blockIdx.x / p.ngrp) * p.ngrp;
+  const int co = grp * p.KG + warp;
+  const int slot4 = p.Cin * G::CH4;  // float4 per ring slot
+  float4* ring = reinterpret_cast<float4*>(smem_raw);
+  float2* Qall = reinterpret_cast<float2*>(ring + kWalkRing * slot4);
+  float2* Q = Qall + warp * G::QSZ;
+  const int CWT = p.NCH * CW;  // carry row length
+  float* carry = reinterpret_cast<float*>(Qall + nw * G::QSZ) + warp * TR * CWT;
+  const int nseq = p.T * p.NCH;
+  const float4* src = p.S + (size_t)b * nseq * slot4;
+  const uint32_t slot_bytes = (uint32_t)slot4 * 16u;
+
+  if (tid == 0) {
+    for (int s = 0; s < kWalkRing; ++s) {
+      mbar_init(&full[s], 1);
+      rel[s] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // zero tile of Q and the carry rows
+  for (int e = lane; e < QT; e += 32) Q[G::QS * QT + e] = make_float2(0.f, 0.f);
+  for (int e = lane; e < TR * CWT; e += 32) carry[e] = 0.f;
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < kWalkRing && s < nseq; ++s) {
+      mbar_expect_tx(&full[s], slot_bytes);
+      bulk_g2s(ring + s * slot4, src + (size_t)s * slot4, slot_bytes, &full[s]);
+    }
+  }
+  const bool active = co < p.Cout;  // (warp-uniform) a warp past Cout still releases slots
+
+  // this lane's kernel spectra: Ŵ[co][c][f1 = lane mod H][f2], f2 pairs
+  const int tt = lane / H, f1 = lane - (lane / H) * H;
+  const bool laneA = tt < TPW;
+  float4 Wr[CR][P2];
+#pragma unroll
+  for (int c = 0; c < CR; ++c)
+#pragma unroll
+    for (int q = 0; q < P2; ++q)
+      Wr[c][q] = (active && laneA && c < p.Cin) ? __ldg(p.spec + (((size_t)co * p.Cin + c) * P2 + q) * H + f1)
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+  // stage-B geometry: lane = column J = i·CW + lane, tile J/n = i·TPW + lq at p2 = pA
+  const int lq = lane / NN, pA = lane - (lane / NN) * NN;
+  const bool laneB = lane < CW;
+  const bool hasB = pA <= NN - 2;
+  const size_t plane = (size_t)p.Ro * p.Ro;
+  float* outp = p.out + ((size_t)b * p.Cout + (active ? co : 0)) * plane;
+
+  int seq = 0;
+  for (int t1 = 0; t1 < p.T; ++t1) {
+    const int r0 = t1 * NN - p.off;  // output row of block row 0
+    for (int i = 0; i < p.NCH; ++i, ++seq) {
+      const int s = seq % kWalkRing;
+      mbar_wait(&full[s], (seq / kWalkRing) & 1);
+      const int half = i & 1;
+      // ---- stage A: contraction + inverse DFT along f2
+      if (active && laneA) {
+        const float4* xs = ring + s * slot4 + lane * RS4;
+        float yr[P], yi[P];
+#pragma unroll
+        for (int c = 0; c < CR; ++c) {
+          if (c < p.Cin) {
+#pragma unroll
+            for (int q = 0; q < P2; ++q) {
+              const float4 x = xs[c * G::CH4 + q];
+              const float4 w = Wr[c][q];
+              const int f = 2 * q;
+              if (c == 0) {
+                yr[f] = w.x * x.x;
+                yi[f] = w.x * x.y;
+              } else {
+                yr[f] = fmaf(w.x, x.x, yr[f]);
+                yi[f] = fmaf(w.x, x.y, yi[f]);
+              }
+              yr[f] = fmaf(-w.y, x.y, yr[f]);
+              yi[f] = fmaf(w.y, x.x, yi[f]);
+              if (f + 1 < P) {
+                if (c == 0) {
+                  yr[f + 1] = w.z * x.z;
+                  yi[f + 1] = w.z * x.w;
+                } else {
+                  yr[f + 1] = fmaf(w.z, x.z, yr[f + 1]);
+                  yi[f + 1] = fmaf(w.z, x.w, yi[f + 1]);
+                }
+                yr[f + 1] = fmaf(-w.w, x.w, yr[f + 1]);
+                yi[f + 1] = fmaf(w.w, x.z, yi[f + 1]);
+              }
+            }
+          }
+        }
+        float qr[P], qi[P];
+        dft<P, +1>(yr, yi, qr, qi);
+        float2* qd = Q + (half * TPW + tt) * QT + f1 * P;
+#pragma unroll
+        for (int p2 = 0; p2 < P; ++p2) qd[p2] = make_float2(qr[p2], qi[p2]);
+      }
+      // release the ring slot; the last warp out refills it with chunk seq + kWalkRing
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        const int old = atomicAdd(&rel[s], 1);
+        if (old == nw - 1) {
+          rel[s] = 0;
+          __threadfence_block();
+          const int nx = seq + kWalkRing;
+          if (nx < nseq) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&full[s], slot_bytes);
+            bulk_g2s(ring + s * slot4, src + (size_t)nx * slot4, slot_bytes, &full[s]);
+          }
+        }
+      }
+      // ---- stage B: horizontal overlap-add, c2r along f1, vertical carry, stores
+      if (active && laneB) {
+        const int tA = i * TPW + lq;
+        const int offA = (half * TPW + lq) * QT + pA;
+        int offB = G::QS * QT;  // zero tile
+        if (hasB && tA >= 1) offB = (lq > 0 ? (half * TPW + lq - 1) : ((half ^ 1) * TPW + TPW - 1)) * QT + pA + NN;
+        float zr[H], zi[H];
+#pragma unroll
+        for (int k = 0; k < H; ++k) {
+          const float2 a = Q[offA + k * P], bb = Q[offB + k * P];
+          zr[k] = a.x + bb.x;
+          zi[k] = a.y + bb.y;
+        }
+        float y[P];
+        c2r_half<P>(zr, zi, y);
+        const int J = i * CW + lane;
+        const int j = J - p.off;
+        float* cr = carry + J;
+        const bool colok = j >= 0 && j < p.Ro;
+        float* op = outp + (ptrdiff_t)r0 * p.Ro + j;
+#pragma unroll
+        for (int p1 = 0; p1 < NN; ++p1) {
+          float v = y[p1];
+          if (p1 < TR) v += cr[p1 * CWT];
+          const int r = r0 + p1;
+          if (colok && r >= 0 && r < p.Ro) __stcs(op + (ptrdiff_t)p1 * p.Ro, v);
+        }
+#pragma unroll
+        for (int p1 = NN; p1 < P; ++p1) cr[(p1 - NN) * CWT] = y[p1];
+      }
+      __syncwarp();
+    }
+  }
+  // flush: the carry holds the last tile row's bottom rows (final)
+  if (active && laneB) {
+    const int r0 = p.T * NN - p.off;
+    for (int i = 0; i < p.NCH; ++i) {
+      const int J = i * CW + lane, j = J - p.off;
+      if (j < 0 || j >= p.Ro) continue;
+#pragma unroll
+      for (int p1 = 0; p1 < TR; ++p1) {
+        const int r = r0 + p1;
+        if (r >= 0 && r < p.Ro) __stcs(outp + (ptrdiff_t)r * p.Ro + j, carry[p1 * CWT + J]);
+      }
+    }
+  }
+}
+
+}  // namespace oaa
