@@ -13,7 +13,8 @@
 //   * dft_pair   : any odd P, pairing x_j with x_{P−j} (cos/sin split); 36 flops at P=5.
 //   * dft15_pfa  : P = 15 by Good–Thomas 3×5 prime-factor mapping, no twiddles.
 //   * dft9_ct    : P = 9 by Cooley–Tukey 3×3 with 4 twiddles.
-//   * c2r_half   : Hermitian half-spectrum Z[0..H) → real y[0..P) (pairs p, P−p).
+//   * c2r_half   : Hermitian half-spectrum Z[0..H) → real y[0..P) (pairs p, P−p);
+//                  P = 15 by a Hermitian-pruned PFA 3×5 (c2r15_pfa).
 #pragma once
 #include <cstdint>
 
@@ -234,11 +235,44 @@ OAA_HD void dft(const float* xr, const float* xi, float* yr, float* yi) {
 
 // ------------------------------------------------- Hermitian half → real (inverse)
 // y[p] = Z0r + Σ_{f=1}^{H−1} 2·Re(Z[f]·exp(+2πi·f·p/P)),  H = (P+1)/2 (odd P).
+// P = 15 Hermitian → real by the 3 × 5 prime-factor map of dft15_pfa with the roles of
+// the index maps swapped (input k = 5k1 + 3k2, output n = 10n1 + 6n2, both mod 15):
+//   A[n1][k2] = Σ_k1 Z[5k1 + 3k2]·W3^{n1 k1}      (Hermitian in k2: only k2 = 0, 1, 2;
+//                                                  column k2 = 0 is real)
+//   y[10n1 + 6n2] = Σ_k2 A[n1][k2]·W5^{n2 k2}     (three real-output 5-point c2r)
+// Z[k] for k ≥ 8 is conj(Z[15 − k]).  ~74 flops instead of ~120 for the direct form.
+template <int P>
+OAA_HD void c2r_half(const float* zr, const float* zi, float* y);
+
+OAA_HD void c2r15_pfa(const float* zr, const float* zi, float* y) {
+  constexpr float r3 = 1.7320508075688772f;
+  // k2 = 0: (Z0, Z5, conj Z5) → real
+  const float t0 = zr[0] - zr[5];
+  float a0[3] = {fmaf(2.f, zr[5], zr[0]), fmaf(-r3, zi[5], t0), fmaf(r3, zi[5], t0)};
+  // k2 = 1: (Z3, conj Z7, conj Z2);  k2 = 2: (Z6, conj Z4, Z1)
+  float xr1[3] = {zr[3], zr[7], zr[2]}, xi1[3] = {zi[3], -zi[7], -zi[2]};
+  float xr2[3] = {zr[6], zr[4], zr[1]}, xi2[3] = {zi[6], -zi[4], zi[1]};
+  float a1r[3], a1i[3], a2r[3], a2i[3];
+  dft_pair<3, +1, 7u>(xr1, xi1, a1r, a1i);
+  dft_pair<3, +1, 7u>(xr2, xi2, a2r, a2i);
+#pragma unroll
+  for (int n1 = 0; n1 < 3; ++n1) {
+    const float cr[3] = {a0[n1], a1r[n1], a2r[n1]};
+    const float ci[3] = {0.f, a1i[n1], a2i[n1]};
+    float o[5];
+    c2r_half<5>(cr, ci, o);
+#pragma unroll
+    for (int n2 = 0; n2 < 5; ++n2) y[(10 * n1 + 6 * n2) % 15] = o[n2];
+  }
+}
+
 template <int P>
 OAA_HD void c2r_half(const float* zr, const float* zi, float* y) {
   constexpr Tw<P> tw{};
   constexpr int H = (P + 1) / 2;
-  if constexpr (P == 1) {
+  if constexpr (P == 15) {
+    c2r15_pfa(zr, zi, y);
+  } else if constexpr (P == 1) {
     y[0] = zr[0];
   } else {
     float s = 0.f;

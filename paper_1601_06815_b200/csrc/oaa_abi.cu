@@ -201,6 +201,20 @@ cudaError_t launch_walk(int n, const oaa::XSpecParams& xp, const oaa::WalkParams
   return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_bwdd(int n, const oaa::BwdDParams& p, int cr, size_t smem, cudaStream_t s) {
+  switch (n) {
+    case 1: return launch_bwdd_n<1>(p, cr, smem, s);
+    case 2: return launch_bwdd_n<2>(p, cr, smem, s);
+    case 3: return launch_bwdd_n<3>(p, cr, smem, s);
+    case 4: return launch_bwdd_n<4>(p, cr, smem, s);
+    case 5: return launch_bwdd_n<5>(p, cr, smem, s);
+    case 6: return launch_bwdd_n<6>(p, cr, smem, s);
+    case 7: return launch_bwdd_n<7>(p, cr, smem, s);
+    case 8: return launch_bwdd_n<8>(p, cr, smem, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_filter(int n, const oaa::FilterParams& p, const FilterPlan& f, cudaStream_t s) {
   switch (n) {
     case 1: return launch_filter_n<1>(p, f, s);
@@ -287,13 +301,38 @@ WalkHostGeo plan_walk(bool is_fwd, int B, int Cin, int Cout, int T, int Ro, int 
   return w;
 }
 
+// bwd_data for few output channels (oaa_bwdd.cuh) ------------------------------------
+struct BwddPlan {
+  bool use;
+  int NCW, BW;
+  size_t spec_b, smem;
+};
+BwddPlan plan_bwdd(bool is_fwd, int Cout, int R, int n, const TcPlan& tc) {
+  BwddPlan d{};
+  d.use = !is_fwd && !tc.use && Cout <= kWalkMaxCin && std::getenv("OAA_NO_BWDD") == nullptr;
+  const int H = n, P = 2 * n - 1, TPW = 32 / H, CW = TPW * n;
+  const int Td = cdiv(R, n);
+  d.NCW = cdiv(Td, TPW);
+  if (d.NCW > 8) d.use = false;
+  d.BW = d.NCW * CW;
+  d.smem = oaa::bwdd_smem_bytes(n, Cout, d.NCW);
+  if (d.smem > 220 * 1024) d.use = false;
+  return d;
+}
+
 // workspace layouts ------------------------------------------------------------
 struct EngineWs {
   size_t spec_off, flags_off, counter_off, xg_off, d_off, total;
 };
-EngineWs engine_ws(int B, int C, int K, int Tr, const Geo& g, const TcPlan& tc, const WalkHostGeo* wk = nullptr) {
+EngineWs engine_ws(int B, int C, int K, int Tr, const Geo& g, const TcPlan& tc, const WalkHostGeo* wk = nullptr,
+                   const BwddPlan* bd = nullptr) {
   EngineWs w{};
   w.spec_off = 0;
+  if (bd && bd->use) {
+    w.flags_off = w.counter_off = w.d_off = w.xg_off = 0;
+    w.total = align_up(sizeof(float4) * (size_t)K * C * g.n * g.H);
+    return w;
+  }
   if (wk && wk->use) {
     w.xg_off = wk->spec_b;  // X̂ chunks
     w.flags_off = w.counter_off = w.d_off = 0;
@@ -497,7 +536,8 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
   if (!plan_engine(R, Ro, off, n, Cin, Cout, &e, tc.use)) return OAA_ERR_UNSUPPORTED;
   if (B == 0) return OAA_OK;
   const WalkHostGeo wk = plan_walk(is_fwd, B, Cin, Cout, e.T, Ro, off, n, tc);
-  EngineWs L = engine_ws(B, C, K, e.T, g, tc, &wk);
+  const BwddPlan bd = plan_bwdd(is_fwd, Cout, R, n, tc);
+  EngineWs L = engine_ws(B, C, K, e.T, g, tc, &wk, &bd);
   if (!ws || ws_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0)
     return OAA_ERR_WORKSPACE;
   if (overlaps(ws, L.total, out, out_bytes) || overlaps(ws, L.total, in, in_bytes))
@@ -509,6 +549,34 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
   int* counter = reinterpret_cast<int*>(base + L.counter_off);
 
   if (tc.use) return run_engine_tc(is_fwd, in, w, out, B, C, K, n, g, e, tc, L, base, s);
+  if (bd.use) {
+    ProfScope prof(OAA_OP_BWD_DATA, s);
+    prof.start();
+    if (cudaMemsetAsync(out, 0, out_bytes, s) != cudaSuccess) return OAA_ERR_CUDA;
+    {
+      const long total = (long)K * C * ((g.P + 1) / 2) * g.H;
+      const int thr = 256;
+      const int blocks = (int)std::min<long>((total + thr - 1) / thr, 4096);
+      oaa::oaa_spectrum_kernel<<<blocks, thr, 0, s>>>(w, spec, K, C, n, 1, 1);
+      g_launches++;
+      if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
+    }
+    oaa::BwdDParams dp;
+    dp.dy = in;
+    dp.spec = spec;
+    dp.dx = out;
+    dp.B = B;
+    dp.K = K;
+    dp.C = C;
+    dp.M = R;
+    dp.N = Ro;
+    dp.Td = e.T;
+    dp.off = off;
+    dp.NCW = bd.NCW;
+    cudaError_t err = launch_bwdd(n, dp, C, bd.smem, s);
+    prof.stop();
+    return err == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
+  }
   if (wk.use) {
     {
       const long total = (long)K * C * ((g.P + 1) / 2) * g.H;
@@ -666,7 +734,8 @@ size_t oaa_conv_workspace_bytes(oaa_op_t op, int B, int C, int K, int N, int n, 
     const TcPlan tc = plan_tc(B, fwd ? C : K, fwd ? K : C, R, n);
     const int Ro = fwd ? g.M : N, off = fwd ? g.o : (n - 1 - g.o);
     const WalkHostGeo wk = plan_walk(fwd, B, fwd ? C : K, fwd ? K : C, cdiv(R, n), Ro, off, n, tc);
-    return engine_ws(B, C, K, cdiv(R, n), g, tc, &wk).total;
+    const BwddPlan bd = plan_bwdd(fwd, fwd ? K : C, R, n, tc);
+    return engine_ws(B, C, K, cdiv(R, n), g, tc, &wk, &bd).total;
   }
   if (op == OAA_OP_BWD_FILTER) {
     const TcFiltPlan t = plan_tc_filter(B, C, K, N, g.M, n);

@@ -1,0 +1,218 @@
+// oaa_bwdd.cuh -- bwd_data for layers with few input channels (C ≤ 4): the first of the
+// two backward convolutions of PAPER.md:89, dx = crop(Σ_k FullConv(dy_k, flip180 w_kc)),
+// evaluated by OaA over the n×n blocks of dy.
+//
+// One CTA per (image b, dy tile row t1).  Compute warp i owns chunk i of the tile row:
+// lanes (tt, f1) hold block t2 = i·TPW + tt, spectrum row f1.  A producer warp streams,
+// for every dy channel k in turn, the n dy rows of the tile row (cp.async, zero padded)
+// and the k-th slice of the flipped-kernel spectra into a ring of shared-memory stages
+// tracked by mbarriers (full: cp.async completion of the producer's 32 lanes; empty: one
+// arrival per compute warp), so compute warps never meet at a CTA barrier inside the k
+// loop.  Per k a lane computes its block-row spectrum Ĝ_k[f1,:] (pruned column DFT +
+// row codelet) and accumulates the C output spectra Ŷ_c += Ŵᶠ_{k,c}·Ĝ_k in registers.
+// Epilogue per output channel c: inverse DFT along f2 (stage A, lanes (tile, f1)) → Q in
+// shared memory → stage B (lanes = full-frame columns: the two block columns summed
+// before the Hermitian c2r along f1, as in the walker) → overlap-add into dx.
+//
+// The vertical overlap (n−1 rows shared by consecutive tile rows) crosses
+// CTAs: every value is added to dx (zeroed by the caller's launch sequence) with a
+// fire-and-forget red.global.add.f32.  Each dx element receives at most two addends onto
+// an exact zero and IEEE addition is commutative, so the result is bitwise deterministic
+// whatever order the two CTAs reach it in.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dft.cuh"
+#include "oaa_kernels.cuh"
+#include "oaa_walk.cuh"
+
+namespace oaa {
+
+struct BwdDParams {
+  const float* dy;     // [B][K][M][M]
+  const float4* spec;  // [K][C][P2][H] float4: DFT_P(flip180 w_kc)/P² (oaa_spectrum_kernel, flip, loop over k)
+  float* dx;           // [B][C][N][N], zero on entry
+  int B, K, C, M, N, Td, off;  // off = n−1−o: full-frame column/row of dx element 0
+  int NCW;                     // compute warps (chunks of the tile row)
+};
+
+constexpr int kBwddStages = 8;  // ring depth (covers HBM latency)
+
+// float4 per Ŵ ring stage ([C][n][n], padded to 128 B)
+__host__ __device__ constexpr int bwdd_w4_stride(int n, int C) { return (C * n * n + 7) & ~7; }
+__host__ __device__ constexpr size_t bwdd_smem_bytes(int n, int C, int NCW) {
+  return (size_t)kBwddStages * bwdd_w4_stride(n, C) * 16 + (size_t)NCW * kBwddStages * n * ((32 / n) * n) * 4 +
+         (size_t)(NCW * (32 / n) + 1) * n * (2 * n - 1) * 8;
+}
+
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Shared memory: Ŵ ring [kBwddStages][C][P2][H] float4 (filled by the producer warp) |
+// per-compute-warp dy ring [NCW][kBwddStages][n][CW] floats (each warp stages the n rows
+// of its own CW columns) | Q [(NCW·TPW + 1) tiles][H][P] float2 (last tile zero).
+template <int NN, int CR>
+__global__ void __launch_bounds__(288, 1) oaa_bwdd_kernel(const BwdDParams p) {
+  using G = WalkGeo<NN>;
+  constexpr int P = G::P, H = G::H, P2 = G::P2, TPW = G::TPW, QT = G::QT, CW = G::CW;
+  constexpr int S = kBwddStages;
+  constexpr int DYS = NN * CW;                // floats per warp stage
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint64_t full[S], empty[S];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NCW = p.NCW;
+  const int item = blockIdx.x;
+  const int b = item / p.Td, t1 = item - (item / p.Td) * p.Td;
+  const int w4 = p.C * P2 * H;                // float4 of kernel spectra per stage
+  const int w4s = bwdd_w4_stride(NN, p.C);    // float4 per stage (padded)
+  float4* Wring = reinterpret_cast<float4*>(smem_raw);
+  float* dyring = reinterpret_cast<float*>(Wring + S * w4s);
+  float2* Q = reinterpret_cast<float2*>(dyring + (size_t)NCW * S * DYS);
+  const int ntile_q = NCW * TPW;  // tiles held in Q; tile ntile_q is the zero tile
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 32);
+      mbar_init(&empty[s], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int e = tid; e < QT; e += blockDim.x) Q[ntile_q * QT + e] = make_float2(0.f, 0.f);
+  __syncthreads();
+
+  if (warp == NCW) {
+    // ---------------- producer: kernel spectra of channel k into stage k % S
+    for (int k = 0; k < p.K; ++k) {
+      const int s = k % S;
+      if (k >= S) mbar_wait(&empty[s], ((k / S) - 1) & 1);
+      float4* wd = Wring + s * w4s;
+      const float4* ws = p.spec + (size_t)k * w4;
+      for (int e = lane; e < w4; e += 32) cp_async16(wd + e, ws + e);
+      cp_async_mbar_arrive_noinc(&full[s]);
+    }
+    cp_async_wait_all();
+    return;
+  }
+
+  // ---------------- compute warps: each stages its own columns of the n dy rows
+  const size_t planeM = (size_t)p.M * p.M;
+  const int col = warp * CW + lane;                     // staged column (lane < CW)
+  const bool cok = lane < CW && col < p.M;
+  int nrow = p.M - t1 * NN;                             // dy rows of this tile row inside dy
+  nrow = nrow < NN ? nrow : NN;
+  const float* src0 = p.dy + (size_t)b * p.K * planeM + (size_t)(t1 * NN) * p.M + (cok ? col : 0);
+  float* mydy = dyring + (size_t)warp * S * DYS;
+  auto stage_dy = [&](int k) {
+    if (k < p.K && lane < CW) {
+      const float* src = src0 + (size_t)k * planeM;
+      float* d = mydy + (k % S) * DYS + lane;
+#pragma unroll
+      for (int rr = 0; rr < NN; ++rr) {
+        const bool ok = cok && rr < nrow;
+        cp_async4(d + rr * CW, ok ? src + (size_t)rr * p.M : p.dy, ok);
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int k = 0; k < S - 1; ++k) stage_dy(k);
+
+  const int tt = lane / H, f1 = lane - (lane / H) * H;
+  const bool laneA = tt < TPW;
+  const int t2 = warp * TPW + tt;
+  float cf[NN], sf[NN];
+#pragma unroll
+  for (int p1 = 0; p1 < NN; ++p1) {
+    float s, c;
+    sincospif(2.0f * (float)((f1 * p1) % P) / (float)P, &s, &c);
+    cf[p1] = c;
+    sf[p1] = s;
+  }
+  float ar[CR][P], ai[CR][P];
+#pragma unroll
+  for (int c = 0; c < CR; ++c)
+#pragma unroll
+    for (int f = 0; f < P; ++f) { ar[c][f] = 0.f; ai[c][f] = 0.f; }
+
+  for (int k = 0; k < p.K; ++k) {
+    const int s = k % S;
+    stage_dy(k + S - 1);                                   // slot of k−1: consumed
+    asm volatile("cp.async.wait_group %0;" ::"n"(S - 1) : "memory");  // group k landed
+    __syncwarp();
+    mbar_wait(&full[s], (k / S) & 1);
+    if (laneA) {
+      float gr[P], gi[P];
+      block_row_spectrum_smem<NN>(mydy + s * DYS, CW, tt * NN, cf, sf, gr, gi);
+      const float4* W = Wring + s * w4s + f1;
+#pragma unroll
+      for (int c = 0; c < CR; ++c) {
+        if (c < p.C) {
+#pragma unroll
+          for (int q = 0; q < P2; ++q) {
+            const float4 w = W[(c * P2 + q) * H];
+            const int f = 2 * q;
+            ar[c][f] = fmaf(w.x, gr[f], ar[c][f]);
+            ar[c][f] = fmaf(-w.y, gi[f], ar[c][f]);
+            ai[c][f] = fmaf(w.x, gi[f], ai[c][f]);
+            ai[c][f] = fmaf(w.y, gr[f], ai[c][f]);
+            if (f + 1 < P) {
+              ar[c][f + 1] = fmaf(w.z, gr[f + 1], ar[c][f + 1]);
+              ar[c][f + 1] = fmaf(-w.w, gi[f + 1], ar[c][f + 1]);
+              ai[c][f + 1] = fmaf(w.z, gi[f + 1], ai[c][f + 1]);
+              ai[c][f + 1] = fmaf(w.w, gr[f + 1], ai[c][f + 1]);
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  cp_async_wait_all();
+
+  // ---------------- epilogue: per output channel, inverse DFT + overlap-add into dx
+  const int nthr_c = 32 * NCW;
+  const int FW = p.Td * NN + NN - 1;  // full-frame width
+  const size_t planeN = (size_t)p.N * p.N;
+  const int I0 = t1 * NN - p.off;     // dx row of block row 0
+#pragma unroll
+  for (int c = 0; c < CR; ++c) {
+    if (c >= p.C) break;
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr_c) : "memory");  // Q free
+    if (laneA) {
+      float qr[P], qi[P];
+      dft<P, +1>(ar[c], ai[c], qr, qi);
+      float2* qd = Q + t2 * QT + f1 * P;
+      const bool real_tile = t2 < p.Td;
+#pragma unroll
+      for (int p2 = 0; p2 < P; ++p2) qd[p2] = real_tile ? make_float2(qr[p2], qi[p2]) : make_float2(0.f, 0.f);
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr_c) : "memory");  // Q complete
+    float* dxc = p.dx + ((size_t)b * p.C + c) * planeN;
+    for (int J = tid; J < FW; J += nthr_c) {
+      const int j = J - p.off;
+      if (j < 0 || j >= p.N) continue;
+      const int tA = J / NN, pA = J - (J / NN) * NN;
+      const int offA = (tA < p.Td ? tA : ntile_q) * QT + pA;
+      const int offB = (pA <= NN - 2 && tA >= 1) ? (tA - 1) * QT + pA + NN : ntile_q * QT;
+      float zr[H], zi[H];
+#pragma unroll
+      for (int f = 0; f < H; ++f) {
+        const float2 a = Q[offA + f * P], bb = Q[offB + f * P];
+        zr[f] = a.x + bb.x;
+        zi[f] = a.y + bb.y;
+      }
+      float y[P];
+      c2r_half<P>(zr, zi, y);
+#pragma unroll
+      for (int p1 = 0; p1 < P; ++p1) {
+        const int r = I0 + p1;
+        if (r >= 0 && r < p.N) atomicAdd(dxc + (size_t)r * p.N + j, y[p1]);
+      }
+    }
+  }
+}
+
+}  // namespace oaa

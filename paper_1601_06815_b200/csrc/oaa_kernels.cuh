@@ -1234,6 +1234,9 @@ __global__ void oaa_filter_finalize_kernel(const float2* __restrict__ partial, f
 __global__ void oaa_spectrum_kernel(const float* __restrict__ w, float4* __restrict__ spec, int K,
                                     int C, int n, int flip, int loop_is_k) {
   const int P = 2 * n - 1, H = n, P2 = (P + 1) / 2;
+  __shared__ double tc[16], ts[16];  // cos / sin (2π m / P), fp64
+  if (threadIdx.x < P) sincospi(2.0 * (double)threadIdx.x / (double)P, &ts[threadIdx.x], &tc[threadIdx.x]);
+  __syncthreads();
   const long total = (long)K * C * P2 * H;
   for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total;
        t += (long)gridDim.x * blockDim.x) {
@@ -1253,10 +1256,8 @@ __global__ void oaa_spectrum_kernel(const float* __restrict__ w, float4* __restr
         for (int p2 = 0; p2 < n; ++p2) {
           const float v = flip ? wk[(n - 1 - p1) * n + (n - 1 - p2)] : wk[p1 * n + p2];
           const int m = (f1 * p1 + f2 * p2) % P;
-          double s, cc;
-          sincospi(2.0 * (double)m / (double)P, &s, &cc);
-          sr += (double)v * cc;
-          si -= (double)v * s;
+          sr += (double)v * tc[m];
+          si -= (double)v * ts[m];
         }
       const double inv = 1.0 / ((double)P * (double)P);
       out[2 * h] = sr * inv;

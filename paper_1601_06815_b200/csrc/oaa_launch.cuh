@@ -11,6 +11,7 @@
 
 #include "oaa_kernels.cuh"
 #include "oaa_walk.cuh"
+#include "oaa_bwdd.cuh"
 
 namespace oaa_host {
 
@@ -156,6 +157,17 @@ cudaError_t launch_walk_n(const oaa::XSpecParams& xp, const oaa::WalkParams& wp,
   return cudaGetLastError();
 }
 
+template <int NN>
+cudaError_t launch_bwdd_n(const oaa::BwdDParams& p, int cr, size_t smem, cudaStream_t s) {
+  auto k = cr <= 1 ? oaa::oaa_bwdd_kernel<NN, 1> : cr == 2 ? oaa::oaa_bwdd_kernel<NN, 2>
+         : cr == 3 ? oaa::oaa_bwdd_kernel<NN, 3> : oaa::oaa_bwdd_kernel<NN, 4>;
+  cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  k<<<p.B * p.Td, 32 * (p.NCW + 1), smem, s>>>(p);
+  g_launches++;
+  return cudaGetLastError();
+}
+
 #define OAA_DECLARE_N(NN)                                                                      \
   extern template cudaError_t launch_engine_n<NN>(const oaa::EngineParams&, const EnginePlan&, \
                                                   cudaStream_t);                              \
@@ -163,7 +175,8 @@ cudaError_t launch_walk_n(const oaa::XSpecParams& xp, const oaa::WalkParams& wp,
                                                   cudaStream_t);                              \
   extern template cudaError_t launch_tile_spectra_n<NN>(const oaa::TileSpecParams&, size_t, cudaStream_t); \
   extern template cudaError_t launch_filter_spectra_n<NN>(const oaa::FiltSpecParams&, bool, int, size_t, cudaStream_t); \
-  extern template cudaError_t launch_walk_n<NN>(const oaa::XSpecParams&, const oaa::WalkParams&, const WalkPlan&, int, cudaStream_t);
+  extern template cudaError_t launch_walk_n<NN>(const oaa::XSpecParams&, const oaa::WalkParams&, const WalkPlan&, int, cudaStream_t); \
+  extern template cudaError_t launch_bwdd_n<NN>(const oaa::BwdDParams&, int, size_t, cudaStream_t);
 #define OAA_INSTANTIATE_N(NN)                                                                 \
   template cudaError_t launch_engine_n<NN>(const oaa::EngineParams&, const EnginePlan&,       \
                                            cudaStream_t);                                     \
@@ -171,6 +184,7 @@ cudaError_t launch_walk_n(const oaa::XSpecParams& xp, const oaa::WalkParams& wp,
                                            cudaStream_t);                                     \
   template cudaError_t launch_tile_spectra_n<NN>(const oaa::TileSpecParams&, size_t, cudaStream_t); \
   template cudaError_t launch_filter_spectra_n<NN>(const oaa::FiltSpecParams&, bool, int, size_t, cudaStream_t); \
-  template cudaError_t launch_walk_n<NN>(const oaa::XSpecParams&, const oaa::WalkParams&, const WalkPlan&, int, cudaStream_t);
+  template cudaError_t launch_walk_n<NN>(const oaa::XSpecParams&, const oaa::WalkParams&, const WalkPlan&, int, cudaStream_t); \
+  template cudaError_t launch_bwdd_n<NN>(const oaa::BwdDParams&, int, size_t, cudaStream_t);
 
 }  // namespace oaa_host

@@ -185,6 +185,11 @@ __global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
   int seq = 0;
   for (int t1 = 0; t1 < p.T; ++t1) {
     const int r0 = t1 * NN - p.off;  // output row of block row 0
+    unsigned rowmask = 0;            // rows p1 < n of this tile row inside [0, Ro)
+#pragma unroll
+    for (int p1 = 0; p1 < NN; ++p1)
+      if (r0 + p1 >= 0 && r0 + p1 < p.Ro) rowmask |= 1u << p1;
+    const bool rows_full = rowmask == (1u << NN) - 1u;
     for (int i = 0; i < p.NCH; ++i, ++seq) {
       const int s = seq % kWalkRing;
       mbar_wait(&full[s], (seq / kWalkRing) & 1);
@@ -234,7 +239,8 @@ __global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
       __syncwarp();
       if (lane == 0) {
         __threadfence_block();
-        const int old = atomicAdd(&rel[s], 1);
+        int old;
+        asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(&rel[s])) : "memory");
         if (old == nw - 1) {
           rel[s] = 0;
           __threadfence_block();
@@ -266,12 +272,23 @@ __global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
         float* cr = carry + J;
         const bool colok = j >= 0 && j < p.Ro;
         float* op = outp + (ptrdiff_t)r0 * p.Ro + j;
+        if (rows_full) {
+          if (colok) {
 #pragma unroll
-        for (int p1 = 0; p1 < NN; ++p1) {
-          float v = y[p1];
-          if (p1 < TR) v += cr[p1 * CWT];
-          const int r = r0 + p1;
-          if (colok && r >= 0 && r < p.Ro) __stcs(op + (ptrdiff_t)p1 * p.Ro, v);
+            for (int p1 = 0; p1 < NN; ++p1) {
+              float v = y[p1];
+              if (p1 < TR) v += cr[p1 * CWT];
+              __stcs(op, v);
+              op += p.Ro;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int p1 = 0; p1 < NN; ++p1) {
+            float v = y[p1];
+            if (p1 < TR) v += cr[p1 * CWT];
+            if (colok && ((rowmask >> p1) & 1u)) __stcs(op + (ptrdiff_t)p1 * p.Ro, v);
+          }
         }
 #pragma unroll
         for (int p1 = NN; p1 < P; ++p1) cr[(p1 - NN) * CWT] = y[p1];
