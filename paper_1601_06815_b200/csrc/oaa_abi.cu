@@ -215,6 +215,25 @@ cudaError_t launch_bwdd(int n, const oaa::BwdDParams& p, int cr, size_t smem, cu
   return cudaErrorInvalidValue;
 }
 
+struct BwdfLaunch {
+  size_t xspec_smem, smem;
+  int nkg;
+};
+cudaError_t launch_bwdf(int n, const oaa::XSpecParams& xp, const oaa::BwdFParams& fp, const BwdfLaunch& f,
+                        cudaStream_t s) {
+  switch (n) {
+    case 1: return launch_bwdf_n<1>(xp, fp, f.xspec_smem, f.smem, f.nkg, s);
+    case 2: return launch_bwdf_n<2>(xp, fp, f.xspec_smem, f.smem, f.nkg, s);
+    case 3: return launch_bwdf_n<3>(xp, fp, f.xspec_smem, f.smem, f.nkg, s);
+    case 4: return launch_bwdf_n<4>(xp, fp, f.xspec_smem, f.smem, f.nkg, s);
+    case 5: return launch_bwdf_n<5>(xp, fp, f.xspec_smem, f.smem, f.nkg, s);
+    case 6: return launch_bwdf_n<6>(xp, fp, f.xspec_smem, f.smem, f.nkg, s);
+    case 7: return launch_bwdf_n<7>(xp, fp, f.xspec_smem, f.smem, f.nkg, s);
+    case 8: return launch_bwdf_n<8>(xp, fp, f.xspec_smem, f.smem, f.nkg, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_filter(int n, const oaa::FilterParams& p, const FilterPlan& f, cudaStream_t s) {
   switch (n) {
     case 1: return launch_filter_n<1>(p, f, s);
@@ -313,11 +332,38 @@ BwddPlan plan_bwdd(bool is_fwd, int Cout, int R, int n, const TcPlan& tc) {
   const int H = n, P = 2 * n - 1, TPW = 32 / H, CW = TPW * n;
   const int Td = cdiv(R, n);
   d.NCW = cdiv(Td, TPW);
-  if (d.NCW > 8) d.use = false;
+  if (d.NCW > 7) d.use = false;  // 7 compute warps + the producer (256 threads, ≤ 255 registers)
   d.BW = d.NCW * CW;
   d.smem = oaa::bwdd_smem_bytes(n, Cout, d.NCW);
   if (d.smem > 220 * 1024) d.use = false;
   return d;
+}
+
+// bwd_filter for few input channels (oaa_bwdf.cuh) ------------------------------------
+struct BwdfPlan {
+  bool use;
+  int TPW, CW, CH4, NCH, Td, KPW, nkg, G, SW;
+  size_t xs_b, part_b, xspec_smem, smem;
+};
+BwdfPlan plan_bwdf(int B, int C, int K, int M, int n) {
+  BwdfPlan f{};
+  f.use = C <= kWalkMaxCin && std::getenv("OAA_NO_BWDF") == nullptr && B > 0;
+  const int H = n, P = 2 * n - 1;
+  f.TPW = 32 / H;
+  f.CW = f.TPW * n;
+  f.CH4 = f.TPW * H * (n | 1);
+  f.Td = cdiv(M, n);
+  f.NCH = cdiv(f.Td, f.TPW);
+  f.KPW = 32 / H;
+  f.nkg = cdiv(K, oaa::kBwdfWarps * f.KPW);
+  f.G = std::max(1, std::min(B * f.Td, 148 / f.nkg));
+  f.SW = cdiv(f.NCH * f.CW + n - 1, 4) * 4;
+  f.xs_b = align_up(sizeof(float4) * (size_t)B * f.Td * f.NCH * C * f.CH4);
+  f.part_b = align_up(sizeof(float2) * (size_t)f.G * K * C * P * H);
+  f.xspec_smem = sizeof(float) * (size_t)C * P * f.SW;
+  f.smem = oaa::bwdf_smem_bytes(n, C);
+  if (f.smem > 220 * 1024 || f.xspec_smem > 220 * 1024) f.use = false;
+  return f;
 }
 
 // workspace layouts ------------------------------------------------------------
@@ -594,6 +640,7 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
     xp.T = e.T;
     xp.NCH = wk.NCH;
     xp.SW = wk.NCH * wk.CW;
+    xp.org = 0;
     oaa::WalkParams wp;
     wp.S = xp.S;
     wp.spec = spec;
@@ -740,6 +787,8 @@ size_t oaa_conv_workspace_bytes(oaa_op_t op, int B, int C, int K, int N, int n, 
   if (op == OAA_OP_BWD_FILTER) {
     const TcFiltPlan t = plan_tc_filter(B, C, K, N, g.M, n);
     if (t.use) return t.a_b + t.b_b + t.part_b;
+    const BwdfPlan bf = plan_bwdf(B, C, K, g.M, n);
+    if (bf.use) return bf.xs_b + bf.part_b;
     FilterPlan f;
     if (!plan_filter(B, C, K, g.M, n, &f)) return 0;
     return align_up(sizeof(float2) * (size_t)f.G * K * C * g.P * g.H);
@@ -778,6 +827,42 @@ oaa_status_t oaa_conv_bwd_filter(const float* x, const float* dy, float* dw, int
   }
   const TcFiltPlan tcf = plan_tc_filter(B, C, K, N, g.M, n);
   if (tcf.use) return run_filter_tc(x, dy, dw, B, C, K, N, n, g, tcf, ws, ws_bytes, s, x_bytes, dy_bytes, dw_bytes);
+  const BwdfPlan bf = plan_bwdf(B, C, K, g.M, n);
+  if (bf.use) {
+    const size_t need = bf.xs_b + bf.part_b;
+    if (!ws || ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0) return OAA_ERR_WORKSPACE;
+    if (overlaps(ws, need, dw, dw_bytes) || overlaps(ws, need, x, x_bytes) || overlaps(ws, need, dy, dy_bytes))
+      return OAA_ERR_INVALID_VALUE;
+    char* base = static_cast<char*>(ws);
+    oaa::XSpecParams xp;
+    xp.in = x;
+    xp.S = reinterpret_cast<float4*>(base);
+    xp.Cin = C;
+    xp.R = N;
+    xp.T = bf.Td;
+    xp.NCH = bf.NCH;
+    xp.SW = bf.SW;
+    xp.org = g.o - (n - 1);
+    oaa::BwdFParams fp;
+    fp.dy = dy;
+    fp.XS = xp.S;
+    fp.partial = reinterpret_cast<float2*>(base + bf.xs_b);
+    fp.B = B;
+    fp.K = K;
+    fp.C = C;
+    fp.M = g.M;
+    fp.Td = bf.Td;
+    fp.NCH = bf.NCH;
+    fp.G = bf.G;
+    ProfScope prof(OAA_OP_BWD_FILTER, s);
+    prof.start();
+    cudaError_t err = launch_bwdf(n, xp, fp, BwdfLaunch{bf.xspec_smem, bf.smem, bf.nkg}, s);
+    prof.stop();
+    if (err != cudaSuccess) return OAA_ERR_CUDA;
+    oaa::oaa_filter_finalize_kernel<<<K * C, 128, sizeof(double2) * g.P * g.H, s>>>(fp.partial, dw, bf.G, K, C, n);
+    g_launches++;
+    return cudaGetLastError() == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
+  }
   FilterPlan f;
   if (!plan_filter(B, C, K, g.M, n, &f)) return OAA_ERR_UNSUPPORTED;
   const size_t need = align_up(sizeof(float2) * (size_t)f.G * K * C * g.P * g.H);

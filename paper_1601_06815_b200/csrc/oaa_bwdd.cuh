@@ -54,7 +54,7 @@ __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
 // per-compute-warp dy ring [NCW][kBwddStages][n][CW] floats (each warp stages the n rows
 // of its own CW columns) | Q [(NCW·TPW + 1) tiles][H][P] float2 (last tile zero).
 template <int NN, int CR>
-__global__ void __launch_bounds__(288, 1) oaa_bwdd_kernel(const BwdDParams p) {
+__global__ void __launch_bounds__(256, 1) oaa_bwdd_kernel(const BwdDParams p) {
   using G = WalkGeo<NN>;
   constexpr int P = G::P, H = G::H, P2 = G::P2, TPW = G::TPW, QT = G::QT, CW = G::CW;
   constexpr int S = kBwddStages;
@@ -108,16 +108,27 @@ __global__ void __launch_bounds__(288, 1) oaa_bwdd_kernel(const BwdDParams p) {
     if (k < p.K && lane < CW) {
       const float* src = src0 + (size_t)k * planeM;
       float* d = mydy + (k % S) * DYS + lane;
+      if (cok && nrow == NN) {
 #pragma unroll
-      for (int rr = 0; rr < NN; ++rr) {
-        const bool ok = cok && rr < nrow;
-        cp_async4(d + rr * CW, ok ? src + (size_t)rr * p.M : p.dy, ok);
+        for (int rr = 0; rr < NN; ++rr) {
+          cp_async4(d, src, true);
+          src += p.M;
+          d += CW;
+        }
+      } else {
+#pragma unroll
+        for (int rr = 0; rr < NN; ++rr) {
+          const bool ok = cok && rr < nrow;
+          cp_async4(d, ok ? src : p.dy, ok);
+          src += p.M;
+          d += CW;
+        }
       }
     }
     cp_async_commit();
   };
 #pragma unroll
-  for (int k = 0; k < S - 1; ++k) stage_dy(k);
+  for (int k = 0; k < S - 2; ++k) stage_dy(k);
 
   const int tt = lane / H, f1 = lane - (lane / H) * H;
   const bool laneA = tt < TPW;
@@ -136,39 +147,65 @@ __global__ void __launch_bounds__(288, 1) oaa_bwdd_kernel(const BwdDParams p) {
 #pragma unroll
     for (int f = 0; f < P; ++f) { ar[c][f] = 0.f; ai[c][f] = 0.f; }
 
-  for (int k = 0; k < p.K; ++k) {
-    const int s = k % S;
-    stage_dy(k + S - 1);                                   // slot of k−1: consumed
-    asm volatile("cp.async.wait_group %0;" ::"n"(S - 1) : "memory");  // group k landed
-    __syncwarp();
-    mbar_wait(&full[s], (k / S) & 1);
-    if (laneA) {
-      float gr[P], gi[P];
-      block_row_spectrum_smem<NN>(mydy + s * DYS, CW, tt * NN, cf, sf, gr, gi);
-      const float4* W = Wring + s * w4s + f1;
+  auto accum = [&](int s, const float (&gr)[P], const float (&gi)[P]) {
+    const float4* W = Wring + s * w4s + f1;
 #pragma unroll
-      for (int c = 0; c < CR; ++c) {
-        if (c < p.C) {
+    for (int c = 0; c < CR; ++c) {
+      if (c < p.C) {
 #pragma unroll
-          for (int q = 0; q < P2; ++q) {
-            const float4 w = W[(c * P2 + q) * H];
-            const int f = 2 * q;
-            ar[c][f] = fmaf(w.x, gr[f], ar[c][f]);
-            ar[c][f] = fmaf(-w.y, gi[f], ar[c][f]);
-            ai[c][f] = fmaf(w.x, gi[f], ai[c][f]);
-            ai[c][f] = fmaf(w.y, gr[f], ai[c][f]);
-            if (f + 1 < P) {
-              ar[c][f + 1] = fmaf(w.z, gr[f + 1], ar[c][f + 1]);
-              ar[c][f + 1] = fmaf(-w.w, gi[f + 1], ar[c][f + 1]);
-              ai[c][f + 1] = fmaf(w.z, gi[f + 1], ai[c][f + 1]);
-              ai[c][f + 1] = fmaf(w.w, gr[f + 1], ai[c][f + 1]);
-            }
+        for (int q = 0; q < P2; ++q) {
+          const float4 w = W[(c * P2 + q) * H];
+          const int f = 2 * q;
+          ar[c][f] = fmaf(w.x, gr[f], ar[c][f]);
+          ar[c][f] = fmaf(-w.y, gi[f], ar[c][f]);
+          ai[c][f] = fmaf(w.x, gi[f], ai[c][f]);
+          ai[c][f] = fmaf(w.y, gr[f], ai[c][f]);
+          if (f + 1 < P) {
+            ar[c][f + 1] = fmaf(w.z, gr[f + 1], ar[c][f + 1]);
+            ar[c][f + 1] = fmaf(-w.w, gi[f + 1], ar[c][f + 1]);
+            ai[c][f + 1] = fmaf(w.z, gi[f + 1], ai[c][f + 1]);
+            ai[c][f + 1] = fmaf(w.w, gr[f + 1], ai[c][f + 1]);
           }
         }
       }
     }
+  };
+  // two dy channels per step: their block transforms are independent (ILP); the
+  // prefetch distance is S − 2 so the two refilled stages are the ones just consumed
+  int k = 0;
+  for (; k + 1 < p.K; k += 2) {
+    const int s0 = k % S, s1 = (k + 1) % S;
+    stage_dy(k + S - 2);
+    stage_dy(k + S - 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(S - 2) : "memory");  // groups k, k+1 landed
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    mbar_wait(&full[s0], (k / S) & 1);
+    mbar_wait(&full[s1], ((k + 1) / S) & 1);
+    if (laneA) {
+      float g0r[P], g0i[P], g1r[P], g1i[P];
+      block_row_spectrum_smem<NN>(mydy + s0 * DYS, CW, tt * NN, cf, sf, g0r, g0i);
+      block_row_spectrum_smem<NN>(mydy + s1 * DYS, CW, tt * NN, cf, sf, g1r, g1i);
+      accum(s0, g0r, g0i);
+      accum(s1, g1r, g1i);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&empty[s0]);
+      mbar_arrive(&empty[s1]);
+    }
+  }
+  if (k < p.K) {  // odd K: last channel
+    const int s0 = k % S;
+    cp_async_wait_all();
+    __syncwarp();
+    mbar_wait(&full[s0], (k / S) & 1);
+    if (laneA) {
+      float gr[P], gi[P];
+      block_row_spectrum_smem<NN>(mydy + s0 * DYS, CW, tt * NN, cf, sf, gr, gi);
+      accum(s0, gr, gi);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s0]);
   }
   cp_async_wait_all();
 

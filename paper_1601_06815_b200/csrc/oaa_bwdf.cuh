@@ -1,0 +1,226 @@
+// oaa_bwdf.cuh -- bwd_filter (the second backward convolution of PAPER.md:89, the
+// correlation of input and output-gradient blocks):
+//   dŴ[f][k][c] = Σ_{b, dy block s} conj(Ĝ_s[k][f]) · Ξ̂_s[c][f]
+// with Ĝ_s the spectrum of dy block s (n×n, zero padded to P×P) and Ξ̂_s the spectrum of
+// the (2n−1)² x-window of that block (computed once per (image, block, channel) by
+// oaa_xspec_kernel<n, true> into the chunked layout of oaa_walk.cuh).
+//
+// CTA (g, k-group): 8 warps, warp w owns KPW = ⌊32/H⌋ kernels, lanes (ks, f1), and
+// accumulates the lane's dŴ row f1 for all C channels in registers over a static,
+// deterministic slice of the (image, dy tile row) items (item = g + j·G).  Per chunk of
+// TPW dy blocks:
+//   * Ξ̂ of the chunk arrives in a shared ring by bulk copy (TMA engine); the last warp to
+//     release a slot refills it (as in the walker), no producer warp, no CTA barrier;
+//   * each warp stages the n dy rows × CW columns of its KPW kernels itself (cp.async,
+//     per-warp ring), so warps never wait for each other;
+//   * per block: Ĝ row f1 (pruned column DFT + row codelet), then the C complex MACs.
+// Partial spectra go to partial[g][k][c][f2][f1]; oaa_filter_finalize_kernel sums the G
+// slices in fp64 (fixed order), inverse-transforms and reads the lags.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dft.cuh"
+#include "oaa_kernels.cuh"
+#include "oaa_walk.cuh"
+
+namespace oaa {
+
+struct BwdFParams {
+  const float* dy;    // [B][K][M][M]
+  const float4* XS;   // Ξ̂ chunks [B·Td][NCH][C][32][RS4]
+  float2* partial;    // [G][K][C][P][H]
+  int B, K, C, M, Td, NCH, G;
+};
+
+constexpr int kBwdfRing = 4;    // Ξ̂ chunk slots
+constexpr int kBwdfDy = 3;      // per-warp dy stages
+constexpr int kBwdfWarps = 8;
+
+__host__ __device__ constexpr size_t bwdf_smem_bytes(int n, int C) {
+  return (size_t)kBwdfRing * C * ((32 / n) * n * (n | 1)) * 16 +
+         (size_t)kBwdfWarps * kBwdfDy * (32 / n) * n * ((32 / n) * n) * 4;
+}
+
+template <int NN, int CR>
+__global__ void __launch_bounds__(32 * kBwdfWarps, 1) oaa_bwdf_kernel(const BwdFParams p) {
+  using G = WalkGeo<NN>;
+  constexpr int P = G::P, H = G::H, P2 = G::P2, TPW = G::TPW, CW = G::CW, RS4 = G::RS4;
+  constexpr int KPW = 32 / H;                 // kernels per warp
+  constexpr int DYS = KPW * NN * CW;          // floats per warp dy stage
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint64_t full[kBwdfRing];
+  __shared__ int rel[kBwdfRing];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nw = kBwdfWarps;
+  const int slot4 = p.C * G::CH4;
+  float4* ring = reinterpret_cast<float4*>(smem_raw);
+  float* dyr = reinterpret_cast<float*>(ring + kBwdfRing * slot4) + (size_t)warp * kBwdfDy * DYS;
+  const int g = blockIdx.x;
+  const int nitems_all = p.B * p.Td;
+  const int nitems = g < nitems_all ? (nitems_all - g + p.G - 1) / p.G : 0;
+  const int nseq = nitems * p.NCH;
+  const uint32_t slot_bytes = (uint32_t)slot4 * 16u;
+  auto seq_src = [&](int sq) {
+    const int j = sq / p.NCH, i = sq - (sq / p.NCH) * p.NCH;
+    return p.XS + ((size_t)(g + j * p.G) * p.NCH + i) * slot4;
+  };
+  if (tid == 0) {
+    for (int s = 0; s < kBwdfRing; ++s) {
+      mbar_init(&full[s], 1);
+      rel[s] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < kBwdfRing && s < nseq; ++s) {
+      mbar_expect_tx(&full[s], slot_bytes);
+      bulk_g2s(ring + s * slot4, seq_src(s), slot_bytes, &full[s]);
+    }
+  }
+
+  const int ks = lane / H, f1 = lane - (lane / H) * H;
+  const int kbase = blockIdx.y * (nw * KPW) + warp * KPW;
+  const int k = kbase + ks;
+  const bool laneK = ks < KPW && k < p.K;
+  float cf[NN], sf[NN];
+#pragma unroll
+  for (int p1 = 0; p1 < NN; ++p1) {
+    float s, c;
+    sincospif(2.0f * (float)((f1 * p1) % P) / (float)P, &s, &c);
+    cf[p1] = c;
+    sf[p1] = s;
+  }
+  float ar[CR][P], ai[CR][P];
+#pragma unroll
+  for (int c = 0; c < CR; ++c)
+#pragma unroll
+    for (int f = 0; f < P; ++f) { ar[c][f] = 0.f; ai[c][f] = 0.f; }
+
+  // this warp's dy rows of chunk sq: rows (kernel kk, block row rr) × CW columns
+  const size_t planeM = (size_t)p.M * p.M;
+  auto stage_dy = [&](int sq) {
+    if (sq < nseq && lane < CW) {
+      const int j = sq / p.NCH, i = sq - (sq / p.NCH) * p.NCH;
+      const int item = g + j * p.G;
+      const int b = item / p.Td, t1 = item - (item / p.Td) * p.Td;
+      const int col = i * CW + lane;
+      const bool cok = col < p.M;
+      int nrow = p.M - t1 * NN;
+      nrow = nrow < NN ? nrow : NN;
+      float* d = dyr + (sq % kBwdfDy) * DYS + lane;
+      const float* src = p.dy + ((size_t)b * p.K + kbase) * planeM + (size_t)(t1 * NN) * p.M + (cok ? col : 0);
+      const int nk = min(KPW, p.K - kbase);
+      const ptrdiff_t kstep = (ptrdiff_t)planeM - (ptrdiff_t)NN * p.M;
+      if (cok && nk == KPW && nrow == NN) {  // interior: no predicates
+#pragma unroll
+        for (int kk = 0; kk < KPW; ++kk) {
+#pragma unroll
+          for (int rr = 0; rr < NN; ++rr) {
+            cp_async4(d, src, true);
+            src += p.M;
+            d += CW;
+          }
+          src += kstep;
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < KPW; ++kk) {
+          const bool kok = cok && kk < nk;
+#pragma unroll
+          for (int rr = 0; rr < NN; ++rr) {
+            const bool ok = kok && rr < nrow;
+            cp_async4(d, ok ? src : p.dy, ok);
+            src += p.M;
+            d += CW;
+          }
+          src += kstep;
+        }
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int sq = 0; sq < kBwdfDy - 1; ++sq) stage_dy(sq);
+
+  for (int sq = 0; sq < nseq; ++sq) {
+    const int s = sq % kBwdfRing;
+    stage_dy(sq + kBwdfDy - 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(kBwdfDy - 1) : "memory");
+    __syncwarp();
+    mbar_wait(&full[s], (sq / kBwdfRing) & 1);
+    if (laneK) {
+      const float* db = dyr + (sq % kBwdfDy) * DYS + ks * NN * CW;
+      const float4* xs = ring + s * slot4 + f1 * RS4;
+      // two blocks per step: independent transforms interleave (ILP)
+      auto accum = [&](int tt, const float (&gr)[P], const float (&gi)[P]) {
+        const float4* xt = xs + tt * H * RS4;
+#pragma unroll
+        for (int c = 0; c < CR; ++c) {
+          if (c < p.C) {
+#pragma unroll
+            for (int q = 0; q < P2; ++q) {
+              const float4 X = xt[c * G::CH4 + q];
+              const int f = 2 * q;
+              ar[c][f] = fmaf(gr[f], X.x, ar[c][f]);
+              ar[c][f] = fmaf(gi[f], X.y, ar[c][f]);
+              ai[c][f] = fmaf(gr[f], X.y, ai[c][f]);
+              ai[c][f] = fmaf(-gi[f], X.x, ai[c][f]);
+              if (f + 1 < P) {
+                ar[c][f + 1] = fmaf(gr[f + 1], X.z, ar[c][f + 1]);
+                ar[c][f + 1] = fmaf(gi[f + 1], X.w, ar[c][f + 1]);
+                ai[c][f + 1] = fmaf(gr[f + 1], X.w, ai[c][f + 1]);
+                ai[c][f + 1] = fmaf(-gi[f + 1], X.z, ai[c][f + 1]);
+              }
+            }
+          }
+        }
+      };
+      int tt = 0;
+#pragma unroll 1
+      for (; tt + 1 < TPW; tt += 2) {
+        float g0r[P], g0i[P], g1r[P], g1i[P];
+        block_row_spectrum_smem<NN>(db, CW, tt * NN, cf, sf, g0r, g0i);
+        block_row_spectrum_smem<NN>(db, CW, (tt + 1) * NN, cf, sf, g1r, g1i);
+        accum(tt, g0r, g0i);
+        accum(tt + 1, g1r, g1i);
+      }
+      if (tt < TPW) {
+        float gr[P], gi[P];
+        block_row_spectrum_smem<NN>(db, CW, tt * NN, cf, sf, gr, gi);
+        accum(tt, gr, gi);
+      }
+    }
+    // release the Ξ̂ slot; the last warp out refills it
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      int old;
+      asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(&rel[s])) : "memory");
+      if (old == nw - 1) {
+        rel[s] = 0;
+        __threadfence_block();
+        const int nx = sq + kBwdfRing;
+        if (nx < nseq) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect_tx(&full[s], slot_bytes);
+          bulk_g2s(ring + s * slot4, seq_src(nx), slot_bytes, &full[s]);
+        }
+      }
+    }
+  }
+  cp_async_wait_all();
+  if (laneK) {
+#pragma unroll
+    for (int c = 0; c < CR; ++c) {
+      if (c < p.C) {
+        float2* dst = p.partial + ((((size_t)g * p.K + k) * p.C + c) * P) * H + f1;
+#pragma unroll
+        for (int f2 = 0; f2 < P; ++f2) dst[f2 * H] = make_float2(ar[c][f2], ai[c][f2]);
+      }
+    }
+  }
+}
+
+}  // namespace oaa

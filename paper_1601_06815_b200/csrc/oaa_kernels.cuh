@@ -1200,6 +1200,8 @@ __global__ void oaa_filter_finalize_kernel(const float2* __restrict__ partial, f
   const int P = 2 * n - 1, H = n, bins = P * H;
   const int kc = blockIdx.x;
   extern __shared__ double2 S[];  // [P][H]
+  __shared__ double tc[16], ts[16];  // cos / sin (2π m / P)
+  if (threadIdx.x < P) sincospi(2.0 * (double)threadIdx.x / (double)P, &ts[threadIdx.x], &tc[threadIdx.x]);
   for (int t = threadIdx.x; t < bins; t += blockDim.x) {
     double sr = 0.0, si = 0.0;
     for (int g = 0; g < G; ++g) {
@@ -1219,10 +1221,8 @@ __global__ void oaa_filter_finalize_kernel(const float2* __restrict__ partial, f
       const double wgt = (f1 == 0) ? 1.0 : 2.0;
       for (int f2 = 0; f2 < P; ++f2) {
         const int m = (f1 * l1 + f2 * l2) % P;
-        double s, c;
-        sincospi(2.0 * (double)m / (double)P, &s, &c);
         const double2 z = S[f2 * H + f1];
-        acc += wgt * (z.x * c - z.y * s);
+        acc += wgt * (z.x * tc[m] - z.y * ts[m]);
       }
     }
     dw[(size_t)kc * n * n + t] = (float)(acc * inv);

@@ -12,6 +12,7 @@
 #include "oaa_kernels.cuh"
 #include "oaa_walk.cuh"
 #include "oaa_bwdd.cuh"
+#include "oaa_bwdf.cuh"
 
 namespace oaa_host {
 
@@ -141,7 +142,7 @@ template <int NN>
 cudaError_t launch_walk_n(const oaa::XSpecParams& xp, const oaa::WalkParams& wp, const WalkPlan& w, int cr,
                           cudaStream_t s) {
   {
-    auto k = oaa::oaa_xspec_kernel<NN>;
+    auto k = oaa::oaa_xspec_kernel<NN, false>;
     cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w.xspec_smem);
     if (err != cudaSuccess) return err;
     k<<<wp.B * wp.T, 256, w.xspec_smem, s>>>(xp);
@@ -168,6 +169,26 @@ cudaError_t launch_bwdd_n(const oaa::BwdDParams& p, int cr, size_t smem, cudaStr
   return cudaGetLastError();
 }
 
+template <int NN>
+cudaError_t launch_bwdf_n(const oaa::XSpecParams& xp, const oaa::BwdFParams& p, size_t xsmem, size_t smem, int nkg,
+                          cudaStream_t s) {
+  {
+    auto k = oaa::oaa_xspec_kernel<NN, true>;
+    cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsmem);
+    if (err != cudaSuccess) return err;
+    k<<<p.B * p.Td, 256, xsmem, s>>>(xp);
+    g_launches++;
+    if ((err = cudaGetLastError()) != cudaSuccess) return err;
+  }
+  auto k = p.C <= 1 ? oaa::oaa_bwdf_kernel<NN, 1> : p.C == 2 ? oaa::oaa_bwdf_kernel<NN, 2>
+         : p.C == 3 ? oaa::oaa_bwdf_kernel<NN, 3> : oaa::oaa_bwdf_kernel<NN, 4>;
+  cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  k<<<dim3(p.G, nkg), 32 * oaa::kBwdfWarps, smem, s>>>(p);
+  g_launches++;
+  return cudaGetLastError();
+}
+
 #define OAA_DECLARE_N(NN)                                                                      \
   extern template cudaError_t launch_engine_n<NN>(const oaa::EngineParams&, const EnginePlan&, \
                                                   cudaStream_t);                              \
@@ -176,7 +197,8 @@ cudaError_t launch_bwdd_n(const oaa::BwdDParams& p, int cr, size_t smem, cudaStr
   extern template cudaError_t launch_tile_spectra_n<NN>(const oaa::TileSpecParams&, size_t, cudaStream_t); \
   extern template cudaError_t launch_filter_spectra_n<NN>(const oaa::FiltSpecParams&, bool, int, size_t, cudaStream_t); \
   extern template cudaError_t launch_walk_n<NN>(const oaa::XSpecParams&, const oaa::WalkParams&, const WalkPlan&, int, cudaStream_t); \
-  extern template cudaError_t launch_bwdd_n<NN>(const oaa::BwdDParams&, int, size_t, cudaStream_t);
+  extern template cudaError_t launch_bwdd_n<NN>(const oaa::BwdDParams&, int, size_t, cudaStream_t); \
+  extern template cudaError_t launch_bwdf_n<NN>(const oaa::XSpecParams&, const oaa::BwdFParams&, size_t, size_t, int, cudaStream_t);
 #define OAA_INSTANTIATE_N(NN)                                                                 \
   template cudaError_t launch_engine_n<NN>(const oaa::EngineParams&, const EnginePlan&,       \
                                            cudaStream_t);                                     \
@@ -185,6 +207,7 @@ cudaError_t launch_bwdd_n(const oaa::BwdDParams& p, int cr, size_t smem, cudaStr
   template cudaError_t launch_tile_spectra_n<NN>(const oaa::TileSpecParams&, size_t, cudaStream_t); \
   template cudaError_t launch_filter_spectra_n<NN>(const oaa::FiltSpecParams&, bool, int, size_t, cudaStream_t); \
   template cudaError_t launch_walk_n<NN>(const oaa::XSpecParams&, const oaa::WalkParams&, const WalkPlan&, int, cudaStream_t); \
-  template cudaError_t launch_bwdd_n<NN>(const oaa::BwdDParams&, int, size_t, cudaStream_t);
+  template cudaError_t launch_bwdd_n<NN>(const oaa::BwdDParams&, int, size_t, cudaStream_t); \
+  template cudaError_t launch_bwdf_n<NN>(const oaa::XSpecParams&, const oaa::BwdFParams&, size_t, size_t, int, cudaStream_t);
 
 }  // namespace oaa_host

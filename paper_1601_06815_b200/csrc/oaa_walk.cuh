@@ -45,37 +45,44 @@ struct WalkGeo {
   static constexpr int QSZ = (QS + 1) * QT;              // + one always-zero tile
 };
 
-// Chunked spectrum layout (X̂ for fwd): S[b][t1][i][c][lane][RS4] float4, lane = tt·H + f1,
-// float4 q = (Re f, Im f, Re f+1, Im f+1) for f = 2q (f2 = P is zero).  Tiles past the
-// last real tile (padding to NCH·TPW) are zero.
+// Chunked spectrum layout (X̂ for fwd, Ξ̂ for bwd_filter): S[b][t1][i][c][lane][RS4]
+// float4, lane = tt·H + f1, float4 q = (Re f, Im f, Re f+1, Im f+1) for f = 2q (f2 = P is
+// zero).  Tiles past the last real tile (padding to NCH·TPW) are zero.
+//   WIN = false: the zero-padded n×n input block of tile (t1, t2), pruned DFT;
+//   WIN = true : the (2n−1)² x-window at (t1·n + org, t2·n + org) correlated with the dy
+//                block in the weight gradient, full DFT.
 struct XSpecParams {
   const float* in;  // [B][Cin][R][R]
   float4* S;        // chunked spectra
-  int Cin, R, T, NCH, SW;  // SW = staged row width (NCH·CW)
+  int Cin, R, T, NCH, SW;  // T tile rows (and columns), SW = staged row width
+  int org;                 // window origin offset (WIN only)
 };
 
-// One CTA per (image, tile row): the n input rows of every channel are staged (zero
-// padded), then each task (chunk i, channel c, lane) computes its block-row spectrum.
-template <int NN>
+// One CTA per (image, tile row): the rows of every channel are staged (zero padded),
+// then each task (chunk i, channel c, lane) computes its block-row spectrum.
+template <int NN, bool WIN>
 __global__ void __launch_bounds__(256) oaa_xspec_kernel(const XSpecParams p) {
   using G = WalkGeo<NN>;
   constexpr int P = G::P, H = G::H, RS4 = G::RS4;
-  extern __shared__ __align__(16) float rows_s[];  // [Cin][NN][SW]
+  constexpr int ROWS = WIN ? P : NN;
+  extern __shared__ __align__(16) float rows_s[];  // [Cin][ROWS][SW]
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int item = blockIdx.x;
   const int b = item / p.T, t1 = item - (item / p.T) * p.T;
   const float* in_b = p.in + (size_t)b * p.Cin * p.R * p.R;
+  const int org = WIN ? p.org : 0;
   {
     const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
-    for (int sg = warp; sg < p.Cin * NN; sg += nw) {
-      const int c = sg / NN, rr = sg - (sg / NN) * NN;
-      const int r = t1 * NN + rr;
-      const bool rok = r < p.R;
+    for (int sg = warp; sg < p.Cin * ROWS; sg += nw) {
+      const int c = sg / ROWS, rr = sg - (sg / ROWS) * ROWS;
+      const int r = t1 * NN + org + rr;
+      const bool rok = r >= 0 && r < p.R;
       const float* src = in_b + ((size_t)c * p.R + (rok ? r : 0)) * p.R;
-      float* d = rows_s + (c * NN + rr) * p.SW;
+      float* d = rows_s + (c * ROWS + rr) * p.SW;
       for (int q = lane; q < p.SW; q += 32) {
-        const bool ok = rok && q < p.R;
-        cp_async4(d + q, ok ? src + q : in_b, ok);
+        const int col = q + org;
+        const bool ok = rok && col >= 0 && col < p.R;
+        cp_async4(d + q, ok ? src + col : in_b, ok);
       }
     }
     cp_async_commit();
@@ -89,16 +96,56 @@ __global__ void __launch_bounds__(256) oaa_xspec_kernel(const XSpecParams p) {
     const int tt = lane / H, f1 = lane - (lane / H) * H;
     if (tt >= G::TPW) continue;
     const int i = ic / p.Cin, c = ic - (ic / p.Cin) * p.Cin;
-    float cf[NN], sf[NN];
-#pragma unroll
-    for (int p1 = 0; p1 < NN; ++p1) {
-      float s, co;
-      sincospif(2.0f * (float)((f1 * p1) % P) / (float)P, &s, &co);
-      cf[p1] = co;
-      sf[p1] = s;
-    }
     float xr[P], xi[P];
-    block_row_spectrum_smem<NN>(rows_s + c * NN * p.SW, p.SW, (i * G::TPW + tt) * NN, cf, sf, xr, xi);
+    const float* blk = rows_s + c * ROWS * p.SW;
+    const int c0 = (i * G::TPW + tt) * NN;
+    if constexpr (!WIN) {
+      float cf[NN], sf[NN];
+#pragma unroll
+      for (int p1 = 0; p1 < NN; ++p1) {
+        float s, co;
+        sincospif(2.0f * (float)((f1 * p1) % P) / (float)P, &s, &co);
+        cf[p1] = co;
+        sf[p1] = s;
+      }
+      block_row_spectrum_smem<NN>(blk, p.SW, c0, cf, sf, xr, xi);
+    } else {
+      float tcx[P], tsx[P];
+#pragma unroll
+      for (int p1 = 0; p1 < P; ++p1) {
+        float s, co;
+        sincospif(2.0f * (float)((f1 * p1) % P) / (float)P, &s, &co);
+        tcx[p1] = co;
+        tsx[p1] = s;
+      }
+      // column DFT of the window rows (row p1 = 0 has twiddle 1), rows read as float4
+      // when the staged width keeps them 16-byte aligned (c0 = t2·n)
+      float rr[P], ri[P];
+#pragma unroll
+      for (int p1 = 0; p1 < P; ++p1) {
+        float v[P + 3];
+        const float* row = blk + p1 * p.SW + c0;
+        if constexpr (NN % 4 == 0) {
+#pragma unroll
+          for (int q = 0; q < (P + 3) / 4; ++q) {
+            const float4 t = *reinterpret_cast<const float4*>(row + 4 * q);
+            v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < P; ++q) v[q] = row[q];
+        }
+#pragma unroll
+        for (int p2 = 0; p2 < P; ++p2) {
+          if (p1 == 0) { rr[p2] = v[p2]; ri[p2] = 0.f; }
+          else {
+            rr[p2] = fmaf(v[p2], tcx[p1], rr[p2]);
+            ri[p2] = fmaf(-v[p2], tsx[p1], ri[p2]);
+          }
+        }
+      }
+      dft<P, -1>(rr, ri, xr, xi);
+    }
     float4* d = out + (size_t)ic * G::CH4 + lane * RS4;
 #pragma unroll
     for (int q = 0; q < RS4; ++q) {
