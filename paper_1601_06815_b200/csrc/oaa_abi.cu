@@ -201,6 +201,20 @@ cudaError_t launch_walk(int n, const oaa::XSpecParams& xp, const oaa::WalkParams
   return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_walk_load(int n, const oaa::WalkParams& wp, size_t smem, int nimg, cudaStream_t s) {
+  switch (n) {
+    case 1: return launch_walk_load_n<1>(wp, smem, nimg, s);
+    case 2: return launch_walk_load_n<2>(wp, smem, nimg, s);
+    case 3: return launch_walk_load_n<3>(wp, smem, nimg, s);
+    case 4: return launch_walk_load_n<4>(wp, smem, nimg, s);
+    case 5: return launch_walk_load_n<5>(wp, smem, nimg, s);
+    case 6: return launch_walk_load_n<6>(wp, smem, nimg, s);
+    case 7: return launch_walk_load_n<7>(wp, smem, nimg, s);
+    case 8: return launch_walk_load_n<8>(wp, smem, nimg, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_bwdd(int n, const oaa::BwdDParams& p, int cr, size_t smem, cudaStream_t s) {
   switch (n) {
     case 1: return launch_bwdd_n<1>(p, cr, smem, s);
@@ -522,22 +536,24 @@ oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* 
   gp.mode = 0;
   gp.partial = nullptr;
   gp.NB = tc.NB;
-  oaa::EngineParams p;
-  std::memset(&p, 0, sizeof(p));
-  p.out = out;
-  p.flags = flags;
-  p.counter = counter;
-  p.D = D;
-  p.Cin = 0;
-  p.Cout = Cout;
-  p.R = e.R;
-  p.T = T;
-  p.Ro = e.Ro;
-  p.off = e.off;
-  p.TS = e.TS;
-  p.BW = e.BW;
-  p.ncomp = e.ncomp;
-  p.CIG = 1;
+  gp.Kuse = tc.Kc;
+  // walker in LOAD mode: inverse DFT + overlap-add of Ŷ straight from the GEMM output
+  const int TPW = 32 / n, CW = TPW * n;
+  oaa::WalkParams wp{};
+  wp.out = out;
+  wp.Cin = 0;
+  wp.Cout = Cout;
+  wp.T = T;
+  wp.Ro = e.Ro;
+  wp.off = e.off;
+  wp.NCH = cdiv(e.off + e.Ro, CW);
+  wp.KG = std::min(8, Cout);
+  wp.ngrp = cdiv(Cout, wp.KG);
+  wp.D = D;
+  const int QSZ = (2 * TPW + 1) * n * g.P;
+  const size_t walk_smem = sizeof(float2) * (size_t)wp.KG * QSZ + sizeof(float) * (size_t)wp.KG * (n - 1) * wp.NCH * CW;
+  (void)flags;
+  (void)counter;
   ProfScope prof(is_fwd ? OAA_OP_FWD : OAA_OP_BWD_DATA, s);
   prof.start();
   for (int b0 = 0; b0 < B; b0 += tc.bc) {
@@ -550,12 +566,10 @@ oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* 
     gp.ldd = (int)btc;
     gp.strideD = (long long)2 * Cout * btc;
     if (launch_bin_gemm(gp, s) != cudaSuccess) return OAA_ERR_CUDA;
-    if (cudaMemsetAsync(flags, 0, L.xg_off - L.flags_off, s) != cudaSuccess) return OAA_ERR_CUDA;
-    p.B = bc;
-    p.b0 = b0;
-    p.BTc = (int)btc;
-    p.num_items = bc * T;
-    if (launch_engine(n, p, e, s) != cudaSuccess) return OAA_ERR_CUDA;
+    wp.B = bc;
+    wp.b0 = b0;
+    wp.BTc = (int)btc;
+    if (launch_walk_load(n, wp, walk_smem, bc, s) != cudaSuccess) return OAA_ERR_CUDA;
   }
   prof.stop();
   (void)g;
@@ -738,10 +752,13 @@ oaa_status_t run_filter_tc(const float* x, const float* dy, float* dw, int B, in
     xs.b0 = b0;
     if (launch_filter_spectra(n, gs, false, bc * t.Td, smem_g, s) != cudaSuccess) return OAA_ERR_CUDA;
     if (launch_filter_spectra(n, xs, true, bc * t.Td, smem_x, s) != cudaSuccess) return OAA_ERR_CUDA;
+    // a short last chunk: the GEMM reduces only the K chunks holding data, and only the
+    // ragged end of the last one is zeroed
     const int j0 = 2 * bc * t.T2;
-    if (j0 < 32 * t.Kc) {
-      oaa::oaa_tc_zero_tail_kernel<<<512, 256, 0, s>>>(Ga, t.F, t.Kc, t.RTA, j0);
-      oaa::oaa_tc_zero_tail_kernel<<<512, 256, 0, s>>>(Xb, t.F, t.Kc, t.RTB, j0);
+    gp.Kuse = cdiv(j0, oaa::kTcK);
+    if (j0 < 32 * gp.Kuse) {
+      oaa::oaa_tc_zero_tail_kernel<<<512, 256, 0, s>>>(Ga, t.F, t.Kc, t.RTA, j0, 32 * gp.Kuse);
+      oaa::oaa_tc_zero_tail_kernel<<<512, 256, 0, s>>>(Xb, t.F, t.Kc, t.RTB, j0, 32 * gp.Kuse);
       g_launches += 2;
       if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
     }
@@ -929,7 +946,7 @@ oaa_status_t oaa_debug_bin_gemm(const float* A, const float* B, float* D, int F,
   p.NB = N > oaa::kTcM ? 2 : 1;
   p.Kc = cdiv(Kd, oaa::kTcK); p.RTA = cdiv(M, oaa::kTcM); p.RTB = cdiv(cdiv(N, oaa::kTcM), p.NB) * p.NB;
   p.strideD = (long long)M * N;
-  p.S = 1; p.kps = p.Kc; p.mode = 0; p.partial = nullptr; p.accumulate = 0;
+  p.S = 1; p.kps = p.Kc; p.mode = 0; p.partial = nullptr; p.accumulate = 0; p.Kuse = p.Kc;
   float* Ap = static_cast<float*>(ws);
   float* Bp = reinterpret_cast<float*>(static_cast<char*>(ws) + align_up(sizeof(float) * (size_t)F * p.Kc * 2 * p.RTA * 4096));
   oaa::oaa_tc_pack_kernel<<<1024, 256, 0, s>>>(A, Ap, F, M, Kd, p.Kc, p.RTA);

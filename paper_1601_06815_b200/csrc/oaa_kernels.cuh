@@ -1516,9 +1516,9 @@ __global__ void __launch_bounds__(256) oaa_filter_spectra_kernel(const FiltSpecP
 }
 
 #ifdef OAA_DEFINE_AUX_KERNELS
-// Zero the reduction tail j ∈ [j0, 32·Kc) of every row of a blocked operand.
-__global__ void oaa_tc_zero_tail_kernel(float* Op, int F, int Kc, int RT, int j0) {
-  const int tail = 32 * Kc - j0;
+// Zero the reduction columns j ∈ [j0, j1) of every row of a blocked operand.
+__global__ void oaa_tc_zero_tail_kernel(float* Op, int F, int Kc, int RT, int j0, int j1) {
+  const int tail = j1 - j0;
   if (tail <= 0) return;
   const long long total = (long long)F * 2 * RT * 128 * tail;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;

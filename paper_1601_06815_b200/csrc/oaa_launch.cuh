@@ -189,6 +189,16 @@ cudaError_t launch_bwdf_n(const oaa::XSpecParams& xp, const oaa::BwdFParams& p, 
   return cudaGetLastError();
 }
 
+template <int NN>
+cudaError_t launch_walk_load_n(const oaa::WalkParams& wp, size_t smem, int nimg, cudaStream_t s) {
+  auto k = oaa::oaa_walk_kernel<NN, 1, true>;
+  cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  k<<<nimg * wp.ngrp, 32 * wp.KG, smem, s>>>(wp);
+  g_launches++;
+  return cudaGetLastError();
+}
+
 #define OAA_DECLARE_N(NN)                                                                      \
   extern template cudaError_t launch_engine_n<NN>(const oaa::EngineParams&, const EnginePlan&, \
                                                   cudaStream_t);                              \
@@ -198,6 +208,7 @@ cudaError_t launch_bwdf_n(const oaa::XSpecParams& xp, const oaa::BwdFParams& p, 
   extern template cudaError_t launch_filter_spectra_n<NN>(const oaa::FiltSpecParams&, bool, int, size_t, cudaStream_t); \
   extern template cudaError_t launch_walk_n<NN>(const oaa::XSpecParams&, const oaa::WalkParams&, const WalkPlan&, int, cudaStream_t); \
   extern template cudaError_t launch_bwdd_n<NN>(const oaa::BwdDParams&, int, size_t, cudaStream_t); \
+  extern template cudaError_t launch_walk_load_n<NN>(const oaa::WalkParams&, size_t, int, cudaStream_t); \
   extern template cudaError_t launch_bwdf_n<NN>(const oaa::XSpecParams&, const oaa::BwdFParams&, size_t, size_t, int, cudaStream_t);
 #define OAA_INSTANTIATE_N(NN)                                                                 \
   template cudaError_t launch_engine_n<NN>(const oaa::EngineParams&, const EnginePlan&,       \
@@ -208,6 +219,7 @@ cudaError_t launch_bwdf_n(const oaa::XSpecParams& xp, const oaa::BwdFParams& p, 
   template cudaError_t launch_filter_spectra_n<NN>(const oaa::FiltSpecParams&, bool, int, size_t, cudaStream_t); \
   template cudaError_t launch_walk_n<NN>(const oaa::XSpecParams&, const oaa::WalkParams&, const WalkPlan&, int, cudaStream_t); \
   template cudaError_t launch_bwdd_n<NN>(const oaa::BwdDParams&, int, size_t, cudaStream_t); \
+  template cudaError_t launch_walk_load_n<NN>(const oaa::WalkParams&, size_t, int, cudaStream_t); \
   template cudaError_t launch_bwdf_n<NN>(const oaa::XSpecParams&, const oaa::BwdFParams&, size_t, size_t, int, cudaStream_t);
 
 }  // namespace oaa_host

@@ -50,6 +50,7 @@ struct BinGemmParams {
   int mode, Cf, H, P, g0, accumulate;
   float* partial;
   int NB;  // B row tiles per CTA (1: N tile 128, 2: N tile 256); RTB is a multiple of NB
+  int Kuse;  // K chunks holding data (≤ Kc; the rest of the layout is never read)
 };
 
 // UMMA shared-memory descriptor, K-major, no swizzle (Blackwell version 1).
@@ -116,7 +117,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) oaa_bin_gemm_kernel(const BinGe
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int f = blockIdx.z / p.S, split = blockIdx.z - (blockIdx.z / p.S) * p.S;
-  const int kbeg = split * p.kps, nk = min(p.Kc, kbeg + p.kps) - kbeg;
+  const int kbeg = split * p.kps, nk = min(min(p.Kc, p.Kuse), kbeg + p.kps) - kbeg;
   const int mt = blockIdx.y, nt = blockIdx.x;
   const int NB = p.NB, ntile = kTcM * NB;
   const int m0 = mt * kTcM, n0 = nt * ntile;

@@ -165,6 +165,10 @@ struct WalkParams {
   int B, Cin, Cout, T, Ro, off, NCH;
   int KG;              // output channels (warps) per CTA
   int ngrp;            // channel groups per image = ceil(Cout / KG)
+  // LOAD mode (tensor-core path): Ŷ = D[f][m][bt] of the bin GEMM (m < Cout real part,
+  // m ≥ Cout imaginary part; bt = (b − b0)·T² + t1·T + t2 over a batch chunk of BTc tiles)
+  const float* D;
+  int BTc, b0;
 };
 
 constexpr int kWalkRing = 4;  // spectrum chunk slots per CTA
@@ -172,7 +176,7 @@ constexpr int kWalkRing = 4;  // spectrum chunk slots per CTA
 // grid = B·ngrp CTAs (image-major: the groups of one image run side by side and share
 // its spectra through L2), KG warps each.
 // Shared memory: ring[kWalkRing][Cin·CH4] float4 | Q[KG][QSZ] float2 | carry[KG][n−1][NCH·CW].
-template <int NN, int CR>
+template <int NN, int CR, bool LOAD = false>
 __global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
   using G = WalkGeo<NN>;
   constexpr int P = G::P, H = G::H, P2 = G::P2, TPW = G::TPW, CW = G::CW, RS4 = G::RS4, QT = G::QT;
@@ -181,16 +185,17 @@ __global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
   __shared__ uint64_t full[kWalkRing];
   __shared__ int rel[kWalkRing];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const int b = blockIdx.x / p.ngrp, grp = blockIdx.x - (blockIdx.x / p.ngrp) * p.ngrp;
+  const int bl = blockIdx.x / p.ngrp, grp = blockIdx.x - (blockIdx.x / p.ngrp) * p.ngrp;
+  const int b = bl + (LOAD ? p.b0 : 0);
   const int co = grp * p.KG + warp;
-  const int slot4 = p.Cin * G::CH4;  // float4 per ring slot
+  const int slot4 = LOAD ? 0 : p.Cin * G::CH4;  // float4 per ring slot
   float4* ring = reinterpret_cast<float4*>(smem_raw);
   float2* Qall = reinterpret_cast<float2*>(ring + kWalkRing * slot4);
   float2* Q = Qall + warp * G::QSZ;
   const int CWT = p.NCH * CW;  // carry row length
   float* carry = reinterpret_cast<float*>(Qall + nw * G::QSZ) + warp * TR * CWT;
   const int nseq = p.T * p.NCH;
-  const float4* src = p.S + (size_t)b * nseq * slot4;
+  const float4* src = LOAD ? nullptr : p.S + (size_t)b * nseq * slot4;
   const uint32_t slot_bytes = (uint32_t)slot4 * 16u;
 
   if (tid == 0) {
@@ -204,7 +209,7 @@ __global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
   for (int e = lane; e < QT; e += 32) Q[G::QS * QT + e] = make_float2(0.f, 0.f);
   for (int e = lane; e < TR * CWT; e += 32) carry[e] = 0.f;
   __syncthreads();
-  if (tid == 0) {
+  if (!LOAD && tid == 0) {
     for (int s = 0; s < kWalkRing && s < nseq; ++s) {
       mbar_expect_tx(&full[s], slot_bytes);
       bulk_g2s(ring + s * slot4, src + (size_t)s * slot4, slot_bytes, &full[s]);
@@ -215,13 +220,33 @@ __global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
   // this lane's kernel spectra: Ŵ[co][c][f1 = lane mod H][f2], f2 pairs
   const int tt = lane / H, f1 = lane - (lane / H) * H;
   const bool laneA = tt < TPW;
-  float4 Wr[CR][P2];
+  float4 Wr[LOAD ? 1 : CR][P2];
+  if constexpr (!LOAD) {
 #pragma unroll
-  for (int c = 0; c < CR; ++c)
+    for (int c = 0; c < CR; ++c)
 #pragma unroll
-    for (int q = 0; q < P2; ++q)
-      Wr[c][q] = (active && laneA && c < p.Cin) ? __ldg(p.spec + (((size_t)co * p.Cin + c) * P2 + q) * H + f1)
-                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = 0; q < P2; ++q)
+        Wr[c][q] = (active && laneA && c < p.Cin) ? __ldg(p.spec + (((size_t)co * p.Cin + c) * P2 + q) * H + f1)
+                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  // LOAD: this lane's Ŷ row (bins f1·P + f2) for chunk (t1, i), prefetched one chunk ahead
+  float ynr[LOAD ? P : 1], yni[LOAD ? P : 1];
+  const size_t dstride = LOAD ? (size_t)2 * p.Cout * p.BTc : 0;  // per bin
+  const float* dlane = LOAD ? p.D + (size_t)(f1 * P) * dstride + (size_t)(active ? co : 0) * p.BTc + (size_t)bl * p.T * p.T
+                            : nullptr;
+  auto load_y = [&](int t1, int i) {
+    if constexpr (LOAD) {
+      const int t2 = i * TPW + tt;
+      const bool ok = active && laneA && t1 < p.T && t2 < p.T;
+      const float* d = dlane + (ok ? t1 * p.T + t2 : 0);
+#pragma unroll
+      for (int f2 = 0; f2 < P; ++f2) {
+        ynr[f2] = ok ? __ldg(d + (size_t)f2 * dstride) : 0.f;
+        yni[f2] = ok ? __ldg(d + (size_t)f2 * dstride + (size_t)p.Cout * p.BTc) : 0.f;
+      }
+    }
+  };
+  if (LOAD) load_y(0, 0);
   // stage-B geometry: lane = column J = i·CW + lane, tile J/n = i·TPW + lq at p2 = pA
   const int lq = lane / NN, pA = lane - (lane / NN) * NN;
   const bool laneB = lane < CW;
@@ -239,10 +264,24 @@ __global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
     const bool rows_full = rowmask == (1u << NN) - 1u;
     for (int i = 0; i < p.NCH; ++i, ++seq) {
       const int s = seq % kWalkRing;
-      mbar_wait(&full[s], (seq / kWalkRing) & 1);
+      if (!LOAD) mbar_wait(&full[s], (seq / kWalkRing) & 1);
       const int half = i & 1;
       // ---- stage A: contraction + inverse DFT along f2
-      if (active && laneA) {
+      if constexpr (LOAD) {
+        float yr[P], yi[P];
+#pragma unroll
+        for (int f2 = 0; f2 < P; ++f2) { yr[f2] = ynr[f2]; yi[f2] = yni[f2]; }
+        if (i + 1 < p.NCH) load_y(t1, i + 1);
+        else load_y(t1 + 1, 0);
+        if (active && laneA) {
+          float qr[P], qi[P];
+          dft<P, +1>(yr, yi, qr, qi);
+          float2* qd = Q + (half * TPW + tt) * QT + f1 * P;
+#pragma unroll
+          for (int p2 = 0; p2 < P; ++p2) qd[p2] = make_float2(qr[p2], qi[p2]);
+        }
+      } else {
+       if (active && laneA) {
         const float4* xs = ring + s * slot4 + lane * RS4;
         float yr[P], yi[P];
 #pragma unroll
@@ -282,9 +321,10 @@ __global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
 #pragma unroll
         for (int p2 = 0; p2 < P; ++p2) qd[p2] = make_float2(qr[p2], qi[p2]);
       }
+       }
       // release the ring slot; the last warp out refills it with chunk seq + kWalkRing
       __syncwarp();
-      if (lane == 0) {
+      if (!LOAD && lane == 0) {
         __threadfence_block();
         int old;
         asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(&rel[s])) : "memory");
