@@ -232,18 +232,19 @@ cudaError_t launch_bwdd(int n, const oaa::BwdDParams& p, int cr, size_t smem, cu
 struct BwdfLaunch {
   size_t xspec_smem, smem;
   int nkg;
+  bool tm;
 };
 cudaError_t launch_bwdf(int n, const oaa::XSpecParams& xp, const oaa::BwdFParams& fp, const BwdfLaunch& f,
                         cudaStream_t s) {
   switch (n) {
-    case 1: return launch_bwdf_n<1>(xp, fp, f.xspec_smem, f.smem, f.nkg, s);
-    case 2: return launch_bwdf_n<2>(xp, fp, f.xspec_smem, f.smem, f.nkg, s);
-    case 3: return launch_bwdf_n<3>(xp, fp, f.xspec_smem, f.smem, f.nkg, s);
-    case 4: return launch_bwdf_n<4>(xp, fp, f.xspec_smem, f.smem, f.nkg, s);
-    case 5: return launch_bwdf_n<5>(xp, fp, f.xspec_smem, f.smem, f.nkg, s);
-    case 6: return launch_bwdf_n<6>(xp, fp, f.xspec_smem, f.smem, f.nkg, s);
-    case 7: return launch_bwdf_n<7>(xp, fp, f.xspec_smem, f.smem, f.nkg, s);
-    case 8: return launch_bwdf_n<8>(xp, fp, f.xspec_smem, f.smem, f.nkg, s);
+    case 1: return launch_bwdf_n<1>(xp, fp, f.xspec_smem, f.smem, f.nkg, f.tm, s);
+    case 2: return launch_bwdf_n<2>(xp, fp, f.xspec_smem, f.smem, f.nkg, f.tm, s);
+    case 3: return launch_bwdf_n<3>(xp, fp, f.xspec_smem, f.smem, f.nkg, f.tm, s);
+    case 4: return launch_bwdf_n<4>(xp, fp, f.xspec_smem, f.smem, f.nkg, f.tm, s);
+    case 5: return launch_bwdf_n<5>(xp, fp, f.xspec_smem, f.smem, f.nkg, f.tm, s);
+    case 6: return launch_bwdf_n<6>(xp, fp, f.xspec_smem, f.smem, f.nkg, f.tm, s);
+    case 7: return launch_bwdf_n<7>(xp, fp, f.xspec_smem, f.smem, f.nkg, f.tm, s);
+    case 8: return launch_bwdf_n<8>(xp, fp, f.xspec_smem, f.smem, f.nkg, f.tm, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -357,6 +358,7 @@ BwddPlan plan_bwdd(bool is_fwd, int Cout, int R, int n, const TcPlan& tc) {
 struct BwdfPlan {
   bool use;
   int TPW, CW, CH4, NCH, Td, KPW, nkg, G, SW;
+  bool tm;
   size_t xs_b, part_b, xspec_smem, smem;
 };
 BwdfPlan plan_bwdf(int B, int C, int K, int M, int n) {
@@ -370,12 +372,13 @@ BwdfPlan plan_bwdf(int B, int C, int K, int M, int n) {
   f.NCH = cdiv(f.Td, f.TPW);
   f.KPW = 32 / H;
   f.nkg = cdiv(K, oaa::kBwdfWarps * f.KPW);
-  f.G = std::max(1, std::min(B * f.Td, 148 / f.nkg));
+  f.tm = std::getenv("OAA_BWDF_REG") == nullptr;  // TMEM accumulators, 2 CTAs / SM
+  f.G = std::max(1, std::min(B * f.Td, (f.tm ? 296 : 148) / f.nkg));
   f.SW = cdiv(f.NCH * f.CW + n - 1, 4) * 4;
   f.xs_b = align_up(sizeof(float4) * (size_t)B * f.Td * f.NCH * C * f.CH4);
   f.part_b = align_up(sizeof(float2) * (size_t)f.G * K * C * P * H);
   f.xspec_smem = sizeof(float) * (size_t)C * P * f.SW;
-  f.smem = oaa::bwdf_smem_bytes(n, C);
+  f.smem = f.tm ? oaa::bwdf_smem_bytes<true>(n, C) : oaa::bwdf_smem_bytes<false>(n, C);
   if (f.smem > 220 * 1024 || f.xspec_smem > 220 * 1024) f.use = false;
   return f;
 }
@@ -873,7 +876,7 @@ oaa_status_t oaa_conv_bwd_filter(const float* x, const float* dy, float* dw, int
     fp.G = bf.G;
     ProfScope prof(OAA_OP_BWD_FILTER, s);
     prof.start();
-    cudaError_t err = launch_bwdf(n, xp, fp, BwdfLaunch{bf.xspec_smem, bf.smem, bf.nkg}, s);
+    cudaError_t err = launch_bwdf(n, xp, fp, BwdfLaunch{bf.xspec_smem, bf.smem, bf.nkg, bf.tm}, s);
     prof.stop();
     if (err != cudaSuccess) return OAA_ERR_CUDA;
     oaa::oaa_filter_finalize_kernel<<<K * C, 128, sizeof(double2) * g.P * g.H, s>>>(fp.partial, dw, bf.G, K, C, n);

@@ -33,24 +33,33 @@ struct BwdFParams {
   int B, K, C, M, Td, NCH, G;
 };
 
-constexpr int kBwdfRing = 4;    // Ξ̂ chunk slots
-constexpr int kBwdfDy = 3;      // per-warp dy stages
 constexpr int kBwdfWarps = 8;
+// TM = false: dŴ accumulators in registers (1 CTA / SM, deeper rings);
+// TM = true : accumulators in tensor memory, ≤ 128 registers, 2 CTAs / SM.
+template <bool TM> struct BwdfCfg;
+template <> struct BwdfCfg<false> { static constexpr int ring = 4, dy = 3, minb = 1; };
+template <> struct BwdfCfg<true> { static constexpr int ring = 3, dy = 2, minb = 2; };
 
+template <bool TM>
 __host__ __device__ constexpr size_t bwdf_smem_bytes(int n, int C) {
-  return (size_t)kBwdfRing * C * ((32 / n) * n * (n | 1)) * 16 +
-         (size_t)kBwdfWarps * kBwdfDy * (32 / n) * n * ((32 / n) * n) * 4;
+  return (size_t)BwdfCfg<TM>::ring * C * ((32 / n) * n * (n | 1)) * 16 +
+         (size_t)kBwdfWarps * BwdfCfg<TM>::dy * (32 / n) * (n * ((32 / n) * n) + 4) * 4;
 }
 
-template <int NN, int CR>
-__global__ void __launch_bounds__(32 * kBwdfWarps, 1) oaa_bwdf_kernel(const BwdFParams p) {
+template <int NN, int CR, bool TM>
+__global__ void __launch_bounds__(32 * kBwdfWarps, BwdfCfg<TM>::minb) oaa_bwdf_kernel(const BwdFParams p) {
+  constexpr int kBwdfRing = BwdfCfg<TM>::ring, kBwdfDy = BwdfCfg<TM>::dy;
   using G = WalkGeo<NN>;
   constexpr int P = G::P, H = G::H, P2 = G::P2, TPW = G::TPW, CW = G::CW, RS4 = G::RS4;
   constexpr int KPW = 32 / H;                 // kernels per warp
-  constexpr int DYS = KPW * NN * CW;          // floats per warp dy stage
+  // floats per kernel in a dy stage: the n×CW rows + 4 floats of padding, so the KPW
+  // kernels a warp reads at the same block position hit different banks
+  constexpr int KSTR = NN * CW + 4;
+  constexpr int DYS = KPW * KSTR;             // floats per warp dy stage
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t full[kBwdfRing];
   __shared__ int rel[kBwdfRing];
+  __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nw = kBwdfWarps;
   const int slot4 = p.C * G::CH4;
@@ -72,7 +81,15 @@ __global__ void __launch_bounds__(32 * kBwdfWarps, 1) oaa_bwdf_kernel(const BwdF
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (TM && warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&s_tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // warp w: TMEM lanes 32·(w mod 4).., columns 128·(w / 4) + 32·c (c < CR ≤ 4)
+  const uint32_t tacc = TM ? s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * 128u : 0u;
   if (tid == 0) {
     for (int s = 0; s < kBwdfRing && s < nseq; ++s) {
       mbar_expect_tx(&full[s], slot_bytes);
@@ -92,11 +109,19 @@ __global__ void __launch_bounds__(32 * kBwdfWarps, 1) oaa_bwdf_kernel(const BwdF
     cf[p1] = c;
     sf[p1] = s;
   }
-  float ar[CR][P], ai[CR][P];
+  float ar[TM ? 1 : CR][P], ai[TM ? 1 : CR][P];
+  if constexpr (!TM) {
 #pragma unroll
-  for (int c = 0; c < CR; ++c)
+    for (int c = 0; c < CR; ++c)
 #pragma unroll
-    for (int f = 0; f < P; ++f) { ar[c][f] = 0.f; ai[c][f] = 0.f; }
+      for (int f = 0; f < P; ++f) { ar[c][f] = 0.f; ai[c][f] = 0.f; }
+  } else {
+    float z[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) z[q] = 0.f;
+#pragma unroll
+    for (int c = 0; c < CR; ++c) tm_st32(tacc + 32 * c, z);
+  }
 
   // this warp's dy rows of chunk sq: rows (kernel kk, block row rr) × CW columns
   const size_t planeM = (size_t)p.M * p.M;
@@ -123,6 +148,7 @@ __global__ void __launch_bounds__(32 * kBwdfWarps, 1) oaa_bwdf_kernel(const BwdF
             d += CW;
           }
           src += kstep;
+          d += KSTR - NN * CW;
         }
       } else {
 #pragma unroll
@@ -136,6 +162,7 @@ __global__ void __launch_bounds__(32 * kBwdfWarps, 1) oaa_bwdf_kernel(const BwdF
             d += CW;
           }
           src += kstep;
+          d += KSTR - NN * CW;
         }
       }
     }
@@ -151,10 +178,11 @@ __global__ void __launch_bounds__(32 * kBwdfWarps, 1) oaa_bwdf_kernel(const BwdF
     __syncwarp();
     mbar_wait(&full[s], (sq / kBwdfRing) & 1);
     if (laneK) {
-      const float* db = dyr + (sq % kBwdfDy) * DYS + ks * NN * CW;
+      const float* db = dyr + (sq % kBwdfDy) * DYS + ks * KSTR;
       const float4* xs = ring + s * slot4 + f1 * RS4;
       // two blocks per step: independent transforms interleave (ILP)
       auto accum = [&](int tt, const float (&gr)[P], const float (&gi)[P]) {
+        if constexpr (TM) return;
         const float4* xt = xs + tt * H * RS4;
 #pragma unroll
         for (int c = 0; c < CR; ++c) {
@@ -178,6 +206,7 @@ __global__ void __launch_bounds__(32 * kBwdfWarps, 1) oaa_bwdf_kernel(const BwdF
         }
       };
       int tt = 0;
+      if constexpr (TM) tt = TPW;  // (TM: the block loop below, outside the lane predicate)
 #pragma unroll 1
       for (; tt + 1 < TPW; tt += 2) {
         float g0r[P], g0i[P], g1r[P], g1i[P];
@@ -190,6 +219,43 @@ __global__ void __launch_bounds__(32 * kBwdfWarps, 1) oaa_bwdf_kernel(const BwdF
         float gr[P], gi[P];
         block_row_spectrum_smem<NN>(db, CW, tt * NN, cf, sf, gr, gi);
         accum(tt, gr, gi);
+      }
+    }
+    if constexpr (TM) {
+      // dŴ row in TMEM: per block, Ĝ row (registers) then per channel ld → MACs → st
+      const float* db = dyr + (sq % kBwdfDy) * DYS + (laneK ? ks : 0) * KSTR;
+      const float4* xs = ring + s * slot4 + f1 * RS4;
+#pragma unroll 1
+      for (int tt = 0; tt < TPW; ++tt) {
+        float gr[P], gi[P];
+        block_row_spectrum_smem<NN>(db, CW, tt * NN, cf, sf, gr, gi);
+        const float4* xt = xs + tt * H * RS4;
+        __syncwarp();
+        tmem_wait_st();
+#pragma unroll
+        for (int c = 0; c < CR; ++c) {
+          if (c < p.C) {
+            float a[32];
+            tm_ld32(tacc + 32 * c, a);
+            tmem_wait_ld();
+#pragma unroll
+            for (int q = 0; q < P2; ++q) {
+              const float4 X = xt[c * G::CH4 + q];
+              const int f = 2 * q;
+              a[f] = fmaf(gr[f], X.x, a[f]);
+              a[f] = fmaf(gi[f], X.y, a[f]);
+              a[16 + f] = fmaf(gr[f], X.y, a[16 + f]);
+              a[16 + f] = fmaf(-gi[f], X.x, a[16 + f]);
+              if (f + 1 < P) {
+                a[f + 1] = fmaf(gr[f + 1], X.z, a[f + 1]);
+                a[f + 1] = fmaf(gi[f + 1], X.w, a[f + 1]);
+                a[17 + f] = fmaf(gr[f + 1], X.w, a[17 + f]);
+                a[17 + f] = fmaf(-gi[f + 1], X.z, a[17 + f]);
+              }
+            }
+            tm_st32(tacc + 32 * c, a);
+          }
+        }
       }
     }
     // release the Ξ̂ slot; the last warp out refills it
@@ -211,7 +277,26 @@ __global__ void __launch_bounds__(32 * kBwdfWarps, 1) oaa_bwdf_kernel(const BwdF
     }
   }
   cp_async_wait_all();
-  if (laneK) {
+  if constexpr (TM) {
+    __syncwarp();
+    tmem_wait_st();
+#pragma unroll
+    for (int c = 0; c < CR; ++c) {
+      if (c < p.C) {
+        float a[32];
+        tm_ld32(tacc + 32 * c, a);
+        tmem_wait_ld();
+        if (laneK) {
+          float2* dst = p.partial + ((((size_t)g * p.K + k) * p.C + c) * P) * H + f1;
+#pragma unroll
+          for (int f2 = 0; f2 < P; ++f2) dst[f2 * H] = make_float2(a[f2], a[16 + f2]);
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(s_tmem));
+  } else if (laneK) {
 #pragma unroll
     for (int c = 0; c < CR; ++c) {
       if (c < p.C) {

@@ -171,7 +171,7 @@ cudaError_t launch_bwdd_n(const oaa::BwdDParams& p, int cr, size_t smem, cudaStr
 
 template <int NN>
 cudaError_t launch_bwdf_n(const oaa::XSpecParams& xp, const oaa::BwdFParams& p, size_t xsmem, size_t smem, int nkg,
-                          cudaStream_t s) {
+                          bool tm, cudaStream_t s) {
   {
     auto k = oaa::oaa_xspec_kernel<NN, true>;
     cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsmem);
@@ -180,8 +180,10 @@ cudaError_t launch_bwdf_n(const oaa::XSpecParams& xp, const oaa::BwdFParams& p, 
     g_launches++;
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
   }
-  auto k = p.C <= 1 ? oaa::oaa_bwdf_kernel<NN, 1> : p.C == 2 ? oaa::oaa_bwdf_kernel<NN, 2>
-         : p.C == 3 ? oaa::oaa_bwdf_kernel<NN, 3> : oaa::oaa_bwdf_kernel<NN, 4>;
+  auto k = tm ? (p.C <= 1 ? oaa::oaa_bwdf_kernel<NN, 1, true> : p.C == 2 ? oaa::oaa_bwdf_kernel<NN, 2, true>
+                : p.C == 3 ? oaa::oaa_bwdf_kernel<NN, 3, true> : oaa::oaa_bwdf_kernel<NN, 4, true>)
+              : (p.C <= 1 ? oaa::oaa_bwdf_kernel<NN, 1, false> : p.C == 2 ? oaa::oaa_bwdf_kernel<NN, 2, false>
+                : p.C == 3 ? oaa::oaa_bwdf_kernel<NN, 3, false> : oaa::oaa_bwdf_kernel<NN, 4, false>);
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   k<<<dim3(p.G, nkg), 32 * oaa::kBwdfWarps, smem, s>>>(p);
@@ -209,7 +211,7 @@ cudaError_t launch_walk_load_n(const oaa::WalkParams& wp, size_t smem, int nimg,
   extern template cudaError_t launch_walk_n<NN>(const oaa::XSpecParams&, const oaa::WalkParams&, const WalkPlan&, int, cudaStream_t); \
   extern template cudaError_t launch_bwdd_n<NN>(const oaa::BwdDParams&, int, size_t, cudaStream_t); \
   extern template cudaError_t launch_walk_load_n<NN>(const oaa::WalkParams&, size_t, int, cudaStream_t); \
-  extern template cudaError_t launch_bwdf_n<NN>(const oaa::XSpecParams&, const oaa::BwdFParams&, size_t, size_t, int, cudaStream_t);
+  extern template cudaError_t launch_bwdf_n<NN>(const oaa::XSpecParams&, const oaa::BwdFParams&, size_t, size_t, int, bool, cudaStream_t);
 #define OAA_INSTANTIATE_N(NN)                                                                 \
   template cudaError_t launch_engine_n<NN>(const oaa::EngineParams&, const EnginePlan&,       \
                                            cudaStream_t);                                     \
@@ -220,6 +222,6 @@ cudaError_t launch_walk_load_n(const oaa::WalkParams& wp, size_t smem, int nimg,
   template cudaError_t launch_walk_n<NN>(const oaa::XSpecParams&, const oaa::WalkParams&, const WalkPlan&, int, cudaStream_t); \
   template cudaError_t launch_bwdd_n<NN>(const oaa::BwdDParams&, int, size_t, cudaStream_t); \
   template cudaError_t launch_walk_load_n<NN>(const oaa::WalkParams&, size_t, int, cudaStream_t); \
-  template cudaError_t launch_bwdf_n<NN>(const oaa::XSpecParams&, const oaa::BwdFParams&, size_t, size_t, int, cudaStream_t);
+  template cudaError_t launch_bwdf_n<NN>(const oaa::XSpecParams&, const oaa::BwdFParams&, size_t, size_t, int, bool, cudaStream_t);
 
 }  // namespace oaa_host
