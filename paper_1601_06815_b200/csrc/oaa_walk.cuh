@@ -91,6 +91,19 @@ __global__ void __launch_bounds__(256) oaa_xspec_kernel(const XSpecParams p) {
   }
   float4* out = p.S + (size_t)item * p.NCH * p.Cin * G::CH4;
   const int ntask = p.NCH * p.Cin * 32;
+  // WIN: a thread's lane (and so its spectrum row f1) is the same for all its tasks (nthr
+  // is a multiple of 32), so its P column twiddles are computed once
+  float tcx[WIN ? ROWS : 1], tsx[WIN ? ROWS : 1];
+  if constexpr (WIN) {
+    const int f1 = (tid & 31) % H;
+#pragma unroll
+    for (int p1 = 0; p1 < ROWS; ++p1) {
+      float s, co;
+      sincospif(2.0f * (float)((f1 * p1) % P) / (float)P, &s, &co);
+      tcx[p1] = co;
+      tsx[p1] = s;
+    }
+  }
   for (int task = tid; task < ntask; task += nthr) {
     const int lane = task & 31, ic = task >> 5;
     const int tt = lane / H, f1 = lane - (lane / H) * H;
@@ -110,14 +123,6 @@ __global__ void __launch_bounds__(256) oaa_xspec_kernel(const XSpecParams p) {
       }
       block_row_spectrum_smem<NN>(blk, p.SW, c0, cf, sf, xr, xi);
     } else {
-      float tcx[P], tsx[P];
-#pragma unroll
-      for (int p1 = 0; p1 < P; ++p1) {
-        float s, co;
-        sincospif(2.0f * (float)((f1 * p1) % P) / (float)P, &s, &co);
-        tcx[p1] = co;
-        tsx[p1] = s;
-      }
       // column DFT of the window rows (row p1 = 0 has twiddle 1), rows read as float4
       // when the staged width keeps them 16-byte aligned (c0 = t2·n)
       float rr[P], ri[P];
