@@ -303,8 +303,16 @@ def run_ours(args, w):
     alu_peak = 2 * SM_COUNT * FP32_LANES_PER_SM * sm_mhz * 1e6 / 1e12  # TFLOP/s
     achieved = terms["flops"][dom] / (avg_ms / 1e3) / 1e12
     hbm_achieved = terms["bytes"][dom] / (avg_ms / 1e3) / 1e9
-    roofline = {"bound": "alu", "kernel": f"oaa main kernel ({dom})", "achieved": achieved,
-                "peak": alu_peak, "unit": "TFLOP/s", "frac": achieved / alu_peak, "traffic": None,
+    traffic = None
+    try:  # measured DRAM bytes of this op from the committed ncu capture (profiles/r1_ncu.md)
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+            traffic = json.load(f)[dom]["op_bytes"]
+    except Exception:
+        pass
+    roofline = {"bound": "alu", "kernel": f"oaa {dom} op (all its launches)", "achieved": achieved,
+                "peak": alu_peak, "unit": "TFLOP/s", "frac": achieved / alu_peak, "traffic": traffic,
+                "traffic_unit": "bytes per launch (ncu dram read+write, profiles/r1_traffic.json)",
+                "algorithmic_bytes": terms["bytes"][dom],
                 "peak_source": f"fp32 FFMA 148 SM x 128 lanes x 2 x {sm_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz, {src})",
                 "hbm_achieved_gbs": hbm_achieved, "hbm_peak_gbs": float(peaks.get("hbm_gbs", 6650.0)),
                 "hbm_frac": hbm_achieved / float(peaks.get("hbm_gbs", 6650.0)),
