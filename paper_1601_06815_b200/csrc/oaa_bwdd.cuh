@@ -53,14 +53,17 @@ __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
 // Shared memory: Ŵ ring [kBwddStages][C][P2][H] float4 (filled by the producer warp) |
 // per-compute-warp dy ring [NCW][kBwddStages][n][CW] floats (each warp stages the n rows
 // of its own CW columns) | Q [(NCW·TPW + 1) tiles][H][P] float2 (last tile zero).
-template <int NN, int CR>
-__global__ void __launch_bounds__(256, 1) oaa_bwdd_kernel(const BwdDParams p) {
+// TM = true: the C output spectra are accumulated in tensor memory (96 columns per warp)
+// instead of registers, so the kernel fits 128 registers and two CTAs share an SM.
+template <int NN, int CR, bool TM = false>
+__global__ void __launch_bounds__(256, TM ? 2 : 1) oaa_bwdd_kernel(const BwdDParams p) {
   using G = WalkGeo<NN>;
   constexpr int P = G::P, H = G::H, P2 = G::P2, TPW = G::TPW, QT = G::QT, CW = G::CW;
   constexpr int S = kBwddStages;
   constexpr int DYS = NN * CW;                // floats per warp stage
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t full[S], empty[S];
+  __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NCW = p.NCW;
   const int item = blockIdx.x;
@@ -80,7 +83,15 @@ __global__ void __launch_bounds__(256, 1) oaa_bwdd_kernel(const BwdDParams p) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int e = tid; e < QT; e += blockDim.x) Q[ntile_q * QT + e] = make_float2(0.f, 0.f);
+  if (TM && warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&s_tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // compute warp w: TMEM lanes 32·(w mod 4).., columns 128·(w / 4) + 32·c
+  const uint32_t tacc = TM ? s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * 128u : 0u;
 
   if (warp == NCW) {
     // ---------------- producer: kernel spectra of channel k into stage k % S
@@ -141,12 +152,50 @@ __global__ void __launch_bounds__(256, 1) oaa_bwdd_kernel(const BwdDParams p) {
     cf[p1] = c;
     sf[p1] = s;
   }
-  float ar[CR][P], ai[CR][P];
+  float ar[TM ? 1 : CR][P], ai[TM ? 1 : CR][P];
+  if constexpr (!TM) {
 #pragma unroll
-  for (int c = 0; c < CR; ++c)
+    for (int c = 0; c < CR; ++c)
 #pragma unroll
-    for (int f = 0; f < P; ++f) { ar[c][f] = 0.f; ai[c][f] = 0.f; }
+      for (int f = 0; f < P; ++f) { ar[c][f] = 0.f; ai[c][f] = 0.f; }
+  } else {
+    float z[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) z[q] = 0.f;
+#pragma unroll
+    for (int c = 0; c < CR; ++c) tm_st32(tacc + 32 * c, z);
+  }
 
+  // TM: acc[c] row in TMEM (re at columns f, im at 16 + f) += Ŵᶠ·Ĝ; warp-collective
+  auto accum_tm = [&](int s, const float (&gr)[P], const float (&gi)[P]) {
+    const float4* W = Wring + s * w4s + f1;
+    __syncwarp();
+    tmem_wait_st();
+#pragma unroll
+    for (int c = 0; c < CR; ++c) {
+      if (c < p.C) {
+        float a[32];
+        tm_ld32(tacc + 32 * c, a);
+        tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < P2; ++q) {
+          const float4 w = W[(c * P2 + q) * H];
+          const int f = 2 * q;
+          a[f] = fmaf(w.x, gr[f], a[f]);
+          a[f] = fmaf(-w.y, gi[f], a[f]);
+          a[16 + f] = fmaf(w.x, gi[f], a[16 + f]);
+          a[16 + f] = fmaf(w.y, gr[f], a[16 + f]);
+          if (f + 1 < P) {
+            a[f + 1] = fmaf(w.z, gr[f + 1], a[f + 1]);
+            a[f + 1] = fmaf(-w.w, gi[f + 1], a[f + 1]);
+            a[17 + f] = fmaf(w.z, gi[f + 1], a[17 + f]);
+            a[17 + f] = fmaf(w.w, gr[f + 1], a[17 + f]);
+          }
+        }
+        tm_st32(tacc + 32 * c, a);
+      }
+    }
+  };
   auto accum = [&](int s, const float (&gr)[P], const float (&gi)[P]) {
     const float4* W = Wring + s * w4s + f1;
 #pragma unroll
@@ -173,6 +222,21 @@ __global__ void __launch_bounds__(256, 1) oaa_bwdd_kernel(const BwdDParams p) {
   // two dy channels per step: their block transforms are independent (ILP); the
   // prefetch distance is S − 2 so the two refilled stages are the ones just consumed
   int k = 0;
+  if constexpr (TM) {
+    // one channel per step (register budget); the ring prefetch distance stays S − 2
+    for (; k < p.K; ++k) {
+      const int s0 = k % S;
+      stage_dy(k + S - 2);
+      asm volatile("cp.async.wait_group %0;" ::"n"(S - 2) : "memory");
+      __syncwarp();
+      mbar_wait(&full[s0], (k / S) & 1);
+      float gr[P], gi[P];
+      block_row_spectrum_smem<NN>(mydy + s0 * DYS, CW, (laneA ? tt : 0) * NN, cf, sf, gr, gi);
+      accum_tm(s0, gr, gi);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s0]);
+    }
+  }
   for (; k + 1 < p.K; k += 2) {
     const int s0 = k % S, s1 = (k + 1) % S;
     stage_dy(k + S - 2);
@@ -218,9 +282,22 @@ __global__ void __launch_bounds__(256, 1) oaa_bwdd_kernel(const BwdDParams p) {
   for (int c = 0; c < CR; ++c) {
     if (c >= p.C) break;
     asm volatile("bar.sync 1, %0;" ::"r"(nthr_c) : "memory");  // Q free
+    float er[P], ei[P];
+    if constexpr (TM) {
+      float a[32];
+      __syncwarp();
+      tmem_wait_st();
+      tm_ld32(tacc + 32 * c, a);
+      tmem_wait_ld();
+#pragma unroll
+      for (int f = 0; f < P; ++f) { er[f] = a[f]; ei[f] = a[16 + f]; }
+    } else {
+#pragma unroll
+      for (int f = 0; f < P; ++f) { er[f] = ar[c][f]; ei[f] = ai[c][f]; }
+    }
     if (laneA) {
       float qr[P], qi[P];
-      dft<P, +1>(ar[c], ai[c], qr, qi);
+      dft<P, +1>(er, ei, qr, qi);
       float2* qd = Q + t2 * QT + f1 * P;
       const bool real_tile = t2 < p.Td;
 #pragma unroll
@@ -249,6 +326,11 @@ __global__ void __launch_bounds__(256, 1) oaa_bwdd_kernel(const BwdDParams p) {
         if (r >= 0 && r < p.N) atomicAdd(dxc + (size_t)r * p.N + j, y[p1]);
       }
     }
+  }
+  if constexpr (TM) {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr_c) : "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(s_tmem));
   }
 }
 

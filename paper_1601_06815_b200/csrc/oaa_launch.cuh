@@ -160,8 +160,11 @@ cudaError_t launch_walk_n(const oaa::XSpecParams& xp, const oaa::WalkParams& wp,
 
 template <int NN>
 cudaError_t launch_bwdd_n(const oaa::BwdDParams& p, int cr, size_t smem, cudaStream_t s) {
-  auto k = cr <= 1 ? oaa::oaa_bwdd_kernel<NN, 1> : cr == 2 ? oaa::oaa_bwdd_kernel<NN, 2>
-         : cr == 3 ? oaa::oaa_bwdd_kernel<NN, 3> : oaa::oaa_bwdd_kernel<NN, 4>;
+  const bool tm = std::getenv("OAA_BWDD_REG") == nullptr && smem <= 110 * 1024;
+  auto k = tm ? (cr <= 1 ? oaa::oaa_bwdd_kernel<NN, 1, true> : cr == 2 ? oaa::oaa_bwdd_kernel<NN, 2, true>
+                 : cr == 3 ? oaa::oaa_bwdd_kernel<NN, 3, true> : oaa::oaa_bwdd_kernel<NN, 4, true>)
+              : (cr <= 1 ? oaa::oaa_bwdd_kernel<NN, 1, false> : cr == 2 ? oaa::oaa_bwdd_kernel<NN, 2, false>
+                 : cr == 3 ? oaa::oaa_bwdd_kernel<NN, 3, false> : oaa::oaa_bwdd_kernel<NN, 4, false>);
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   k<<<p.B * p.Td, 32 * (p.NCW + 1), smem, s>>>(p);
