@@ -553,8 +553,8 @@ oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* 
   wp.KG = std::min(8, Cout);
   wp.ngrp = cdiv(Cout, wp.KG);
   wp.D = D;
-  const int QSZ = (2 * TPW + 1) * n * g.P;
-  const size_t walk_smem = sizeof(float2) * (size_t)wp.KG * QSZ + sizeof(float) * (size_t)wp.KG * (n - 1) * wp.NCH * CW;
+  const int QSZ = ((2 * TPW + 1) * n * g.P + 1) & ~1;
+  const size_t walk_smem = sizeof(float2) * (size_t)wp.KG * QSZ + sizeof(float) * (size_t)wp.KG * oaa::walk_trp(n) * wp.NCH * CW;
   (void)flags;
   (void)counter;
   ProfScope prof(is_fwd ? OAA_OP_FWD : OAA_OP_BWD_DATA, s);
@@ -677,9 +677,9 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
     wpl.NCH = wk.NCH;
     wpl.SW = xp.SW;
     wpl.xspec_smem = sizeof(float) * (size_t)Cin * n * xp.SW;
-    const int QSZ = (2 * wk.TPW + 1) * n * g.P;
+    const int QSZ = ((2 * wk.TPW + 1) * n * g.P + 1) & ~1;
     wpl.walk_smem = sizeof(float4) * (size_t)oaa::kWalkRing * Cin * wk.CH4 + sizeof(float2) * (size_t)wk.KG * QSZ +
-                    sizeof(float) * (size_t)wk.KG * (n - 1) * wk.NCH * wk.CW;
+                    sizeof(float) * (size_t)wk.KG * oaa::walk_trp(n) * wk.NCH * wk.CW;
     if (wpl.walk_smem > 220 * 1024 || wpl.xspec_smem > 220 * 1024) return OAA_ERR_UNSUPPORTED;
     ProfScope prof(OAA_OP_FWD, s);
     prof.start();

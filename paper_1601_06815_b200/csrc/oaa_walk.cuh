@@ -42,7 +42,7 @@ struct WalkGeo {
   static constexpr int CH4 = TPW * H * RS4;              // float4 per channel in a chunk
   static constexpr int QT = H * P;                       // float2 per tile in Q
   static constexpr int QS = 2 * TPW;                     // Q ring slots (tiles)
-  static constexpr int QSZ = (QS + 1) * QT;              // + one always-zero tile
+  static constexpr int QSZ = ((QS + 1) * QT + 1) & ~1;   // + one always-zero tile; even (16-byte multiple)
 };
 
 // Chunked spectrum layout (X̂ for fwd, Ξ̂ for bwd_filter): S[b][t1][i][c][lane][RS4]
@@ -180,7 +180,10 @@ constexpr int kWalkRing = 4;  // spectrum chunk slots per CTA
 
 // grid = B·ngrp CTAs (image-major: the groups of one image run side by side and share
 // its spectra through L2), KG warps each.
-// Shared memory: ring[kWalkRing][Cin·CH4] float4 | Q[KG][QSZ] float2 | carry[KG][n−1][NCH·CW].
+// Shared memory: ring[kWalkRing][Cin·CH4] float4 | Q[KG][QSZ] float2 |
+// carry[KG][TRP/4][NCH·CW][4] floats (TRP = n−1 rounded up to 4: a column's carry rows are
+// two float4, consecutive lanes' float4 contiguous).
+__host__ __device__ constexpr int walk_trp(int n) { return ((n - 1) + 3) & ~3; }
 template <int NN, int CR, bool LOAD = false>
 __global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
   using G = WalkGeo<NN>;
@@ -198,7 +201,8 @@ __global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
   float2* Qall = reinterpret_cast<float2*>(ring + kWalkRing * slot4);
   float2* Q = Qall + warp * G::QSZ;
   const int CWT = p.NCH * CW;  // carry row length
-  float* carry = reinterpret_cast<float*>(Qall + nw * G::QSZ) + warp * TR * CWT;
+  constexpr int TRP = walk_trp(NN), TQ = TRP / 4;
+  float* carry = reinterpret_cast<float*>(Qall + nw * G::QSZ) + warp * TRP * CWT;
   const int nseq = p.T * p.NCH;
   const float4* src = LOAD ? nullptr : p.S + (size_t)b * nseq * slot4;
   const uint32_t slot_bytes = (uint32_t)slot4 * 16u;
@@ -212,7 +216,7 @@ __global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
   }
   // zero tile of Q and the carry rows
   for (int e = lane; e < QT; e += 32) Q[G::QS * QT + e] = make_float2(0.f, 0.f);
-  for (int e = lane; e < TR * CWT; e += 32) carry[e] = 0.f;
+  for (int e = lane; e < TRP * CWT; e += 32) carry[e] = 0.f;
   __syncthreads();
   if (!LOAD && tid == 0) {
     for (int s = 0; s < kWalkRing && s < nseq; ++s) {
@@ -331,10 +335,9 @@ __global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
       __syncwarp();
       if (!LOAD && lane == 0) {
         __threadfence_block();
-        int old;
-        asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(&rel[s])) : "memory");
+        int old;  // inc wraps to 0 after the nw-th arrival: no reset store needed
+        asm volatile("atom.shared.inc.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(&rel[s])), "r"(nw - 1) : "memory");
         if (old == nw - 1) {
-          rel[s] = 0;
           __threadfence_block();
           const int nx = seq + kWalkRing;
           if (nx < nseq) {
@@ -361,29 +364,42 @@ __global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
         c2r_half<P>(zr, zi, y);
         const int J = i * CW + lane;
         const int j = J - p.off;
-        float* cr = carry + J;
+        float4* cr = reinterpret_cast<float4*>(carry) + J;
+        float cv[TQ > 0 ? 4 * TQ : 4];
+#pragma unroll
+        for (int q = 0; q < TQ; ++q) {
+          const float4 t = cr[q * CWT];
+          cv[4 * q] = t.x; cv[4 * q + 1] = t.y; cv[4 * q + 2] = t.z; cv[4 * q + 3] = t.w;
+        }
         const bool colok = j >= 0 && j < p.Ro;
-        float* op = outp + (ptrdiff_t)r0 * p.Ro + j;
         if (rows_full) {
           if (colok) {
+            char* op = reinterpret_cast<char*>(outp + ((ptrdiff_t)r0 * p.Ro + j));
+            const ptrdiff_t rb = (ptrdiff_t)p.Ro * (ptrdiff_t)sizeof(float);
 #pragma unroll
             for (int p1 = 0; p1 < NN; ++p1) {
               float v = y[p1];
-              if (p1 < TR) v += cr[p1 * CWT];
-              __stcs(op, v);
-              op += p.Ro;
+              if (p1 < TR) v += cv[p1];
+              __stcs(reinterpret_cast<float*>(op), v);
+              op += rb;
             }
           }
         } else {
+          float* op = outp + (ptrdiff_t)r0 * p.Ro + j;
 #pragma unroll
           for (int p1 = 0; p1 < NN; ++p1) {
             float v = y[p1];
-            if (p1 < TR) v += cr[p1 * CWT];
+            if (p1 < TR) v += cv[p1];
             if (colok && ((rowmask >> p1) & 1u)) __stcs(op + (ptrdiff_t)p1 * p.Ro, v);
           }
         }
 #pragma unroll
-        for (int p1 = NN; p1 < P; ++p1) cr[(p1 - NN) * CWT] = y[p1];
+        for (int q = 0; q < TQ; ++q) {
+          float t[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) t[r] = (4 * q + r < TR) ? y[NN + 4 * q + r] : 0.f;
+          cr[q * CWT] = make_float4(t[0], t[1], t[2], t[3]);
+        }
       }
       __syncwarp();
     }
@@ -397,7 +413,7 @@ __global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
 #pragma unroll
       for (int p1 = 0; p1 < TR; ++p1) {
         const int r = r0 + p1;
-        if (r >= 0 && r < p.Ro) __stcs(outp + (ptrdiff_t)r * p.Ro + j, carry[p1 * CWT + J]);
+        if (r >= 0 && r < p.Ro) __stcs(outp + (ptrdiff_t)r * p.Ro + j, carry[((p1 >> 2) * CWT + J) * 4 + (p1 & 3)]);
       }
     }
   }
