@@ -37,13 +37,21 @@ struct BwdDParams {
   int NCW;                     // compute warps (chunks of the tile row)
 };
 
-constexpr int kBwddStages = 8;  // ring depth (covers HBM latency)
+constexpr int kBwddStages = 8;    // per-warp dy ring depth (covers HBM latency)
+constexpr int kBwddWStages = 16;  // shared Ŵ ring depth: how far the fastest warp may run ahead
 
 // float4 per Ŵ ring stage ([C][n][n], padded to 128 B)
 __host__ __device__ constexpr int bwdd_w4_stride(int n, int C) { return (C * n * n + 7) & ~7; }
+__host__ __device__ constexpr size_t bwdd_dy_bytes(int n, int NCW) {
+  return (size_t)NCW * kBwddStages * n * ((32 / n) * n) * 4;
+}
+__host__ __device__ constexpr size_t bwdd_q_bytes(int n, int NCW) {
+  return (size_t)(NCW * (32 / n) + 1) * n * (2 * n - 1) * 8;
+}
+// the epilogue's Q buffer reuses the dy ring (the k loop is over by then)
 __host__ __device__ constexpr size_t bwdd_smem_bytes(int n, int C, int NCW) {
-  return (size_t)kBwddStages * bwdd_w4_stride(n, C) * 16 + (size_t)NCW * kBwddStages * n * ((32 / n) * n) * 4 +
-         (size_t)(NCW * (32 / n) + 1) * n * (2 * n - 1) * 8;
+  return (size_t)kBwddWStages * bwdd_w4_stride(n, C) * 16 +
+         (bwdd_dy_bytes(n, NCW) > bwdd_q_bytes(n, NCW) ? bwdd_dy_bytes(n, NCW) : bwdd_q_bytes(n, NCW));
 }
 
 __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
@@ -59,10 +67,10 @@ template <int NN, int CR, bool TM = false>
 __global__ void __launch_bounds__(256, TM ? 2 : 1) oaa_bwdd_kernel(const BwdDParams p) {
   using G = WalkGeo<NN>;
   constexpr int P = G::P, H = G::H, P2 = G::P2, TPW = G::TPW, QT = G::QT, CW = G::CW;
-  constexpr int S = kBwddStages;
+  constexpr int S = kBwddStages, SW = kBwddWStages;
   constexpr int DYS = NN * CW;                // floats per warp stage
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ uint64_t full[S], empty[S];
+  __shared__ uint64_t full[SW], empty[SW];
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NCW = p.NCW;
@@ -71,18 +79,17 @@ __global__ void __launch_bounds__(256, TM ? 2 : 1) oaa_bwdd_kernel(const BwdDPar
   const int w4 = p.C * P2 * H;                // float4 of kernel spectra per stage
   const int w4s = bwdd_w4_stride(NN, p.C);    // float4 per stage (padded)
   float4* Wring = reinterpret_cast<float4*>(smem_raw);
-  float* dyring = reinterpret_cast<float*>(Wring + S * w4s);
-  float2* Q = reinterpret_cast<float2*>(dyring + (size_t)NCW * S * DYS);
+  float* dyring = reinterpret_cast<float*>(Wring + SW * w4s);
+  float2* Q = reinterpret_cast<float2*>(dyring);  // epilogue only (aliases the dy ring)
   const int ntile_q = NCW * TPW;  // tiles held in Q; tile ntile_q is the zero tile
 
   if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
+    for (int s = 0; s < SW; ++s) {
       mbar_init(&full[s], 32);
       mbar_init(&empty[s], NCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int e = tid; e < QT; e += blockDim.x) Q[ntile_q * QT + e] = make_float2(0.f, 0.f);
   if (TM && warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&s_tmem)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -94,10 +101,10 @@ __global__ void __launch_bounds__(256, TM ? 2 : 1) oaa_bwdd_kernel(const BwdDPar
   const uint32_t tacc = TM ? s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * 128u : 0u;
 
   if (warp == NCW) {
-    // ---------------- producer: kernel spectra of channel k into stage k % S
+    // ---------------- producer: kernel spectra of channel k into stage k % SW
     for (int k = 0; k < p.K; ++k) {
-      const int s = k % S;
-      if (k >= S) mbar_wait(&empty[s], ((k / S) - 1) & 1);
+      const int s = k % SW;
+      if (k >= SW) mbar_wait(&empty[s], ((k / SW) - 1) & 1);
       float4* wd = Wring + s * w4s;
       const float4* ws = p.spec + (size_t)k * w4;
       for (int e = lane; e < w4; e += 32) cp_async16(wd + e, ws + e);
@@ -225,56 +232,59 @@ __global__ void __launch_bounds__(256, TM ? 2 : 1) oaa_bwdd_kernel(const BwdDPar
   if constexpr (TM) {
     // one channel per step (register budget); the ring prefetch distance stays S − 2
     for (; k < p.K; ++k) {
-      const int s0 = k % S;
+      const int s0 = k % S, w0 = k % SW;
       stage_dy(k + S - 2);
       asm volatile("cp.async.wait_group %0;" ::"n"(S - 2) : "memory");
       __syncwarp();
-      mbar_wait(&full[s0], (k / S) & 1);
+      mbar_wait(&full[w0], (k / SW) & 1);
       float gr[P], gi[P];
       block_row_spectrum_smem<NN>(mydy + s0 * DYS, CW, (laneA ? tt : 0) * NN, cf, sf, gr, gi);
-      accum_tm(s0, gr, gi);
+      accum_tm(w0, gr, gi);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s0]);
+      if (lane == 0) mbar_arrive(&empty[w0]);
     }
   }
   for (; k + 1 < p.K; k += 2) {
-    const int s0 = k % S, s1 = (k + 1) % S;
+    const int s0 = k % S, s1 = (k + 1) % S, w0 = k % SW, w1 = (k + 1) % SW;
     stage_dy(k + S - 2);
     stage_dy(k + S - 1);
     asm volatile("cp.async.wait_group %0;" ::"n"(S - 2) : "memory");  // groups k, k+1 landed
     __syncwarp();
-    mbar_wait(&full[s0], (k / S) & 1);
-    mbar_wait(&full[s1], ((k + 1) / S) & 1);
+    mbar_wait(&full[w0], (k / SW) & 1);
+    mbar_wait(&full[w1], ((k + 1) / SW) & 1);
     if (laneA) {
       float g0r[P], g0i[P], g1r[P], g1i[P];
       block_row_spectrum_smem<NN>(mydy + s0 * DYS, CW, tt * NN, cf, sf, g0r, g0i);
       block_row_spectrum_smem<NN>(mydy + s1 * DYS, CW, tt * NN, cf, sf, g1r, g1i);
-      accum(s0, g0r, g0i);
-      accum(s1, g1r, g1i);
+      accum(w0, g0r, g0i);
+      accum(w1, g1r, g1i);
     }
     __syncwarp();
     if (lane == 0) {
-      mbar_arrive(&empty[s0]);
-      mbar_arrive(&empty[s1]);
+      mbar_arrive(&empty[w0]);
+      mbar_arrive(&empty[w1]);
     }
   }
   if (k < p.K) {  // odd K: last channel
-    const int s0 = k % S;
+    const int s0 = k % S, w0 = k % SW;
     cp_async_wait_all();
     __syncwarp();
-    mbar_wait(&full[s0], (k / S) & 1);
+    mbar_wait(&full[w0], (k / SW) & 1);
     if (laneA) {
       float gr[P], gi[P];
       block_row_spectrum_smem<NN>(mydy + s0 * DYS, CW, tt * NN, cf, sf, gr, gi);
-      accum(s0, gr, gi);
+      accum(w0, gr, gi);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s0]);
+    if (lane == 0) mbar_arrive(&empty[w0]);
   }
   cp_async_wait_all();
 
   // ---------------- epilogue: per output channel, inverse DFT + overlap-add into dx
   const int nthr_c = 32 * NCW;
+  // Q reuses the dy ring: every compute warp is past its last dy stage first
+  asm volatile("bar.sync 1, %0;" ::"r"(nthr_c) : "memory");
+  for (int e = tid; e < QT; e += nthr_c) Q[ntile_q * QT + e] = make_float2(0.f, 0.f);
   const int FW = p.Td * NN + NN - 1;  // full-frame width
   const size_t planeN = (size_t)p.N * p.N;
   const int I0 = t1 * NN - p.off;     // dx row of block row 0
