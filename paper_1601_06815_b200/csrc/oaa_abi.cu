@@ -347,7 +347,7 @@ BwddPlan plan_bwdd(bool is_fwd, int Cout, int R, int n, const TcPlan& tc) {
   const int H = n, P = 2 * n - 1, TPW = 32 / H, CW = TPW * n;
   const int Td = cdiv(R, n);
   d.NCW = cdiv(Td, TPW);
-  if (d.NCW > 7) d.use = false;  // 7 compute warps + the producer (256 threads, ≤ 255 registers)
+  if (d.NCW > 8) d.use = false;  // ≤ 8 warps (256 threads)
   d.BW = d.NCW * CW;
   d.smem = oaa::bwdd_smem_bytes(n, Cout, d.NCW);
   if (d.smem > 220 * 1024) d.use = false;

@@ -3,12 +3,11 @@
 // evaluated by OaA over the n×n blocks of dy.
 //
 // One CTA per (image b, dy tile row t1).  Compute warp i owns chunk i of the tile row:
-// lanes (tt, f1) hold block t2 = i·TPW + tt, spectrum row f1.  A producer warp streams,
-// for every dy channel k in turn, the n dy rows of the tile row (cp.async, zero padded)
-// and the k-th slice of the flipped-kernel spectra into a ring of shared-memory stages
-// tracked by mbarriers (full: cp.async completion of the producer's 32 lanes; empty: one
-// arrival per compute warp), so compute warps never meet at a CTA barrier inside the k
-// loop.  Per k a lane computes its block-row spectrum Ĝ_k[f1,:] (pruned column DFT +
+// lanes (tt, f1) hold block t2 = i·TPW + tt, spectrum row f1.  For every dy channel k in
+// turn each warp stages the n dy rows of its own columns (cp.async, zero padded, 8-deep
+// per-warp ring); the k-th slice of the flipped-kernel spectra comes from a 16-deep
+// shared ring of bulk copies that the last warp to release a stage refills, so warps never
+// meet at a CTA barrier inside the k loop.  Per k a lane computes its block-row spectrum Ĝ_k[f1,:] (pruned column DFT +
 // row codelet) and accumulates the C output spectra Ŷ_c += Ŵᶠ_{k,c}·Ĝ_k in registers.
 // Epilogue per output channel c: inverse DFT along f2 (stage A, lanes (tile, f1)) → Q in
 // shared memory → stage B (lanes = full-frame columns: the two block columns summed
@@ -40,17 +39,17 @@ struct BwdDParams {
 constexpr int kBwddStages = 8;    // per-warp dy ring depth (covers HBM latency)
 constexpr int kBwddWStages = 16;  // shared Ŵ ring depth: how far the fastest warp may run ahead
 
-// float4 per Ŵ ring stage ([C][n][n], padded to 128 B)
-__host__ __device__ constexpr int bwdd_w4_stride(int n, int C) { return (C * n * n + 7) & ~7; }
 __host__ __device__ constexpr size_t bwdd_dy_bytes(int n, int NCW) {
   return (size_t)NCW * kBwddStages * n * ((32 / n) * n) * 4;
 }
 __host__ __device__ constexpr size_t bwdd_q_bytes(int n, int NCW) {
   return (size_t)(NCW * (32 / n) + 1) * n * (2 * n - 1) * 8;
 }
-// the epilogue's Q buffer reuses the dy ring (the k loop is over by then)
+// bytes of one Ŵ ring stage ([C][n][n] float4, padded to 128 B)
+__host__ __device__ constexpr int bwdd_w_bytes(int n, int C) { return (C * n * n * 16 + 127) & ~127; }
+// Ŵ ring | dy ring (the epilogue's Q buffer reuses the dy ring: the k loop is over by then)
 __host__ __device__ constexpr size_t bwdd_smem_bytes(int n, int C, int NCW) {
-  return (size_t)kBwddWStages * bwdd_w4_stride(n, C) * 16 +
+  return (size_t)kBwddWStages * bwdd_w_bytes(n, C) +
          (bwdd_dy_bytes(n, NCW) > bwdd_q_bytes(n, NCW) ? bwdd_dy_bytes(n, NCW) : bwdd_q_bytes(n, NCW));
 }
 
@@ -58,9 +57,10 @@ __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Shared memory: Ŵ ring [kBwddStages][C][P2][H] float4 (filled by the producer warp) |
-// per-compute-warp dy ring [NCW][kBwddStages][n][CW] floats (each warp stages the n rows
-// of its own CW columns) | Q [(NCW·TPW + 1) tiles][H][P] float2 (last tile zero).
+// Shared memory: Ŵ ring [kBwddWStages][C][P2][H] float4 (bulk copies, refilled by the last
+// warp to release a stage) | per-warp dy ring [NCW][kBwddStages][n][CW] floats (each warp
+// stages the n rows of its own CW columns); the epilogue's Q [(NCW·TPW + 1) tiles][H][P]
+// float2 (last tile zero) reuses the dy ring.
 // TM = true: the C output spectra are accumulated in tensor memory (96 columns per warp)
 // instead of registers, so the kernel fits 128 registers and two CTAs share an SM.
 template <int NN, int CR, bool TM = false>
@@ -70,26 +70,31 @@ __global__ void __launch_bounds__(256, TM ? 2 : 1) oaa_bwdd_kernel(const BwdDPar
   constexpr int S = kBwddStages, SW = kBwddWStages;
   constexpr int DYS = NN * CW;                // floats per warp stage
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ uint64_t full[SW], empty[SW];
+  __shared__ uint64_t wfull[SW];
+  __shared__ int wrel[SW];
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NCW = p.NCW;
   const int item = blockIdx.x;
   const int b = item / p.Td, t1 = item - (item / p.Td) * p.Td;
-  const int w4 = p.C * P2 * H;                // float4 of kernel spectra per stage
-  const int w4s = bwdd_w4_stride(NN, p.C);    // float4 per stage (padded)
-  float4* Wring = reinterpret_cast<float4*>(smem_raw);
-  float* dyring = reinterpret_cast<float*>(Wring + SW * w4s);
-  float2* Q = reinterpret_cast<float2*>(dyring);  // epilogue only (aliases the dy ring)
-  const int ntile_q = NCW * TPW;  // tiles held in Q; tile ntile_q is the zero tile
-
+  const int w4 = p.C * P2 * H;                // float4 of kernel spectra per dy channel
+  const int wst = bwdd_w_bytes(NN, p.C);      // bytes per Ŵ stage
+  unsigned char* Wring = smem_raw;
+  float* dyring = reinterpret_cast<float*>(smem_raw + (size_t)SW * wst);
+  const uint32_t wbytes = (uint32_t)w4 * 16u;
+  // Ŵ ring: stage k % SW holds the kernel spectra of dy channel k, brought in by a bulk
+  // copy (TMA engine) whose completion is counted on wfull; the last warp to release a
+  // stage issues the copy that refills it, so no warp ever waits for another to issue.
   if (tid == 0) {
     for (int s = 0; s < SW; ++s) {
-      mbar_init(&full[s], 32);
-      mbar_init(&empty[s], NCW);
+      mbar_init(&wfull[s], 1);
+      wrel[s] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  float2* Q = reinterpret_cast<float2*>(dyring);  // epilogue only (aliases the dy ring)
+  const int ntile_q = NCW * TPW;  // tiles held in Q; tile ntile_q is the zero tile
+
   if (TM && warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&s_tmem)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -97,22 +102,33 @@ __global__ void __launch_bounds__(256, TM ? 2 : 1) oaa_bwdd_kernel(const BwdDPar
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (tid == 0) {
+    for (int k = 0; k < SW && k < p.K; ++k) {
+      mbar_expect_tx(&wfull[k], wbytes);
+      bulk_g2s(Wring + (size_t)k * wst, p.spec + (size_t)k * w4, wbytes, &wfull[k]);
+    }
+  }
+  // a CTA of 7 chunks is launched with one extra, idle warp (both CTAs of an SM then put
+  // exactly two warps on each SMSP)
+  if (warp >= NCW) return;
+  auto w_wait = [&](int k) { mbar_wait(&wfull[k % SW], (k / SW) & 1); };
+  auto w_release = [&](int k) {  // after __syncwarp: this warp is done with stage k % SW
+    if (lane == 0) {
+      // no membar here: it would also wait for this lane's in-flight dy cp.asyncs.  The
+      // warp's reads of the stage are complete (their values were consumed before the
+      // __syncwarp), and the atomic orders the warps' releases.
+      const int s = k % SW;
+      int old;
+      asm volatile("atom.shared.inc.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(&wrel[s])), "r"(NCW - 1) : "memory");
+      if (old == NCW - 1 && k + SW < p.K) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&wfull[s], wbytes);
+        bulk_g2s(Wring + (size_t)s * wst, p.spec + (size_t)(k + SW) * w4, wbytes, &wfull[s]);
+      }
+    }
+  };
   // compute warp w: TMEM lanes 32·(w mod 4).., columns 128·(w / 4) + 32·c
   const uint32_t tacc = TM ? s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * 128u : 0u;
-
-  if (warp == NCW) {
-    // ---------------- producer: kernel spectra of channel k into stage k % SW
-    for (int k = 0; k < p.K; ++k) {
-      const int s = k % SW;
-      if (k >= SW) mbar_wait(&empty[s], ((k / SW) - 1) & 1);
-      float4* wd = Wring + s * w4s;
-      const float4* ws = p.spec + (size_t)k * w4;
-      for (int e = lane; e < w4; e += 32) cp_async16(wd + e, ws + e);
-      cp_async_mbar_arrive_noinc(&full[s]);
-    }
-    cp_async_wait_all();
-    return;
-  }
 
   // ---------------- compute warps: each stages its own columns of the n dy rows
   const size_t planeM = (size_t)p.M * p.M;
@@ -174,8 +190,8 @@ __global__ void __launch_bounds__(256, TM ? 2 : 1) oaa_bwdd_kernel(const BwdDPar
   }
 
   // TM: acc[c] row in TMEM (re at columns f, im at 16 + f) += Ŵᶠ·Ĝ; warp-collective
-  auto accum_tm = [&](int s, const float (&gr)[P], const float (&gi)[P]) {
-    const float4* W = Wring + s * w4s + f1;
+  auto accum_tm = [&](int k, const float (&gr)[P], const float (&gi)[P]) {
+    const float4* W = reinterpret_cast<const float4*>(Wring + (size_t)(k % SW) * wst) + f1;
     __syncwarp();
     tmem_wait_st();
 #pragma unroll
@@ -203,8 +219,8 @@ __global__ void __launch_bounds__(256, TM ? 2 : 1) oaa_bwdd_kernel(const BwdDPar
       }
     }
   };
-  auto accum = [&](int s, const float (&gr)[P], const float (&gi)[P]) {
-    const float4* W = Wring + s * w4s + f1;
+  auto accum = [&](int k, const float (&gr)[P], const float (&gi)[P]) {
+    const float4* W = reinterpret_cast<const float4*>(Wring + (size_t)(k % SW) * wst) + f1;
 #pragma unroll
     for (int c = 0; c < CR; ++c) {
       if (c < p.C) {
@@ -232,51 +248,49 @@ __global__ void __launch_bounds__(256, TM ? 2 : 1) oaa_bwdd_kernel(const BwdDPar
   if constexpr (TM) {
     // one channel per step (register budget); the ring prefetch distance stays S − 2
     for (; k < p.K; ++k) {
-      const int s0 = k % S, w0 = k % SW;
+      const int s0 = k % S;
       stage_dy(k + S - 2);
       asm volatile("cp.async.wait_group %0;" ::"n"(S - 2) : "memory");
       __syncwarp();
-      mbar_wait(&full[w0], (k / SW) & 1);
+      w_wait(k);
       float gr[P], gi[P];
       block_row_spectrum_smem<NN>(mydy + s0 * DYS, CW, (laneA ? tt : 0) * NN, cf, sf, gr, gi);
-      accum_tm(w0, gr, gi);
+      accum_tm(k, gr, gi);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[w0]);
+      w_release(k);
     }
   }
   for (; k + 1 < p.K; k += 2) {
-    const int s0 = k % S, s1 = (k + 1) % S, w0 = k % SW, w1 = (k + 1) % SW;
+    const int s0 = k % S, s1 = (k + 1) % S;
     stage_dy(k + S - 2);
     stage_dy(k + S - 1);
     asm volatile("cp.async.wait_group %0;" ::"n"(S - 2) : "memory");  // groups k, k+1 landed
     __syncwarp();
-    mbar_wait(&full[w0], (k / SW) & 1);
-    mbar_wait(&full[w1], ((k + 1) / SW) & 1);
+    w_wait(k);
+    w_wait(k + 1);
     if (laneA) {
       float g0r[P], g0i[P], g1r[P], g1i[P];
       block_row_spectrum_smem<NN>(mydy + s0 * DYS, CW, tt * NN, cf, sf, g0r, g0i);
       block_row_spectrum_smem<NN>(mydy + s1 * DYS, CW, tt * NN, cf, sf, g1r, g1i);
-      accum(w0, g0r, g0i);
-      accum(w1, g1r, g1i);
+      accum(k, g0r, g0i);
+      accum(k + 1, g1r, g1i);
     }
     __syncwarp();
-    if (lane == 0) {
-      mbar_arrive(&empty[w0]);
-      mbar_arrive(&empty[w1]);
-    }
+    w_release(k);
+    w_release(k + 1);
   }
   if (k < p.K) {  // odd K: last channel
-    const int s0 = k % S, w0 = k % SW;
+    const int s0 = k % S;
     cp_async_wait_all();
     __syncwarp();
-    mbar_wait(&full[w0], (k / SW) & 1);
+    w_wait(k);
     if (laneA) {
       float gr[P], gi[P];
       block_row_spectrum_smem<NN>(mydy + s0 * DYS, CW, tt * NN, cf, sf, gr, gi);
-      accum(w0, gr, gi);
+      accum(k, gr, gi);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[w0]);
+    w_release(k);
   }
   cp_async_wait_all();
 

@@ -261,12 +261,11 @@ __global__ void __launch_bounds__(32 * kBwdfWarps, BwdfCfg<TM>::minb) oaa_bwdf_k
     // release the Ξ̂ slot; the last warp out refills it
     __syncwarp();
     if (lane == 0) {
-      __threadfence_block();
-      int old;
-      asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(&rel[s])) : "memory");
+      // (no membar: it would also wait for this lane's in-flight dy cp.asyncs; the warp's
+      // reads of the slot are complete and the atomic orders the releases)
+      int old;  // inc wraps to 0 after the nw-th arrival
+      asm volatile("atom.shared.inc.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(&rel[s])), "r"(nw - 1) : "memory");
       if (old == nw - 1) {
-        rel[s] = 0;
-        __threadfence_block();
         const int nx = sq + kBwdfRing;
         if (nx < nseq) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

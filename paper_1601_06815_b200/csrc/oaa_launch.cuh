@@ -167,7 +167,7 @@ cudaError_t launch_bwdd_n(const oaa::BwdDParams& p, int cr, size_t smem, cudaStr
                  : cr == 3 ? oaa::oaa_bwdd_kernel<NN, 3, false> : oaa::oaa_bwdd_kernel<NN, 4, false>);
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  k<<<p.B * p.Td, 32 * (p.NCW + 1), smem, s>>>(p);
+  k<<<p.B * p.Td, 32 * (p.NCW == 7 ? 8 : p.NCW), smem, s>>>(p);
   g_launches++;
   return cudaGetLastError();
 }
