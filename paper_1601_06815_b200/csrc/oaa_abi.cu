@@ -357,7 +357,7 @@ BwddPlan plan_bwdd(bool is_fwd, int Cout, int R, int n, const TcPlan& tc) {
 // bwd_filter for few input channels (oaa_bwdf.cuh) ------------------------------------
 struct BwdfPlan {
   bool use;
-  int TPW, CW, CH4, NCH, Td, KPW, nkg, G, SW;
+  int TPW, CW, CH4, NCH, Td, KPW, nkg, nwb, KG, G, SW;
   bool tm;
   size_t xs_b, part_b, xspec_smem, smem;
 };
@@ -372,6 +372,9 @@ BwdfPlan plan_bwdf(int B, int C, int K, int M, int n) {
   f.NCH = cdiv(f.Td, f.TPW);
   f.KPW = 32 / H;
   f.nkg = cdiv(K, oaa::kBwdfWarps * f.KPW);
+  // balanced kernel groups: each CTA takes ⌈K / nkg⌉ kernels rounded up to whole warps
+  f.nwb = cdiv(cdiv(K, f.nkg), f.KPW);
+  f.KG = f.nwb * f.KPW;
   f.tm = std::getenv("OAA_BWDF_REG") == nullptr;  // TMEM accumulators, 2 CTAs / SM
   f.G = std::max(1, std::min(B * f.Td, (f.tm ? 296 : 148) / f.nkg));
   f.SW = cdiv(f.NCH * f.CW + n - 1, 4) * 4;
@@ -874,6 +877,7 @@ oaa_status_t oaa_conv_bwd_filter(const float* x, const float* dy, float* dw, int
     fp.Td = bf.Td;
     fp.NCH = bf.NCH;
     fp.G = bf.G;
+    fp.KG = bf.KG;
     ProfScope prof(OAA_OP_BWD_FILTER, s);
     prof.start();
     cudaError_t err = launch_bwdf(n, xp, fp, BwdfLaunch{bf.xspec_smem, bf.smem, bf.nkg, bf.tm}, s);

@@ -31,6 +31,7 @@ struct BwdFParams {
   const float4* XS;   // Ξ̂ chunks [B·Td][NCH][C][32][RS4]
   float2* partial;    // [G][K][C][P][H]
   int B, K, C, M, Td, NCH, G;
+  int KG;             // kernels per CTA (a multiple of ⌊32/n⌋; blockDim = 32·KG/⌊32/n⌋)
 };
 
 constexpr int kBwdfWarps = 8;
@@ -61,7 +62,7 @@ __global__ void __launch_bounds__(32 * kBwdfWarps, BwdfCfg<TM>::minb) oaa_bwdf_k
   __shared__ int rel[kBwdfRing];
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int nw = kBwdfWarps;
+  const int nw = blockDim.x >> 5;  // ≤ kBwdfWarps: as many as the kernel group needs
   const int slot4 = p.C * G::CH4;
   float4* ring = reinterpret_cast<float4*>(smem_raw);
   float* dyr = reinterpret_cast<float*>(ring + kBwdfRing * slot4) + (size_t)warp * kBwdfDy * DYS;
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(32 * kBwdfWarps, BwdfCfg<TM>::minb) oaa_bwdf_k
   }
 
   const int ks = lane / H, f1 = lane - (lane / H) * H;
-  const int kbase = blockIdx.y * (nw * KPW) + warp * KPW;
+  const int kbase = blockIdx.y * p.KG + warp * KPW;
   const int k = kbase + ks;
   const bool laneK = ks < KPW && k < p.K;
   float cf[NN], sf[NN];

@@ -189,7 +189,7 @@ cudaError_t launch_bwdf_n(const oaa::XSpecParams& xp, const oaa::BwdFParams& p, 
                 : p.C == 3 ? oaa::oaa_bwdf_kernel<NN, 3, false> : oaa::oaa_bwdf_kernel<NN, 4, false>);
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  k<<<dim3(p.G, nkg), 32 * oaa::kBwdfWarps, smem, s>>>(p);
+  k<<<dim3(p.G, nkg), 32 * (p.KG / (32 / NN)), smem, s>>>(p);
   g_launches++;
   return cudaGetLastError();
 }
