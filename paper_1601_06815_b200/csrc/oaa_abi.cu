@@ -282,7 +282,7 @@ oaa_status_t validate(int B, int C, int K, int N, int n, oaa_crop_t crop, Geo* g
 // tensor-core path ----------------------------------------------
 // Layers with many input AND output channels evaluate the per-bin contraction as a
 // real-ified GEMM on the tensor cores (oaa_tc.cuh): tile spectra Xg → D = Ag·Xgᵀ → the
-// engine in LY mode inverts and overlap-adds.  Xg and D hold one batch chunk at a time.
+// walker (load mode) inverts and overlap-adds.  Xg and D hold one batch chunk at a time.
 constexpr int kTcMinChannels = 16;
 constexpr size_t kTcChunkBytes = size_t(1) << 31;  // Xg + D per chunk
 
@@ -498,7 +498,7 @@ cudaError_t launch_bin_gemm(const oaa::BinGemmParams& p, cudaStream_t s) {
 }
 
 // Tensor-core evaluation of fwd / bwd_data: per batch chunk, T1 (tile spectra) → bin
-// GEMM (3×TF32 tcgen05) → engine in LY mode (inverse DFT + overlap-add + crop).
+// GEMM (3×TF32 tcgen05) → walker in load mode (inverse DFT + overlap-add + crop).
 oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* out, int B, int C, int K, int n,
                            const Geo& g, const EnginePlan& e, const TcPlan& tc, const EngineWs& L, char* base,
                            cudaStream_t s) {

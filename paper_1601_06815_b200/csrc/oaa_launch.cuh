@@ -73,7 +73,7 @@ cudaError_t launch_engine_s1t_t(const oaa::EngineParams& p, const EnginePlan& e,
 
 template <int NN>
 cudaError_t launch_engine_n(const oaa::EngineParams& p, const EnginePlan& e, cudaStream_t s) {
-  if (e.LY) return launch_engine_s1t_t<NN, 1, true>(p, e, s);
+  if (e.LY) return cudaErrorInvalidValue;  // Ŷ from the bin GEMM goes through the walker (load mode)
   if (e.S1) {
     switch (e.CR) {
       case 1: return launch_engine_s1t_t<NN, 1, false>(p, e, s);

@@ -91,7 +91,7 @@ def test_channel_regimes(B, C, K, crop):
                                        (2, 16, 16, 9, 1), (1, 20, 18, 40, 7), (2, 33, 17, 23, 2)])
 def test_tensor_core_path(B, C, K, N, n, crop):
     """C ≥ 16 and K ≥ 16: fwd and bwd_data run tile spectra → tcgen05 bin GEMM (3×TF32)
-    → engine (LY mode); ragged 2C (K padding), ragged GEMM tiles, ragged spatial tails."""
+    → walker (load mode); ragged 2C (K padding), ragged GEMM tiles, ragged spatial tails."""
     if crop == "valid" and n > N:
         pytest.skip("Valid needs n <= N")
     d = make_inputs(B, C, K, N, n, crop, seed=B * 131 + C * 17 + K * 3 + n)
@@ -149,6 +149,27 @@ def test_deterministic_and_stream_ordered():
         y2 = oaa.conv_fwd(x, w); dx2 = oaa.conv_bwd_data(dy, w, c.N); dw2 = oaa.conv_bwd_filter(x, dy, c.n)
     s.synchronize()
     assert torch.equal(y1, y2) and torch.equal(dx1, dx2) and torch.equal(dw1, dw2)
+
+
+def test_concurrent_streams_match_sequential():
+    """The three ops on three streams at once (the bench step runs bwd_filter beside
+    bwd_data): every call gets its own workspace and the results are bitwise those of
+    the sequential calls -- including the red.add overlap-add of bwd_data, whose two
+    addends per element meet on an exact zero in either order."""
+    c = CONFIGS["headline"]
+    B = 6
+    d = make_inputs(B, c.C, c.K, c.N, c.n, "valid", seed=17)
+    x = torch.from_numpy(d["x"]).cuda(); w = torch.from_numpy(d["w"]).cuda()
+    dy = torch.from_numpy(d["dy"]).cuda()
+    y0 = oaa.conv_fwd(x, w); dx0 = oaa.conv_bwd_data(dy, w, c.N); dw0 = oaa.conv_bwd_filter(x, dy, c.n)
+    torch.cuda.synchronize()
+    s1, s2, s3 = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        y = oaa.conv_fwd(x, w, stream=s1)
+        dx = oaa.conv_bwd_data(dy, w, c.N, stream=s2)
+        dw = oaa.conv_bwd_filter(x, dy, c.n, stream=s3)
+        torch.cuda.synchronize()
+        assert torch.equal(y, y0) and torch.equal(dx, dx0) and torch.equal(dw, dw0)
 
 
 def test_outputs_fully_overwritten():
