@@ -66,7 +66,13 @@ __global__ void __launch_bounds__(256) oaa_xspec_kernel(const XSpecParams p) {
   constexpr int P = G::P, H = G::H, RS4 = G::RS4;
   constexpr int ROWS = WIN ? P : NN;
   extern __shared__ __align__(16) float rows_s[];  // [Cin][ROWS][SW]
+  __shared__ float2 tw_s[16];                        // (cos, sin)(2π m / P), m < P
   const int tid = threadIdx.x, nthr = blockDim.x;
+  if (tid < P) {
+    float sn, cs;
+    sincospif(2.0f * (float)tid / (float)P, &sn, &cs);
+    tw_s[tid] = make_float2(cs, sn);
+  }
   const int item = blockIdx.x;
   const int b = item / p.T, t1 = item - (item / p.T) * p.T;
   const float* in_b = p.in + (size_t)b * p.Cin * p.R * p.R;
@@ -91,17 +97,19 @@ __global__ void __launch_bounds__(256) oaa_xspec_kernel(const XSpecParams p) {
   }
   float4* out = p.S + (size_t)item * p.NCH * p.Cin * G::CH4;
   const int ntask = p.NCH * p.Cin * 32;
-  // WIN: a thread's lane (and so its spectrum row f1) is the same for all its tasks (nthr
-  // is a multiple of 32), so its P column twiddles are computed once
+  // a thread's lane (and so its spectrum row f1) is the same for all its tasks (nthr is a
+  // multiple of 32): its column twiddles e^{−2πi f1 p1 / P} come from the table once
   float tcx[WIN ? ROWS : 1], tsx[WIN ? ROWS : 1];
   if constexpr (WIN) {
     const int f1 = (tid & 31) % H;
+    int m = 0;
 #pragma unroll
     for (int p1 = 0; p1 < ROWS; ++p1) {
-      float s, co;
-      sincospif(2.0f * (float)((f1 * p1) % P) / (float)P, &s, &co);
-      tcx[p1] = co;
-      tsx[p1] = s;
+      const float2 t = tw_s[m];
+      tcx[p1] = t.x;
+      tsx[p1] = t.y;
+      m += f1;
+      if (m >= P) m -= P;
     }
   }
   for (int task = tid; task < ntask; task += nthr) {
@@ -113,6 +121,8 @@ __global__ void __launch_bounds__(256) oaa_xspec_kernel(const XSpecParams p) {
     const float* blk = rows_s + c * ROWS * p.SW;
     const int c0 = (i * G::TPW + tt) * NN;
     if constexpr (!WIN) {
+      // (pruned blocks: per-task sincospif measured faster than the hoisted table values,
+      // 0.143 vs 0.165 ms at the headline -- more registers live across the task loop)
       float cf[NN], sf[NN];
 #pragma unroll
       for (int p1 = 0; p1 < NN; ++p1) {
