@@ -1350,11 +1350,11 @@ __global__ void __launch_bounds__(128) oaa_tile_spectra_kernel(const TileSpecPar
       const int ch = sgm / NN, rr = sgm - (sgm / NN) * NN;
       const int r = t1 * NN + rr;
       const bool rok = r < p.R;
-      const float* src = in_b + ((size_t)(c0 + ch) * p.R + (rok ? r : 0)) * p.R;
+      const int roff = ((c0 + ch) * p.R + (rok ? r : 0)) * p.R;  // within the image (32-bit)
       float* d = band + ch * p.CSTR + rr * p.BW;
       for (int q = lane; q < p.BW; q += 32) {
         const bool ok = rok && q < p.R;
-        cp_async4(d + q, ok ? src + q : in_b, ok);
+        cp_async4(d + q, in_b + (ok ? roff + q : 0), ok);
       }
     }
     cp_async_commit();
@@ -1442,32 +1442,34 @@ __global__ void __launch_bounds__(256) oaa_filter_spectra_kernel(const FiltSpecP
     tcx[p1] = cs;
     tsx[p1] = sn;
   }
-  const size_t plane = (size_t)p.R * p.R;
+  const int plane = p.R * p.R;
   const int r0 = t1 * NN + p.org;
   const int q_lo = bt0 >> 1, q_hi = (bt0 + p.Td - 1) >> 1;
-  for (int c0 = 0; c0 < p.nch; c0 += CG) {
+  // one channel group of CG per CTA (blockIdx.y): items × groups CTAs keep every SM busy
+  {
+    const int c0 = blockIdx.y * CG;
+    if (c0 >= p.nch) return;
     const int ncg = min(CG, p.nch - c0);
-    __syncthreads();
     {
       const int lane = tid & 31, warp = tid >> 5;
-      const float* base = p.src + ((size_t)b * p.nch + c0) * plane;
+      const float* base = p.src + ((size_t)b * p.nch + c0) * plane;  // 32-bit offsets below
       for (int sg = warp; sg < ncg * ROWS; sg += 8) {
         const int ch = sg / ROWS, rr = sg - (sg / ROWS) * ROWS;
         const int r = r0 + rr;
         const bool rok = r >= 0 && r < p.R;
-        const float* srow = base + ch * plane + (size_t)(rok ? r : 0) * p.R;
+        const int roff = ch * plane + (rok ? r : 0) * p.R + p.org;
         float* d = band + (ch * ROWS + rr) * p.SW;
         for (int q = lane; q < p.SW; q += 32) {
           const int col = q + p.org;
           const bool ok = rok && col >= 0 && col < p.R;
-          cp_async4(d + q, ok ? srow + col : base, ok);
+          cp_async4(d + q, base + (ok ? roff + q : 0), ok);
         }
       }
       cp_async_commit();
       cp_async_wait_all();
       __syncthreads();
     }
-    if (kl >= ncg || tsub >= nsub) continue;
+    if (kl >= ncg || tsub >= nsub) return;
     const float* bsrc = band + kl * ROWS * p.SW;
     const int ch = c0 + kl;
     for (int q = q_lo + tsub; q <= q_hi; q += nsub) {
