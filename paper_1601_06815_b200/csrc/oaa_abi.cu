@@ -284,7 +284,7 @@ oaa_status_t validate(int B, int C, int K, int N, int n, oaa_crop_t crop, Geo* g
 // real-ified GEMM on the tensor cores (oaa_tc.cuh): tile spectra Xg → D = Ag·Xgᵀ → the
 // walker (load mode) inverts and overlap-adds.  Xg and D hold one batch chunk at a time.
 constexpr int kTcMinChannels = 16;
-constexpr size_t kTcChunkBytes = size_t(1) << 31;  // Xg + D per chunk
+constexpr size_t kTcChunkBytes = size_t(1) << 33;  // Xg + D per chunk (8 GB: launches large enough to fill the GPU)
 
 struct TcPlan {
   bool use;
