@@ -300,47 +300,47 @@ __global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
           for (int p2 = 0; p2 < P; ++p2) qd[p2] = make_float2(qr[p2], qi[p2]);
         }
       } else {
-       if (active && laneA) {
-        const float4* xs = ring + s * slot4 + lane * RS4;
-        float yr[P], yi[P];
+        if (active && laneA) {
+          const float4* xs = ring + s * slot4 + lane * RS4;
+          float yr[P], yi[P];
 #pragma unroll
-        for (int c = 0; c < CR; ++c) {
-          if (c < p.Cin) {
+          for (int c = 0; c < CR; ++c) {
+            if (c < p.Cin) {
 #pragma unroll
-            for (int q = 0; q < P2; ++q) {
-              const float4 x = xs[c * G::CH4 + q];
-              const float4 w = Wr[c][q];
-              const int f = 2 * q;
-              if (c == 0) {
-                yr[f] = w.x * x.x;
-                yi[f] = w.x * x.y;
-              } else {
-                yr[f] = fmaf(w.x, x.x, yr[f]);
-                yi[f] = fmaf(w.x, x.y, yi[f]);
-              }
-              yr[f] = fmaf(-w.y, x.y, yr[f]);
-              yi[f] = fmaf(w.y, x.x, yi[f]);
-              if (f + 1 < P) {
+              for (int q = 0; q < P2; ++q) {
+                const float4 x = xs[c * G::CH4 + q];
+                const float4 w = Wr[c][q];
+                const int f = 2 * q;
                 if (c == 0) {
-                  yr[f + 1] = w.z * x.z;
-                  yi[f + 1] = w.z * x.w;
+                  yr[f] = w.x * x.x;
+                  yi[f] = w.x * x.y;
                 } else {
-                  yr[f + 1] = fmaf(w.z, x.z, yr[f + 1]);
-                  yi[f + 1] = fmaf(w.z, x.w, yi[f + 1]);
+                  yr[f] = fmaf(w.x, x.x, yr[f]);
+                  yi[f] = fmaf(w.x, x.y, yi[f]);
                 }
-                yr[f + 1] = fmaf(-w.w, x.w, yr[f + 1]);
-                yi[f + 1] = fmaf(w.w, x.z, yi[f + 1]);
+                yr[f] = fmaf(-w.y, x.y, yr[f]);
+                yi[f] = fmaf(w.y, x.x, yi[f]);
+                if (f + 1 < P) {
+                  if (c == 0) {
+                    yr[f + 1] = w.z * x.z;
+                    yi[f + 1] = w.z * x.w;
+                  } else {
+                    yr[f + 1] = fmaf(w.z, x.z, yr[f + 1]);
+                    yi[f + 1] = fmaf(w.z, x.w, yi[f + 1]);
+                  }
+                  yr[f + 1] = fmaf(-w.w, x.w, yr[f + 1]);
+                  yi[f + 1] = fmaf(w.w, x.z, yi[f + 1]);
+                }
               }
             }
           }
-        }
-        float qr[P], qi[P];
-        dft<P, +1>(yr, yi, qr, qi);
-        float2* qd = Q + (half * TPW + tt) * QT + f1 * P;
+          float qr[P], qi[P];
+          dft<P, +1>(yr, yi, qr, qi);
+          float2* qd = Q + (half * TPW + tt) * QT + f1 * P;
 #pragma unroll
-        for (int p2 = 0; p2 < P; ++p2) qd[p2] = make_float2(qr[p2], qi[p2]);
+          for (int p2 = 0; p2 < P; ++p2) qd[p2] = make_float2(qr[p2], qi[p2]);
+        }
       }
-       }
       // release the ring slot; the last warp out refills it with chunk seq + kWalkRing
       __syncwarp();
       if (!LOAD && lane == 0) {
