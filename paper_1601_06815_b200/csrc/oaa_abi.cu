@@ -491,7 +491,12 @@ cudaError_t launch_bin_gemm(const oaa::BinGemmParams& p, cudaStream_t s) {
   cudaError_t err = cudaFuncSetAttribute(oaa::oaa_bin_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)oaa::kTcSmem);
   if (err != cudaSuccess) return err;
-  dim3 grid(cdiv(p.N, oaa::kTcM * p.NB), cdiv(p.M, oaa::kTcM), p.F * p.S);
+  // persistent: one CTA per SM (512 TMEM columns, 192 KB of stages), tiles strided over them
+  const long long ntiles = (long long)cdiv(p.N, oaa::kTcM * p.NB) * cdiv(p.M, oaa::kTcM) * p.F * p.S;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::max<long long>(1, std::min<long long>(ntiles, sms));
   oaa::oaa_bin_gemm_kernel<<<grid, oaa::kTcThreads, oaa::kTcSmem, s>>>(p);
   g_launches++;
   return cudaGetLastError();

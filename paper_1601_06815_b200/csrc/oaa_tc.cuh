@@ -34,7 +34,7 @@ namespace oaa {
 constexpr int kTcM = 128, kTcN = 256, kTcK = 32;  // CTA tile and K chunk (fp32 elements)
 constexpr int kTcStages = 2;
 constexpr size_t kTcStageBytes = (size_t)(2 * kTcM + 2 * kTcN) * kTcK * sizeof(float);  // 96 KB
-constexpr size_t kTcSmem = kTcStages * kTcStageBytes;
+constexpr size_t kTcSmem = kTcStages * kTcStageBytes + 8 * 32 * 33 * sizeof(float);  // + epilogue transpose buffers
 
 struct BinGemmParams {
   const float* A;  // blocked [F][Kc][2][RTA][4096]
@@ -111,18 +111,18 @@ constexpr int kTcThreads = 320;  // warp 0 TMA producer, warp 1 MMA issuer, warp
 // Two TMEM accumulators of 256 columns alternate per group of kTcDrain K chunks, so the
 // MMAs of group g+1 run while the epilogue warps drain group g.
 __global__ void __launch_bounds__(kTcThreads, 1) oaa_bin_gemm_kernel(const BinGemmParams p) {
+  // Persistent: CTA b takes output tiles b, b + gridDim.x, ...  (tile order: M tiles of one
+  // (bin, N tile) first, so their shared B operand is re-read from L2).  The smem stage ring
+  // and the two TMEM accumulators carry on across tiles: the drain warps write tile t while
+  // the MMAs of tile t+1 already run into the other accumulator.
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // stage s: [A_hi 16K][A_lo 16K][B_hi 32K][B_lo 32K]
   __shared__ uint64_t full[kTcStages], empty[kTcStages], accf[2], acce[2];
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int f = blockIdx.z / p.S, split = blockIdx.z - (blockIdx.z / p.S) * p.S;
-  const int kbeg = split * p.kps, nk = min(min(p.Kc, p.Kuse), kbeg + p.kps) - kbeg;
-  const int mt = blockIdx.y, nt = blockIdx.x;
   const int NB = p.NB, ntile = kTcM * NB;
-  const int m0 = mt * kTcM, n0 = nt * ntile;
-  const int mrows = min(kTcM, p.M - m0), ncols = min(ntile, p.N - n0);
-  const int nb = min(NB, p.RTB - NB * nt);  // B row tiles present
+  const int nN = (p.N + ntile - 1) / ntile, nM = (p.M + kTcM - 1) / kTcM;
+  const int ntiles = nN * nM * p.F * p.S;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -142,112 +142,148 @@ __global__ void __launch_bounds__(kTcThreads, 1) oaa_bin_gemm_kernel(const BinGe
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = s_tmem;
-  const int ngroups = (nk + kTcDrain - 1) / kTcDrain;
   constexpr uint32_t kBlk = 4096 * sizeof(float);
+  struct Tile {
+    int f, split, kbeg, nk, mt, nt, m0, n0, mrows, ncols, nb;
+  };
+  auto tile_of = [&](int t) {
+    Tile T;
+    const int fz = t / (nN * nM), rem = t - fz * (nN * nM);
+    T.nt = rem / nM;
+    T.mt = rem - T.nt * nM;
+    T.f = fz / p.S;
+    T.split = fz - T.f * p.S;
+    T.kbeg = T.split * p.kps;
+    T.nk = min(min(p.Kc, p.Kuse), T.kbeg + p.kps) - T.kbeg;
+    T.m0 = T.mt * kTcM;
+    T.n0 = T.nt * ntile;
+    T.mrows = min(kTcM, p.M - T.m0);
+    T.ncols = min(ntile, p.N - T.n0);
+    T.nb = min(NB, p.RTB - NB * T.nt);
+    return T;
+  };
+  auto groups_of = [](int nk) { return nk > 0 ? (nk + kTcDrain - 1) / kTcDrain : 0; };
   if (warp == 0) {
     if (lane == 0) {  // producer
-      for (int ch = 0; ch < nk; ++ch) {
-        const int s = ch % kTcStages;
-        if (ch >= kTcStages) mbar_wait(&empty[s], ((ch / kTcStages) - 1) & 1);
-        unsigned char* st = smem_raw + s * kTcStageBytes;
-        mbar_expect_tx(&full[s], 2 * kBlk + 2 * nb * kBlk);
-        const float* a = p.A + ((((size_t)f * p.Kc + kbeg + ch) * 2) * p.RTA + mt) * 4096;
-        const float* b = p.B + ((((size_t)f * p.Kc + kbeg + ch) * 2) * p.RTB + NB * nt) * 4096;
-        bulk_g2s(st, a, kBlk, &full[s]);
-        bulk_g2s(st + kBlk, a + (size_t)p.RTA * 4096, kBlk, &full[s]);
-        bulk_g2s(st + 2 * kBlk, b, nb * kBlk, &full[s]);
-        bulk_g2s(st + 4 * kBlk, b + (size_t)p.RTB * 4096, nb * kBlk, &full[s]);
+      int gch = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const Tile T = tile_of(t);
+        for (int ch = 0; ch < T.nk; ++ch, ++gch) {
+          const int s = gch % kTcStages;
+          if (gch >= kTcStages) mbar_wait(&empty[s], ((gch / kTcStages) - 1) & 1);
+          unsigned char* st = smem_raw + s * kTcStageBytes;
+          mbar_expect_tx(&full[s], 2 * kBlk + 2 * T.nb * kBlk);
+          const float* a = p.A + ((((size_t)T.f * p.Kc + T.kbeg + ch) * 2) * p.RTA + T.mt) * 4096;
+          const float* b = p.B + ((((size_t)T.f * p.Kc + T.kbeg + ch) * 2) * p.RTB + NB * T.nt) * 4096;
+          bulk_g2s(st, a, kBlk, &full[s]);
+          bulk_g2s(st + kBlk, a + (size_t)p.RTA * 4096, kBlk, &full[s]);
+          bulk_g2s(st + 2 * kBlk, b, T.nb * kBlk, &full[s]);
+          bulk_g2s(st + 4 * kBlk, b + (size_t)p.RTB * 4096, T.nb * kBlk, &full[s]);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
       const uint32_t idesc = NB == 2 ? umma_idesc_tf32(kTcM, 256) : umma_idesc_tf32(kTcM, 128);
-      for (int ch = 0; ch < nk; ++ch) {
-        const int g = ch / kTcDrain, buf = g & 1;
-        const bool first = (ch % kTcDrain) == 0;
-        if (first && g >= 2) mbar_wait(&acce[buf], ((g >> 1) - 1) & 1);
-        const int s = ch % kTcStages;
-        mbar_wait(&full[s], (ch / kTcStages) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t base = smem_u32(smem_raw + s * kTcStageBytes);
-        const uint32_t a_hi = base, a_lo = base + kBlk, b_hi = base + 2 * kBlk, b_lo = base + 4 * kBlk;
-        const uint32_t acc_t = tmem + buf * 256;
+      int gch = 0, gg0 = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const Tile T = tile_of(t);
+        for (int ch = 0; ch < T.nk; ++ch, ++gch) {
+          const int gg = gg0 + ch / kTcDrain, buf = gg & 1;
+          const bool first = (ch % kTcDrain) == 0;
+          if (first && gg >= 2) mbar_wait(&acce[buf], ((gg >> 1) - 1) & 1);
+          const int s = gch % kTcStages;
+          mbar_wait(&full[s], (gch / kTcStages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t base = smem_u32(smem_raw + s * kTcStageBytes);
+          const uint32_t a_hi = base, a_lo = base + kBlk, b_hi = base + 2 * kBlk, b_lo = base + 4 * kBlk;
+          const uint32_t acc_t = tmem + buf * 256;
 #pragma unroll
-        for (int ks = 0; ks < kTcK / 8; ++ks) {  // K = 8 tf32 per MMA = 2 core-matrix columns
-          const uint32_t koff = ks * 256;        // 2 × 128 B
-          const uint64_t dah = umma_desc_kmajor(a_hi + koff, 128, 1024);
-          const uint64_t dal = umma_desc_kmajor(a_lo + koff, 128, 1024);
-          const uint64_t dbh = umma_desc_kmajor(b_hi + koff, 128, 1024);
-          const uint64_t dbl = umma_desc_kmajor(b_lo + koff, 128, 1024);
-          umma_tf32(acc_t, dal, dbh, idesc, (first && ks == 0) ? 0u : 1u);
-          umma_tf32(acc_t, dah, dbl, idesc, 1u);
-          umma_tf32(acc_t, dah, dbh, idesc, 1u);
+          for (int ks = 0; ks < kTcK / 8; ++ks) {  // K = 8 tf32 per MMA = 2 core-matrix columns
+            const uint32_t koff = ks * 256;        // 2 × 128 B
+            const uint64_t dah = umma_desc_kmajor(a_hi + koff, 128, 1024);
+            const uint64_t dal = umma_desc_kmajor(a_lo + koff, 128, 1024);
+            const uint64_t dbh = umma_desc_kmajor(b_hi + koff, 128, 1024);
+            const uint64_t dbl = umma_desc_kmajor(b_lo + koff, 128, 1024);
+            umma_tf32(acc_t, dal, dbh, idesc, (first && ks == 0) ? 0u : 1u);
+            umma_tf32(acc_t, dah, dbl, idesc, 1u);
+            umma_tf32(acc_t, dah, dbh, idesc, 1u);
+          }
+          umma_commit(&empty[s]);
+          if ((ch % kTcDrain) == kTcDrain - 1 || ch == T.nk - 1) umma_commit(&accf[buf]);
         }
-        umma_commit(&empty[s]);
-        if ((ch % kTcDrain) == kTcDrain - 1 || ch == nk - 1) umma_commit(&accf[buf]);
+        gg0 += groups_of(T.nk);
       }
     }
   } else {
     // drain / epilogue: warp w reads TMEM lanes 32·(w%4).., column half (w−2)/4
     const int q = warp & 3, half = (warp - 2) >> 2;
     const int row = 32 * q + lane, cb = 128 * half;
-    const bool active = cb < ncols;
-    float acc[128];
+    int gg0 = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const Tile T = tile_of(t);
+      const int ngroups = groups_of(T.nk);
+      const bool active = cb < T.ncols;
+      float acc[128];
 #pragma unroll
-    for (int j = 0; j < 128; ++j) acc[j] = 0.f;
-    for (int g = 0; g < ngroups; ++g) {
-      const int buf = g & 1;
-      mbar_wait(&accf[buf], (g >> 1) & 1);
-      __syncwarp();
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (active) {
+      for (int j = 0; j < 128; ++j) acc[j] = 0.f;
+      for (int gl = 0; gl < ngroups; ++gl) {
+        const int gg = gg0 + gl, buf = gg & 1;
+        mbar_wait(&accf[buf], (gg >> 1) & 1);
+        __syncwarp();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (active) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          float v[32];
-          tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + buf * 256 + cb + 32 * c, v);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          for (int c = 0; c < 4; ++c) {
+            float v[32];
+            tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + buf * 256 + cb + 32 * c, v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-          for (int j = 0; j < 32; ++j) acc[32 * c + j] += v[j];
+            for (int j = 0; j < 32; ++j) acc[32 * c + j] += v[j];
+          }
         }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acce[buf]);
       }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&acce[buf]);
-    }
-    if (active && row < mrows) {
-      if (p.mode == 1) {
-        const int k = m0 + row, f1 = f / p.P, f2 = f - (f / p.P) * p.P;
-        const int bins = p.H * p.P;
-        float* pk = p.partial + ((size_t)(p.g0 + split) * p.M + k) * p.Cf * bins * 2 + (size_t)(f2 * p.H + f1) * 2;
+      gg0 += ngroups;
+      if (active && row < T.mrows) {
+        if (p.mode == 1) {
+          const int k = T.m0 + row, f1 = T.f / p.P, f2 = T.f - (T.f / p.P) * p.P;
+          const int bins = p.H * p.P;
+          float* pk = p.partial + ((size_t)(p.g0 + T.split) * p.M + k) * p.Cf * bins * 2 + (size_t)(f2 * p.H + f1) * 2;
 #pragma unroll
-        for (int j = 0; j < 128; ++j) {
-          const int nn = cb + j;
-          if (nn < ncols) {
-            const int n = n0 + nn;
-            const int im = n >= p.Cf, c = im ? n - p.Cf : n;
-            float* d = pk + (size_t)c * bins * 2 + im;
-            *d = p.accumulate ? *d + acc[j] : acc[j];
+          for (int j = 0; j < 128; ++j) {
+            const int nn = cb + j;
+            if (nn < T.ncols) {
+              const int n = T.n0 + nn;
+              const int im = n >= p.Cf, c = im ? n - p.Cf : n;
+              float* d = pk + (size_t)c * bins * 2 + im;
+              *d = p.accumulate ? *d + acc[j] : acc[j];
+            }
           }
         }
       }
-    }
-    if (p.mode == 0 && active) {
-      // transpose through shared memory (the pipeline stages are idle now: every bulk copy
-      // was consumed by an MMA that has completed) so each store instruction writes 128
-      // contiguous bytes of one D row
-      float* tile = reinterpret_cast<float*>(smem_raw) + (warp - 2) * 32 * 129;
+      if (p.mode == 0 && active) {
+        // transpose 32 columns at a time through this warp's own 32×33 buffer (the stages
+        // already hold the next tile's operands), so every store writes 128 contiguous
+        // bytes of one D row
+        float* tb = reinterpret_cast<float*>(smem_raw + kTcStages * kTcStageBytes) + (warp - 2) * 32 * 33;
+        const int nc = min(128, T.ncols - cb);
+        float* dbase = p.D + (long long)T.f * p.strideD + (long long)(T.m0 + 32 * q) * p.ldd + T.n0 + cb;
 #pragma unroll
-      for (int j = 0; j < 128; ++j) tile[lane * 129 + j] = acc[j];
-      __syncwarp();
-      const int nc = min(128, ncols - cb);
-      for (int r = 0; r < 32; ++r) {
-        const int m = 32 * q + r;
-        if (m >= mrows) break;
-        float* drow = p.D + (long long)f * p.strideD + (long long)(m0 + m) * p.ldd + n0 + cb;
+        for (int c = 0; c < 4; ++c) {
+          __syncwarp();
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int j = lane + 32 * i;
-          if (j < nc) __stcg(drow + j, tile[r * 129 + j]);
+          for (int j = 0; j < 32; ++j) tb[lane * 33 + j] = acc[32 * c + j];
+          __syncwarp();
+          const int col = 32 * c + lane;
+          if (col < nc) {
+            for (int r = 0; r < 32; ++r) {
+              if (32 * q + r >= T.mrows) break;
+              __stcg(dbase + (long long)r * p.ldd + col, tb[r * 33 + lane]);
+            }
+          }
         }
       }
     }
