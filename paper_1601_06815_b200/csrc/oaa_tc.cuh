@@ -53,17 +53,6 @@ struct BinGemmParams {
   int Kuse;  // K chunks holding data (≤ Kc; the rest of the layout is never read)
 };
 
-// UMMA shared-memory descriptor, K-major, no swizzle (Blackwell version 1).
-__device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;  // version = 1 (sm_100)
-  // base_offset 0, lbo_mode 0, layout_type 0 (SWIZZLE_NONE)
-  return d;
-}
-
 // Instruction descriptor: D f32, A/B tf32, both K-major.
 __host__ __device__ constexpr uint32_t umma_idesc_tf32(int M, int N) {
   return (1u << 4)                 // c_format = F32
@@ -81,11 +70,6 @@ __device__ __forceinline__ void umma_tf32(uint32_t dtmem, uint64_t adesc, uint64
       " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(dtmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
-}
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t ta, float (&v)[32]) {
