@@ -57,6 +57,8 @@ def main():
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     alu_peak = 2 * 148 * 128 * sm_mhz * 1e6  # flop/s
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0)) * 1e9
+    # fp32-accurate tensor rate: TF32 dense = bf16 × (1.1 / 2.25) (B200_PROFILING.md nominal ratio), / 3 for 3×TF32
+    tc_peak = float(peaks.get("bf16_tflops", 1590.0)) * 1e12 * (1.1 / 2.25) / 3
     wls = [CONFIGS["headline"]] + list(SWEEP) + [CONFIGS["alexnet"]]
     sh = CONFIGS["sharded"]
     from workloads import Workload
@@ -71,10 +73,22 @@ def main():
         direct = 3 * 2 * wl.B * wl.K * wl.C * wl.n ** 2 * M ** 2
         t_alu = sum(terms["flops"].values()) / alu_peak
         t_hbm = sum(terms["bytes"].values()) / hbm_peak
+        # SURVEY.md §8(d) roofline: T_roof = max(T_HBM, T_ALU(FFTs + overlap-add), T_TC(contraction
+        # at the fp32-accurate 3×TF32 rate)); the tensor-core path is taken for C, K ≥ 16
+        P = 2 * wl.n - 1
+        bins = P * wl.n
+        T = math.ceil(wl.N / wl.n) ** 2
+        Td = math.ceil(M / wl.n) ** 2
+        contraction = 8 * wl.K * wl.C * wl.B * bins * (T + 2 * Td)
+        t_fft = (sum(terms["flops"].values()) - contraction) / alu_peak
+        t_tc = contraction / tc_peak
+        t_roof = max(t_hbm, t_fft, t_tc)
+        bound = {t_hbm: "HBM", t_fft: "ALU", t_tc: "TC"}[t_roof]
         r = dict(config=wl.name, B=wl.B, C=wl.C, K=wl.K, N=wl.N, n=wl.n,
                  ms={k: round(v, 4) for k, v in t.items()}, step_ms=round(step, 4),
                  images_per_s=wl.B / (step / 1e3), tflop_eq_per_s=direct / (step / 1e3) / 1e12,
-                 alu_roofline_frac=t_alu / (step / 1e3), hbm_roofline_frac=t_hbm / (step / 1e3))
+                 alu_roofline_frac=t_alu / (step / 1e3), hbm_roofline_frac=t_hbm / (step / 1e3),
+                 roofline_bound=bound, roofline_frac=t_roof / (step / 1e3))
         rows.append(r)
         print(json.dumps(r), flush=True)
     lines = ["# r1 sweep: every BASELINE.json config on one B200 (tools/sweep.py)", "",
@@ -82,14 +96,17 @@ def main():
              f"Roofline denominators: fp32 FFMA {alu_peak / 1e12:.1f} TFLOP/s (148 SM × 128 lanes × 2 × "
              f"{sm_mhz:.0f} MHz) for the FFT-convention flops of SURVEY.md §8(d), HBM {hbm_peak / 1e9:.0f} GB/s "
              f"({src}) for the algorithmic bytes. TFLOP-eq/s counts the direct-convolution flops "
-             "(3 passes × 2·B·K·C·n²·M²), the convention for FFT-convolution layers.", "",
-             "| config | B | C | K | N | n | fwd ms | bwd_data ms | bwd_filter ms | step ms | images/s | TFLOP-eq/s | ALU frac | HBM frac |",
-             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
+             "(3 passes × 2·B·K·C·n²·M²), the convention for FFT-convolution layers. "
+             f"Roofline (SURVEY.md §8(d)): T_roof = max(T_HBM, T_ALU of the FFTs + overlap-add, T_TC of the "
+             f"contraction at the fp32-accurate 3×TF32 rate {tc_peak / 1e12:.0f} TFLOP/s = bf16 peak × 1.1/2.25 / 3); "
+             "'ALU frac (FMA path)' also counts the contraction on the FMA pipe, as the small-C kernels do.", "",
+             "| config | B | C | K | N | n | fwd ms | bwd_data ms | bwd_filter ms | step ms | images/s | TFLOP-eq/s | bound | roofline frac | ALU frac (FMA path) | HBM frac |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         lines.append(f"| {r['config']} | {r['B']} | {r['C']} | {r['K']} | {r['N']} | {r['n']} | {r['ms']['fwd']:.3f} | "
                      f"{r['ms']['bwd_data']:.3f} | {r['ms']['bwd_filter']:.3f} | {r['step_ms']:.3f} | "
-                     f"{r['images_per_s']:.0f} | {r['tflop_eq_per_s']:.1f} | {r['alu_roofline_frac']:.2f} | "
-                     f"{r['hbm_roofline_frac']:.2f} |")
+                     f"{r['images_per_s']:.0f} | {r['tflop_eq_per_s']:.1f} | {r['roofline_bound']} | "
+                     f"{r['roofline_frac']:.2f} | {r['alu_roofline_frac']:.2f} | {r['hbm_roofline_frac']:.2f} |")
     with open(args.out, "w") as f:
         f.write("\n".join(lines) + "\n")
 
