@@ -1359,9 +1359,11 @@ __global__ void __launch_bounds__(128) oaa_tile_spectra_kernel(const TileSpecPar
   const int Cinp = (p.Cin + 3) & ~3;
   const int TH8 = (p.T + 7) >> 3;
   const float* in_b = p.in + (size_t)b * p.Cin * p.R * p.R;
-  for (int c0 = 0; c0 < Cinp; c0 += CG) {
+  // one channel group of CG per CTA (blockIdx.y; the last group also zeroes the K padding):
+  // items × groups CTAs keep more of them in flight than a channel loop inside the CTA
+  {
+    const int c0 = blockIdx.y * CG;
     const int ncg = min(CG, p.Cin - c0);
-    __syncthreads();
     const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
     for (int sgm = warp; sgm < ncg * NN; sgm += nwarps) {
       const int ch = sgm / NN, rr = sgm - (sgm / NN) * NN;
@@ -1416,6 +1418,7 @@ __global__ void __launch_bounds__(128) oaa_tile_spectra_kernel(const TileSpecPar
     }
   }
   // zero the K padding columns (2·Cinp ≤ kk < 32·Kc) of this item's rows
+  if (blockIdx.y != gridDim.y - 1) return;
   const int padq = (32 * p.Kc - 2 * Cinp) >> 2;
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int e = tid; e < NN * P * p.T * padq; e += nthr) {

@@ -117,7 +117,7 @@ cudaError_t launch_tile_spectra_n(const oaa::TileSpecParams& p, size_t smem, cud
   auto k = oaa::oaa_tile_spectra_kernel<NN>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  k<<<p.bc * p.T, 128, smem, s>>>(p);
+  k<<<dim3(p.bc * p.T, (((p.Cin + 3) & ~3) + 15) / 16), 128, smem, s>>>(p);
   g_launches++;
   return cudaGetLastError();
 }
