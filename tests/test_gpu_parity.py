@@ -101,6 +101,19 @@ def test_tensor_core_path(B, C, K, N, n, crop):
     check(dw, oracle.conv_bwd_filter(d["x"], d["dy"], n, crop), "bwd_filter")
 
 
+@pytest.mark.parametrize("crop", ["valid", "same"])
+@pytest.mark.parametrize("n", [3, 5, 8])
+def test_largest_images(n, crop):
+    """N = 250, near the v1 limit: 8 chunk warps in the walker / bwd_data kernels (n = 8),
+    and the fallback engine where a tile row needs more than 8 chunk warps (n = 3)."""
+    B, C, K, N = 2, 3, 9, 250
+    d = make_inputs(B, C, K, N, n, crop, seed=250 + n)
+    y, dx, dw = run_all(d, N, n, crop)
+    check(y, oracle.conv_fwd(d["x"], d["w"], crop), f"fwd N=250 n={n} {crop}")
+    check(dx, oracle.conv_bwd_data(d["dy"], d["w"], N, crop), f"bwd_data N=250 n={n} {crop}")
+    check(dw, oracle.conv_bwd_filter(d["x"], d["dy"], n, crop), f"bwd_filter N=250 n={n} {crop}")
+
+
 @pytest.mark.parametrize("crop", CROPS)
 def test_config1_parity(crop):
     """BASELINE config 1: N=32, n=3, C=K=B=1, forward, vs CPU float64 direct."""
