@@ -44,7 +44,10 @@
  * order.  Outputs are fully overwritten, never accumulated; dw is the sum over this
  * call's B images only (the cross-GPU sum is the caller's all-reduce).  Concurrent
  * calls must use distinct workspaces.  Results are bitwise deterministic for a given
- * device and arguments.
+ * device and arguments (bwd_data adds the two overlapping contributions of a dx element
+ * with red.add onto an exact zero, which is order-independent).  Internally the kernels
+ * allocate tensor memory (tcgen05.alloc, ≤ 512 columns per SM) for their accumulators and
+ * release it before they exit.
  *
  * Errors: arguments are validated on the host before any launch; on error nothing is
  * written.  Launch failures are reported as OAA_ERR_CUDA (the call stays asynchronous).

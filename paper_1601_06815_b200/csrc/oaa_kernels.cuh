@@ -1,4 +1,11 @@
-// oaa_kernels.cuh -- the fused sm_100a kernels of the OaA convolution layer.
+// oaa_kernels.cuh -- shared helpers and the first-generation fused kernels of the OaA layer.
+//
+// Where the hot path runs: the forward walker (oaa_walk.cuh), bwd_data
+// (oaa_bwdd.cuh), bwd_filter (oaa_bwdf.cuh) for small channel counts; the tcgen05 bin GEMM
+// (oaa_tc.cuh) with the operand producers below for C, K ≥ 16.  The engines in this file
+// (oaa_engine_kernel S1/S2, oaa_engine_s1t_kernel, oaa_bwd_filter_kernel) cover the shapes
+// those kernels do not (e.g. 5 ≤ C ≤ 15 with small K, or a tile row needing more than 8
+// chunk warps); oaa_spectrum_kernel and oaa_filter_finalize_kernel are used by all paths.
 //
 // Notation: input blocks are n×n, transforms are P×P with
 // P = 2n−1, the half spectrum keeps rows f1 ∈ [0,H), H = n, and all
