@@ -376,7 +376,9 @@ BwdfPlan plan_bwdf(int B, int C, int K, int M, int n) {
   f.nwb = cdiv(cdiv(K, f.nkg), f.KPW);
   f.KG = f.nwb * f.KPW;
   f.tm = std::getenv("OAA_BWDF_REG") == nullptr;  // TMEM accumulators, 2 CTAs / SM
-  f.G = std::max(1, std::min(B * f.Td, (f.tm ? 296 : 148) / f.nkg));
+  int slots = f.tm ? 296 : 148;
+  if (const char* e = std::getenv("OAA_BWDF_SLOTS")) slots = std::max(1, atoi(e));  // experiment knob
+  f.G = std::max(1, std::min(B * f.Td, slots / f.nkg));
   f.SW = cdiv(f.NCH * f.CW + n - 1, 4) * 4;
   f.xs_b = align_up(sizeof(float4) * (size_t)B * f.Td * f.NCH * C * f.CH4);
   f.part_b = align_up(sizeof(float2) * (size_t)f.G * K * C * P * H);
