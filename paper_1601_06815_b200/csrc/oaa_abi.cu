@@ -382,7 +382,7 @@ BwdfPlan plan_bwdf(int B, int C, int K, int M, int n) {
   f.SW = cdiv(f.NCH * f.CW + n - 1, 4) * 4;
   f.xs_b = align_up(sizeof(float4) * (size_t)B * f.Td * f.NCH * C * f.CH4);
   f.part_b = align_up(sizeof(float2) * (size_t)f.G * K * C * P * H);
-  f.xspec_smem = sizeof(float) * (size_t)C * P * f.SW;
+  f.xspec_smem = oaa::xspec_smem_bytes(C, P, f.SW, f.CH4);
   f.smem = f.tm ? oaa::bwdf_smem_bytes<true>(n, C) : oaa::bwdf_smem_bytes<false>(n, C);
   if (f.smem > 220 * 1024 || f.xspec_smem > 220 * 1024) f.use = false;
   return f;
@@ -686,7 +686,7 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
     wpl.ngrp = wk.ngrp;
     wpl.NCH = wk.NCH;
     wpl.SW = xp.SW;
-    wpl.xspec_smem = sizeof(float) * (size_t)Cin * n * xp.SW;
+    wpl.xspec_smem = oaa::xspec_smem_bytes(Cin, n, xp.SW, wk.CH4);
     const int QSZ = ((2 * wk.TPW + 1) * n * g.P + 1) & ~1;
     wpl.walk_smem = sizeof(float4) * (size_t)oaa::kWalkRing * Cin * wk.CH4 + sizeof(float2) * (size_t)wk.KG * QSZ +
                     sizeof(float) * (size_t)wk.KG * oaa::walk_trp(n) * wk.NCH * wk.CW;

@@ -60,12 +60,21 @@ struct XSpecParams {
 
 // One CTA per (image, tile row): the rows of every channel are staged (zero padded),
 // then each task (chunk i, channel c, lane) computes its block-row spectrum.
+// Shared memory of oaa_xspec_kernel (256 threads): the staged input rows, then one output
+// tile of CH4 float4 per warp (128-byte aligned) for the bulk stores.
+__host__ __device__ inline size_t xspec_rows_floats(int Cin, int rows, int SW) {
+  return ((size_t)Cin * rows * SW + 31) & ~(size_t)31;
+}
+inline size_t xspec_smem_bytes(int Cin, int rows, int SW, int CH4) {
+  return sizeof(float) * xspec_rows_floats(Cin, rows, SW) + 8 * 16 * (size_t)CH4;
+}
+
 template <int NN, bool WIN>
 __global__ void __launch_bounds__(256) oaa_xspec_kernel(const XSpecParams p) {
   using G = WalkGeo<NN>;
   constexpr int P = G::P, H = G::H, RS4 = G::RS4;
   constexpr int ROWS = WIN ? P : NN;
-  extern __shared__ __align__(16) float rows_s[];  // [Cin][ROWS][SW]
+  extern __shared__ __align__(128) float rows_s[];  // [Cin][ROWS][SW] | per-warp output tile
   __shared__ float2 tw_s[16];                        // (cos, sin)(2π m / P), m < P
   const int tid = threadIdx.x, nthr = blockDim.x;
   if (tid < P) {
@@ -114,8 +123,8 @@ __global__ void __launch_bounds__(256) oaa_xspec_kernel(const XSpecParams p) {
   }
   for (int task = tid; task < ntask; task += nthr) {
     const int lane = task & 31, ic = task >> 5;
-    const int tt = lane / H, f1 = lane - (lane / H) * H;
-    if (tt >= G::TPW) continue;
+    const int tt0 = lane / H, f1 = lane - (lane / H) * H;
+    const int tt = tt0 < G::TPW ? tt0 : 0;  // (lanes past the last tile compute a dummy row)
     const int i = ic / p.Cin, c = ic - (ic / p.Cin) * p.Cin;
     float xr[P], xi[P];
     const float* blk = rows_s + c * ROWS * p.SW;
@@ -161,16 +170,29 @@ __global__ void __launch_bounds__(256) oaa_xspec_kernel(const XSpecParams p) {
       }
       dft<P, -1>(rr, ri, xr, xi);
     }
-    float4* d = out + (size_t)ic * G::CH4 + lane * RS4;
+    // the warp's 32 rows of this task are one contiguous 32·RS4 float4 run of S: stage them
+    // in the warp's smem tile and write them with one bulk copy (TMA engine)
+    float4* tb = reinterpret_cast<float4*>(rows_s + xspec_rows_floats(p.Cin, ROWS, p.SW)) + (tid >> 5) * G::CH4;
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // tile free
+    __syncwarp();
 #pragma unroll
     for (int q = 0; q < RS4; ++q) {
       const int f = 2 * q;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (f < P) { v.x = xr[f]; v.y = xi[f]; }
       if (f + 1 < P) { v.z = xr[f + 1]; v.w = xi[f + 1]; }
-      d[q] = v;
+      if (tt0 < G::TPW) tb[lane * RS4 + q] = v;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + (size_t)ic * G::CH4),
+                   "r"(smem_u32(tb)), "r"((uint32_t)(G::CH4 * 16))
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
   }
+  if ((tid & 31) == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // tiles read before exit
 }
 
 struct WalkParams {
