@@ -308,7 +308,9 @@ TcPlan plan_tc(int B, int Cin, int Cout, int R, int n) {
   t.RTB = cdiv(cdiv(t.bc * t.T * t.T, oaa::kTcM), t.NB) * t.NB;
   t.ag_b = sizeof(float) * (size_t)t.F * t.Kc * 2 * t.RTA * 4096;
   t.xg_b = sizeof(float) * (size_t)t.F * t.Kc * 2 * t.RTB * 4096;
-  t.d_b = sizeof(float) * (size_t)t.F * 2 * Cout * t.bc * t.T * t.T;
+  // Ŷ in the walker layout (oaa_tc.cuh mode 2): tile rows padded to whole walker chunks
+  const int TPW = 32 / n;
+  t.d_b = sizeof(float) * (size_t)t.F * 2 * Cout * ((size_t)t.bc * t.T * (cdiv(t.T, TPW) * TPW) + 31) / 32 * 32;
   return t;
 }
 
@@ -546,8 +548,17 @@ oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* 
   gp.RTB = tc.RTB;
   gp.S = 1;
   gp.kps = tc.Kc;
-  gp.mode = 0;
+  gp.mode = 2;  // Ŷ straight into the walker's chunk layout
   gp.partial = nullptr;
+  gp.Cf = Cout;
+  gp.H = n;
+  gp.P = g.P;
+  gp.TT = T;
+  gp.TPW = 32 / n;
+  gp.NT4 = cdiv(T, gp.TPW);
+  gp.SBL = 5;
+  if (const char* e = std::getenv("OAA_SBL")) gp.SBL = std::max(0, std::min(5, atoi(e)));  // experiment knob
+  gp.SB = 1 << gp.SBL;
   gp.NB = tc.NB;
   gp.Kuse = tc.Kc;
   // walker in LOAD mode: inverse DFT + overlap-add of Ŷ straight from the GEMM output
@@ -578,10 +589,12 @@ oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* 
     gp.N = (int)btc;
     gp.ldd = (int)btc;
     gp.strideD = (long long)2 * Cout * btc;
+    gp.plane = ((long long)bc * T * gp.NT4 * gp.TPW + gp.SB - 1) / gp.SB * 2 * tc.F * gp.SB;
     if (launch_bin_gemm(gp, s) != cudaSuccess) return OAA_ERR_CUDA;
     wp.B = bc;
     wp.b0 = b0;
     wp.BTc = (int)btc;
+    wp.SBL = gp.SBL;
     if (launch_walk_load(n, wp, walk_smem, bc, s) != cudaSuccess) return OAA_ERR_CUDA;
   }
   prof.stop();

@@ -51,6 +51,14 @@ struct BinGemmParams {
   float* partial;
   int NB;  // B row tiles per CTA (1: N tile 128, 2: N tile 256); RTB is a multiple of NB
   int Kuse;  // K chunks holding data (≤ Kc; the rest of the layout is never read)
+  // mode 2 (fwd / bwd_data, read by oaa_walk_kernel in load mode): column bt = (b·TT + t1)·TT
+  // + t2 is walker slot s = ((b·TT + t1)·NT4 + t2 / TPW)·TPW + t2 % TPW (tile rows padded to
+  // whole walker chunks of TPW tiles); row m = ri·Cf + o of bin f = f1·P + f2 goes to
+  //   D[o·plane + (s / 8)·16·F + ri·8·F + f·8 + s % 8],   F = H·P bins,
+  // i.e. blocks of 8 slots: every bin's run is one aligned 32-byte sector, and a walker chunk
+  // spans one or two blocks
+  int TT, TPW, NT4, SB, SBL;  // SB = 1 << SBL slots per block (8 in the text below)
+  long long plane;
 };
 
 // Instruction descriptor: D f32, A/B tf32, both K-major.
@@ -245,6 +253,35 @@ __global__ void __launch_bounds__(kTcThreads, 1) oaa_bin_gemm_kernel(const BinGe
               float* d = pk + (size_t)c * bins * 2 + im;
               *d = p.accumulate ? *d + acc[j] : acc[j];
             }
+          }
+        }
+      }
+      if (p.mode == 2 && active) {
+        // walker layout: per bin an SB-float run of slots; transpose 32 columns at a time
+        float* tb = reinterpret_cast<float*>(smem_raw + kTcStages * kTcStageBytes) + (warp - 2) * 32 * 33;
+        const int nc = min(128, T.ncols - cb);
+        const long long bf8 = (long long)p.SB * p.H * p.P;
+        // this lane's row offset (row 32·q + lane), fetched by the storing lanes with a shuffle
+        const int mrow = T.m0 + 32 * q + lane, rri = mrow >= p.Cf;
+        const long long rowoff = (long long)(mrow - (rri ? p.Cf : 0)) * p.plane + (rri ? bf8 : 0);
+        const int nr = min(32, T.mrows - 32 * q);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) tb[lane * 33 + j] = acc[32 * c + j];
+          __syncwarp();
+          const int col = 32 * c + lane;
+          float* dcol = p.D;
+          if (col < nc) {
+            const int n = T.n0 + cb + col;
+            const int rowt = n / p.TT, t2 = n - rowt * p.TT, ch = t2 / p.TPW;
+            const long long sl = ((long long)rowt * p.NT4 + ch) * p.TPW + (t2 - ch * p.TPW);
+            dcol += (sl >> p.SBL) * 2 * bf8 + (long long)T.f * p.SB + (sl & (p.SB - 1));
+          }
+          for (int r = 0; r < nr; ++r) {
+            const long long ro = __shfl_sync(0xffffffffu, rowoff, r);
+            if (col < nc) __stcg(dcol + ro, tb[r * 33 + lane]);
           }
         }
       }

@@ -202,10 +202,12 @@ struct WalkParams {
   int B, Cin, Cout, T, Ro, off, NCH;
   int KG;              // output channels (warps) per CTA
   int ngrp;            // channel groups per image = ceil(Cout / KG)
-  // LOAD mode (tensor-core path): Ŷ = D[f][m][bt] of the bin GEMM (m < Cout real part,
-  // m ≥ Cout imaginary part; bt = (b − b0)·T² + t1·T + t2 over a batch chunk of BTc tiles)
+  // LOAD mode (tensor-core path): Ŷ written by the bin GEMM in its mode-2 chunk layout
+  // (oaa_tc.cuh): per output channel, per (image, tile row, chunk) 2·H·P·TPW contiguous
+  // floats [re/im][f1·P + f2][tile in chunk]; BTc = tiles of the batch chunk (images × T²)
   const float* D;
   int BTc, b0;
+  int SBL;  // log2 of the slots per Ŷ block (oaa_tc.cuh mode 2)
 };
 
 constexpr int kWalkRing = 4;  // spectrum chunk slots per CTA
@@ -272,18 +274,22 @@ __global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
   }
   // LOAD: this lane's Ŷ row (bins f1·P + f2) for chunk (t1, i), prefetched one chunk ahead
   float ynr[LOAD ? P : 1], yni[LOAD ? P : 1];
-  const size_t dstride = LOAD ? (size_t)2 * p.Cout * p.BTc : 0;  // per bin
-  const float* dlane = LOAD ? p.D + (size_t)(f1 * P) * dstride + (size_t)(active ? co : 0) * p.BTc + (size_t)bl * p.T * p.T
-                            : nullptr;
+  // Ŷ in the layout of oaa_bin_gemm_kernel mode 2: blocks of 8 walker slots, per bin one
+  // 32-byte run; the chunk's TPW slots lie in one or two blocks
+  const int SB = 1 << p.SBL, BF8 = SB * H * P;
+  const int NT4 = (p.T + TPW - 1) / TPW;
+  const size_t dplane = LOAD ? ((size_t)(p.BTc / p.T) * NT4 * TPW + SB - 1) / SB * 2 * BF8 : 0;
+  const float* dlane = LOAD ? p.D + (size_t)(active ? co : 0) * dplane + f1 * P * SB : nullptr;
   auto load_y = [&](int t1, int i) {
     if constexpr (LOAD) {
       const int t2 = i * TPW + tt;
       const bool ok = active && laneA && t1 < p.T && t2 < p.T;
-      const float* d = dlane + (ok ? t1 * p.T + t2 : 0);
+      const size_t sl = ((size_t)(bl * p.T + t1) * NT4 + i) * TPW + tt;
+      const float* d = dlane + (ok ? (sl >> p.SBL) * 2 * BF8 + (sl & (SB - 1)) : 0);
 #pragma unroll
       for (int f2 = 0; f2 < P; ++f2) {
-        ynr[f2] = ok ? __ldg(d + (size_t)f2 * dstride) : 0.f;
-        yni[f2] = ok ? __ldg(d + (size_t)f2 * dstride + (size_t)p.Cout * p.BTc) : 0.f;
+        ynr[f2] = ok ? __ldg(d + f2 * SB) : 0.f;
+        yni[f2] = ok ? __ldg(d + BF8 + f2 * SB) : 0.f;
       }
     }
   };

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out/g89
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/g89/alex.csv python tools/prof_step.py 2 fwd,bwd_data 256,96,256,27,5 > /dev/null 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/g89/shard.csv python tools/prof_step.py 1 fwd,bwd_data 128,64,128,224,8 > /dev/null 2>&1
