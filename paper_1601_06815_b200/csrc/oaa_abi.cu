@@ -300,14 +300,14 @@ TcPlan plan_tc(int B, int Cin, int Cout, int R, int n) {
   t.T = cdiv(R, n);
   t.Kc = cdiv(2 * ((Cin + 3) & ~3), oaa::kTcK);
   t.RTA = cdiv(2 * Cout, oaa::kTcM);
-  const size_t per_img = sizeof(float) * (size_t)t.F * t.T * t.T * (2 * (size_t)t.Kc * oaa::kTcK + 2 * (size_t)Cout);
+  const size_t per_img = sizeof(float) * (size_t)t.F * t.T * t.T * ((size_t)t.Kc * oaa::kTcK + 2 * (size_t)Cout);
   t.nchunks = (int)std::max<size_t>(1, (B * per_img + kTcChunkBytes - 1) / kTcChunkBytes);
   t.bc = cdiv(B, t.nchunks);
   t.nchunks = cdiv(B, t.bc);
   t.NB = t.bc * t.T * t.T > oaa::kTcM ? 2 : 1;
   t.RTB = cdiv(cdiv(t.bc * t.T * t.T, oaa::kTcM), t.NB) * t.NB;
-  t.ag_b = sizeof(float) * (size_t)t.F * t.Kc * 2 * t.RTA * 4096;
-  t.xg_b = sizeof(float) * (size_t)t.F * t.Kc * 2 * t.RTB * 4096;
+  t.ag_b = sizeof(float) * (size_t)t.F * t.Kc * 2 * t.RTA * 4096;  // pre-split (hi | lo)
+  t.xg_b = sizeof(float) * (size_t)t.F * t.Kc * t.RTB * 4096;
   // Ŷ in the walker layout (oaa_tc.cuh mode 2): tile rows padded to whole walker chunks
   const int TPW = 32 / n;
   t.d_b = sizeof(float) * (size_t)t.F * 2 * Cout * ((size_t)t.bc * t.T * (cdiv(t.T, TPW) * TPW) + 31) / 32 * 32;
@@ -455,7 +455,7 @@ TcFiltPlan plan_tc_filter(int B, int C, int K, int N, int M, int n) {
   t.RTA = cdiv(K, oaa::kTcM);
   t.NB = 2 * C > oaa::kTcM ? 2 : 1;
   t.RTB = cdiv(cdiv(2 * C, oaa::kTcM), t.NB) * t.NB;
-  const size_t per_img = sizeof(float) * (size_t)t.F * 2 * t.T2 * 2 * 128 * (size_t)(t.RTA + t.RTB);
+  const size_t per_img = sizeof(float) * (size_t)t.F * 2 * t.T2 * 128 * (size_t)(t.RTA + t.RTB);
   t.nchunks = (int)std::max<size_t>(1, (B * per_img + kTcChunkBytes - 1) / kTcChunkBytes);
   t.bc = cdiv(B, t.nchunks);
   t.nchunks = cdiv(B, t.bc);
@@ -470,8 +470,8 @@ TcFiltPlan plan_tc_filter(int B, int C, int K, int N, int M, int n) {
   t.G = t.S;  // chunks accumulate into the same per-split slabs, in stream order
   t.SWg = cdiv(t.Td * n, 4) * 4;
   t.SWx = cdiv(t.Td * n + n - 1, 4) * 4;
-  t.a_b = align_up(sizeof(float) * (size_t)t.F * t.Kc * 2 * t.RTA * 4096);
-  t.b_b = align_up(sizeof(float) * (size_t)t.F * t.Kc * 2 * t.RTB * 4096);
+  t.a_b = align_up(sizeof(float) * (size_t)t.F * t.Kc * t.RTA * 4096);
+  t.b_b = align_up(sizeof(float) * (size_t)t.F * t.Kc * t.RTB * 4096);
   t.part_b = align_up(sizeof(float2) * (size_t)t.G * K * C * t.F);
   return t;
 }
@@ -549,6 +549,8 @@ oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* 
   gp.S = 1;
   gp.kps = tc.Kc;
   gp.mode = 2;  // Ŷ straight into the walker's chunk layout
+  gp.a_split = 1;
+  gp.nohi = std::getenv("OAA_TC_NOHI") != nullptr;  // experiment knob
   gp.partial = nullptr;
   gp.Cf = Cout;
   gp.H = n;
@@ -768,7 +770,7 @@ oaa_status_t run_filter_tc(const float* x, const float* dy, float* dw, int B, in
   const size_t smem_x = sizeof(float) * 8 * (2 * n - 1) * (size_t)t.SWx;
   oaa::BinGemmParams gp{};
   gp.A = Ga; gp.B = Xb; gp.D = nullptr; gp.F = t.F; gp.M = K; gp.N = 2 * C; gp.Kc = t.Kc; gp.RTA = t.RTA;
-  gp.RTB = t.RTB; gp.ldd = 0; gp.strideD = 0; gp.S = t.S; gp.kps = t.kps; gp.mode = 1; gp.Cf = C; gp.H = n;
+  gp.RTB = t.RTB; gp.ldd = 0; gp.strideD = 0; gp.S = t.S; gp.kps = t.kps; gp.mode = 1; gp.a_split = 0; gp.nohi = std::getenv("OAA_TC_NOHI") != nullptr; gp.Cf = C; gp.H = n;
   gp.P = 2 * n - 1; gp.partial = part; gp.NB = t.NB;
   ProfScope prof(OAA_OP_BWD_FILTER, s);
   prof.start();
@@ -959,7 +961,7 @@ size_t oaa_debug_bin_gemm_workspace_bytes(int F, int M, int N, int Kd) {
   if (F < 1 || M < 1 || N < 1 || Kd < 1) return 0;
   const size_t NB = N > oaa::kTcM ? 2 : 1;
   const size_t Kc = cdiv(Kd, oaa::kTcK), RTA = cdiv(M, oaa::kTcM), RTB = (cdiv(cdiv(N, oaa::kTcM), (int)NB)) * NB;
-  return align_up(sizeof(float) * (size_t)F * Kc * 2 * RTA * 4096) + align_up(sizeof(float) * (size_t)F * Kc * 2 * RTB * 4096);
+  return align_up(sizeof(float) * (size_t)F * Kc * RTA * 4096) + align_up(sizeof(float) * (size_t)F * Kc * RTB * 4096);
 }
 
 oaa_status_t oaa_debug_bin_gemm(const float* A, const float* B, float* D, int F, int M, int N, int Kd, void* ws,
@@ -968,14 +970,14 @@ oaa_status_t oaa_debug_bin_gemm(const float* A, const float* B, float* D, int F,
   const size_t need = oaa_debug_bin_gemm_workspace_bytes(F, M, N, Kd);
   if (!ws || ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0) return OAA_ERR_WORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  oaa::BinGemmParams p;
+  oaa::BinGemmParams p{};
   p.F = F; p.M = M; p.N = N; p.ldd = N;
   p.NB = N > oaa::kTcM ? 2 : 1;
   p.Kc = cdiv(Kd, oaa::kTcK); p.RTA = cdiv(M, oaa::kTcM); p.RTB = cdiv(cdiv(N, oaa::kTcM), p.NB) * p.NB;
   p.strideD = (long long)M * N;
   p.S = 1; p.kps = p.Kc; p.mode = 0; p.partial = nullptr; p.accumulate = 0; p.Kuse = p.Kc;
   float* Ap = static_cast<float*>(ws);
-  float* Bp = reinterpret_cast<float*>(static_cast<char*>(ws) + align_up(sizeof(float) * (size_t)F * p.Kc * 2 * p.RTA * 4096));
+  float* Bp = reinterpret_cast<float*>(static_cast<char*>(ws) + align_up(sizeof(float) * (size_t)F * p.Kc * p.RTA * 4096));
   oaa::oaa_tc_pack_kernel<<<1024, 256, 0, s>>>(A, Ap, F, M, Kd, p.Kc, p.RTA);
   g_launches++;
   oaa::oaa_tc_pack_kernel<<<1024, 256, 0, s>>>(B, Bp, F, N, Kd, p.Kc, p.RTB);

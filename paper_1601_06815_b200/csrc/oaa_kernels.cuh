@@ -1317,23 +1317,29 @@ __global__ void oaa_spectrum_kernel(const float* __restrict__ w, float4* __restr
 namespace oaa {
 
 // ------------------------------------------------------------------ operand producers
-// Operands of the tensor-core bin GEMM (oaa_tc.cuh) are written pre-split (3×TF32:
-// x = hi + lo, hi = x with the low 13 mantissa bits cleared) in the UMMA-blocked layout
-//   Op[f][kc][h][rt][4096 floats],  kc = k/32, h = hi|lo, rt = r/128,
-// each block a 128-row × 32-k tile in canonical no-swizzle K-major order.
-__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-  hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-  lo = x - hi;
-}
-__device__ __forceinline__ size_t tc_idx(int f, int Kc, int RT, int h, int r, int k) {
-  return ((((size_t)f * Kc + (k >> 5)) * 2 + h) * RT + (r >> 7)) * 4096 + ((r & 127) >> 3) * 256 +
+// Operands of the tensor-core bin GEMM (oaa_tc.cuh) are written as plain fp32 in the
+// UMMA-blocked layout
+//   Op[f][kc][rt][4096 floats],  kc = k/32, rt = r/128,
+// each block a 128-row × 32-k tile in canonical no-swizzle K-major order.  The GEMM splits
+// them for 3×TF32 in shared memory (hi = x with the low 13 mantissa bits cleared, lo = x − hi).
+__device__ __forceinline__ size_t tc_idx(int f, int Kc, int RT, int r, int k) {
+  return (((size_t)f * Kc + (k >> 5)) * RT + (r >> 7)) * 4096 + ((r & 127) >> 3) * 256 +
          ((k & 31) >> 2) * 32 + (r & 7) * 4 + (k & 3);
 }
 __device__ __forceinline__ void tc_put(float* Op, int f, int Kc, int RT, int r, int k, float v) {
-  float hi, lo;
-  split_tf32(v, hi, lo);
-  Op[tc_idx(f, Kc, RT, 0, r, k)] = hi;
-  Op[tc_idx(f, Kc, RT, 1, r, k)] = lo;
+  Op[tc_idx(f, Kc, RT, r, k)] = v;
+}
+// Pre-split variant for the small, reused A operand of fwd / bwd_data (the real-ified
+// weights): Op[f][kc][h][rt][4096], h = hi | lo, so the GEMM copies both halves and its
+// converter warps only split B.
+__device__ __forceinline__ size_t tc_idx_split(int f, int Kc, int RT, int h, int r, int k) {
+  return ((((size_t)f * Kc + (k >> 5)) * 2 + h) * RT + (r >> 7)) * 4096 + ((r & 127) >> 3) * 256 +
+         ((k & 31) >> 2) * 32 + (r & 7) * 4 + (k & 3);
+}
+__device__ __forceinline__ void tc_put_split(float* Op, int f, int Kc, int RT, int r, int k, float v) {
+  const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+  Op[tc_idx_split(f, Kc, RT, 0, r, k)] = hi;
+  Op[tc_idx_split(f, Kc, RT, 1, r, k)] = v - hi;
 }
 
 // B operand: the forward spectra of every input block of a batch chunk, row
@@ -1412,15 +1418,10 @@ __global__ void __launch_bounds__(128) oaa_tile_spectra_kernel(const TileSpecPar
 #pragma unroll
       for (int f2 = 0; f2 < P; ++f2) {
         const int f = f1 * P + f2;
-        float h[4], l[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) split_tf32(xr[i][f2], h[i], l[i]);
-        *reinterpret_cast<float4*>(p.Xg + tc_idx(f, p.Kc, p.RTB, 0, bt, cb)) = make_float4(h[0], h[1], h[2], h[3]);
-        *reinterpret_cast<float4*>(p.Xg + tc_idx(f, p.Kc, p.RTB, 1, bt, cb)) = make_float4(l[0], l[1], l[2], l[3]);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) split_tf32(xi[i][f2], h[i], l[i]);
-        *reinterpret_cast<float4*>(p.Xg + tc_idx(f, p.Kc, p.RTB, 0, bt, Cinp + cb)) = make_float4(h[0], h[1], h[2], h[3]);
-        *reinterpret_cast<float4*>(p.Xg + tc_idx(f, p.Kc, p.RTB, 1, bt, Cinp + cb)) = make_float4(l[0], l[1], l[2], l[3]);
+        *reinterpret_cast<float4*>(p.Xg + tc_idx(f, p.Kc, p.RTB, bt, cb)) =
+            make_float4(xr[0][f2], xr[1][f2], xr[2][f2], xr[3][f2]);
+        *reinterpret_cast<float4*>(p.Xg + tc_idx(f, p.Kc, p.RTB, bt, Cinp + cb)) =
+            make_float4(xi[0][f2], xi[1][f2], xi[2][f2], xi[3][f2]);
       }
     }
   }
@@ -1431,8 +1432,7 @@ __global__ void __launch_bounds__(128) oaa_tile_spectra_kernel(const TileSpecPar
   for (int e = tid; e < NN * P * p.T * padq; e += nthr) {
     const int qq = e % padq, rest = e / padq;
     const int t2 = rest % p.T, f = rest / p.T;
-    *reinterpret_cast<float4*>(p.Xg + tc_idx(f, p.Kc, p.RTB, 0, bt0 + t2, 2 * Cinp + 4 * qq)) = z;
-    *reinterpret_cast<float4*>(p.Xg + tc_idx(f, p.Kc, p.RTB, 1, bt0 + t2, 2 * Cinp + 4 * qq)) = z;
+    *reinterpret_cast<float4*>(p.Xg + tc_idx(f, p.Kc, p.RTB, bt0 + t2, 2 * Cinp + 4 * qq)) = z;
   }
 }
 
@@ -1543,20 +1543,13 @@ __global__ void __launch_bounds__(256) oaa_filter_spectra_kernel(const FiltSpecP
             v[2 * h + 1] = rowk == 0 ? si[h][f2] : -sr[h][f2];
           }
           const int row = ch + rowk * p.nch;
-          float hi[4], lo[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) split_tf32(v[e], hi[e], lo[e]);
-          float* dh = p.Op + tc_idx(f, p.Kc, p.RT, 0, row, 4 * q);
-          float* dl = p.Op + tc_idx(f, p.Kc, p.RT, 1, row, 4 * q);
+          float* dh = p.Op + tc_idx(f, p.Kc, p.RT, row, 4 * q);
           if (have[0] && have[1]) {
-            *reinterpret_cast<float4*>(dh) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-            *reinterpret_cast<float4*>(dl) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+            *reinterpret_cast<float4*>(dh) = make_float4(v[0], v[1], v[2], v[3]);
           } else if (have[0]) {
-            *reinterpret_cast<float2*>(dh) = make_float2(hi[0], hi[1]);
-            *reinterpret_cast<float2*>(dl) = make_float2(lo[0], lo[1]);
+            *reinterpret_cast<float2*>(dh) = make_float2(v[0], v[1]);
           } else {
-            *reinterpret_cast<float2*>(dh + 2) = make_float2(hi[2], hi[3]);
-            *reinterpret_cast<float2*>(dl + 2) = make_float2(lo[2], lo[3]);
+            *reinterpret_cast<float2*>(dh + 2) = make_float2(v[2], v[3]);
           }
         }
       }
@@ -1569,14 +1562,13 @@ __global__ void __launch_bounds__(256) oaa_filter_spectra_kernel(const FiltSpecP
 __global__ void oaa_tc_zero_tail_kernel(float* Op, int F, int Kc, int RT, int j0, int j1) {
   const int tail = j1 - j0;
   if (tail <= 0) return;
-  const long long total = (long long)F * 2 * RT * 128 * tail;
+  const long long total = (long long)F * RT * 128 * tail;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
     const int j = j0 + (int)(t % tail);
     const int r = (int)((t / tail) % (RT * 128));
-    const int h = (int)((t / ((long long)tail * RT * 128)) % 2);
-    const int f = (int)(t / ((long long)tail * RT * 128 * 2));
-    Op[tc_idx(f, Kc, RT, h, r, j)] = 0.f;
+    const int f = (int)(t / ((long long)tail * RT * 128));
+    Op[tc_idx(f, Kc, RT, r, j)] = 0.f;
   }
 }
 

@@ -10,12 +10,13 @@
 // x = hi + lo (hi = x with the low 13 mantissa bits cleared, lo = x − hi) and
 // D = A_lo·B_hi + A_hi·B_lo + A_hi·B_hi accumulates in tensor memory.
 //
-// Operands arrive pre-split in the UMMA-blocked layout written by their producers
-// (tile spectra / real-ified weights, oaa_kernels.cuh): for each (bin, 32-wide K chunk,
-// hi|lo) the row tiles of 128 rows are consecutive 16 KB blocks in the canonical
-// no-swizzle K-major order (8-row × 16-byte core matrices: LBO = 128 B between the two K
-// halves of an MMA, SBO = 1 KB between 8-row groups).  So every pipeline stage is four
-// plain bulk copies (cp.async.bulk, TMA engine) and no thread touches operand data.
+// Operands arrive as plain fp32 in the UMMA-blocked layout written by their producers
+// (tile spectra / real-ified weights, oaa_kernels.cuh): for each (bin, 32-wide K chunk)
+// the row tiles of 128 rows are consecutive 16 KB blocks in the canonical no-swizzle
+// K-major order (8-row × 16-byte core matrices: LBO = 128 B between the two K halves of an
+// MMA, SBO = 1 KB between 8-row groups).  Every pipeline stage is two bulk copies
+// (cp.async.bulk, TMA engine); two converter warps split the stage in shared memory (hi in
+// place, lo into the stage's second half), so HBM carries each operand once.
 //
 // Kernel (one CTA = one 128 × 256 output tile of one bin, 128 threads, 1 CTA/SM):
 //   * warp 0 lane 0: producer -- per K chunk waits for the stage to be free, posts the
@@ -57,6 +58,8 @@ struct BinGemmParams {
   //   D[o·plane + (s / 8)·16·F + ri·8·F + f·8 + s % 8],   F = H·P bins,
   // i.e. blocks of 8 slots: every bin's run is one aligned 32-byte sector, and a walker chunk
   // spans one or two blocks
+  int a_split;  // A arrives pre-split ([F][Kc][hi|lo][RTA][4096]); B is always plain fp32
+  int nohi;     // experiment: leave x in the hi slot (relies on the MMA ignoring the low bits)
   int TT, TPW, NT4, SB, SBL;  // SB = 1 << SBL slots per block (8 in the text below)
   long long plane;
 };
@@ -97,7 +100,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t ta, float (&v)[32]) {
 // round-to-nearest FADDs keeps long reductions (the weight gradient's B·T′) at fp32
 // accuracy.
 constexpr int kTcDrain = 8;
-constexpr int kTcThreads = 320;  // warp 0 TMA producer, warp 1 MMA issuer, warps 2..9 drain/epilogue
+constexpr int kTcThreads = 384;  // warp 0 TMA producer, warp 1 MMA issuer, warps 2..9 drain/epilogue,
+                                 // warps 10, 11 hi/lo converters
 
 // D[f][m][n] = Σ_k A[f][m][k] · B[f][n][k]  (3×TF32).  grid = (ceil(N/(128·NB)), ceil(M/128), F·S)
 // Two TMEM accumulators of 256 columns alternate per group of kTcDrain K chunks, so the
@@ -109,7 +113,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) oaa_bin_gemm_kernel(const BinGe
   // the MMAs of tile t+1 already run into the other accumulator.
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // stage s: [A_hi 16K][A_lo 16K][B_hi 32K][B_lo 32K]
-  __shared__ uint64_t full[kTcStages], empty[kTcStages], accf[2], acce[2];
+  __shared__ uint64_t full[kTcStages], conv[kTcStages], empty[kTcStages], accf[2], acce[2];
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int NB = p.NB, ntile = kTcM * NB;
@@ -122,6 +126,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) oaa_bin_gemm_kernel(const BinGe
   if (tid == 32) {
     for (int s = 0; s < kTcStages; ++s) {
       mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 2);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -164,13 +169,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) oaa_bin_gemm_kernel(const BinGe
           const int s = gch % kTcStages;
           if (gch >= kTcStages) mbar_wait(&empty[s], ((gch / kTcStages) - 1) & 1);
           unsigned char* st = smem_raw + s * kTcStageBytes;
-          mbar_expect_tx(&full[s], 2 * kBlk + 2 * T.nb * kBlk);
-          const float* a = p.A + ((((size_t)T.f * p.Kc + T.kbeg + ch) * 2) * p.RTA + T.mt) * 4096;
-          const float* b = p.B + ((((size_t)T.f * p.Kc + T.kbeg + ch) * 2) * p.RTB + NB * T.nt) * 4096;
+          mbar_expect_tx(&full[s], (p.a_split ? 2 : 1) * kBlk + T.nb * kBlk);
+          const size_t kk = (size_t)T.f * p.Kc + T.kbeg + ch;
+          const float* a = p.A + ((p.a_split ? 2 * kk : kk) * p.RTA + T.mt) * 4096;
+          const float* b = p.B + (kk * p.RTB + NB * T.nt) * 4096;
           bulk_g2s(st, a, kBlk, &full[s]);
-          bulk_g2s(st + kBlk, a + (size_t)p.RTA * 4096, kBlk, &full[s]);
+          if (p.a_split) bulk_g2s(st + kBlk, a + (size_t)p.RTA * 4096, kBlk, &full[s]);
           bulk_g2s(st + 2 * kBlk, b, T.nb * kBlk, &full[s]);
-          bulk_g2s(st + 4 * kBlk, b + (size_t)p.RTB * 4096, T.nb * kBlk, &full[s]);
         }
       }
     }
@@ -185,7 +190,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) oaa_bin_gemm_kernel(const BinGe
           const bool first = (ch % kTcDrain) == 0;
           if (first && gg >= 2) mbar_wait(&acce[buf], ((gg >> 1) - 1) & 1);
           const int s = gch % kTcStages;
-          mbar_wait(&full[s], (gch / kTcStages) & 1);
+          mbar_wait(&conv[s], (gch / kTcStages) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t base = smem_u32(smem_raw + s * kTcStageBytes);
           const uint32_t a_hi = base, a_lo = base + kBlk, b_hi = base + 2 * kBlk, b_lo = base + 4 * kBlk;
@@ -205,6 +210,51 @@ __global__ void __launch_bounds__(kTcThreads, 1) oaa_bin_gemm_kernel(const BinGe
           if ((ch % kTcDrain) == kTcDrain - 1 || ch == T.nk - 1) umma_commit(&accf[buf]);
         }
         gg0 += groups_of(T.nk);
+      }
+    }
+  } else if (warp >= 10) {
+    // converters: x → hi (low 13 mantissa bits cleared, in place) and lo = x − hi (the
+    // stage's lo slot) for the A block and the nb B blocks; the tensor core reads the
+    // stage through the async proxy, hence the proxy fence before the arrive
+    const int ct = tid - 320;
+    int gch = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const Tile T = tile_of(t);
+      for (int ch = 0; ch < T.nk; ++ch, ++gch) {
+        const int s = gch % kTcStages;
+        mbar_wait(&full[s], (gch / kTcStages) & 1);
+        unsigned char* st = smem_raw + s * kTcStageBytes;
+        float4* ah = reinterpret_cast<float4*>(st);
+        float4* al = reinterpret_cast<float4*>(st + kBlk);
+        float4* bh = reinterpret_cast<float4*>(st + 2 * kBlk);
+        float4* bl = reinterpret_cast<float4*>(st + 4 * kBlk);
+        const int nb4 = T.nb * 1024;
+        auto split4 = [](float4& h, float4& l, float4 x) {
+          h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+          h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+          h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+          h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+          l = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+        };
+        if (!p.a_split) {
+#pragma unroll 4
+          for (int e = ct; e < 1024; e += 64) {
+            float4 h, l;
+            split4(h, l, ah[e]);
+            if (!p.nohi) ah[e] = h;
+            al[e] = l;
+          }
+        }
+#pragma unroll 4
+        for (int e = ct; e < nb4; e += 64) {
+          float4 h, l;
+          split4(h, l, bh[e]);
+          if (!p.nohi) bh[e] = h;
+          bl[e] = l;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[s]);
       }
     }
   } else {
@@ -350,10 +400,10 @@ __global__ void oaa_realified_spectrum_kernel(const float* __restrict__ w, float
         si -= (double)v * ts[mm];
       }
     const float re = (float)(sr * inv), im = (float)(si * inv);
-    tc_put(Ag, f, Kc, RTA, o, i, re);
-    tc_put(Ag, f, Kc, RTA, o, Cip + i, -im);
-    tc_put(Ag, f, Kc, RTA, Co + o, i, im);
-    tc_put(Ag, f, Kc, RTA, Co + o, Cip + i, re);
+    tc_put_split(Ag, f, Kc, RTA, o, i, re);
+    tc_put_split(Ag, f, Kc, RTA, o, Cip + i, -im);
+    tc_put_split(Ag, f, Kc, RTA, Co + o, i, im);
+    tc_put_split(Ag, f, Kc, RTA, Co + o, Cip + i, re);
   }
 }
 
