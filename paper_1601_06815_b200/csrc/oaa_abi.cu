@@ -766,8 +766,8 @@ oaa_status_t run_filter_tc(const float* x, const float* dy, float* dw, int B, in
   oaa::FiltSpecParams xs{};
   xs.src = x; xs.Op = Xb; xs.nch = C; xs.R = N; xs.Td = t.Td; xs.org = g.o - (n - 1); xs.Kc = t.Kc;
   xs.RT = t.RTB; xs.SW = t.SWx;
-  const size_t smem_g = sizeof(float) * 8 * n * (size_t)t.SWg;
-  const size_t smem_x = sizeof(float) * 8 * (2 * n - 1) * (size_t)t.SWx;
+  const size_t smem_g = sizeof(float) * oaa::kFsCG * n * (size_t)t.SWg;
+  const size_t smem_x = sizeof(float) * oaa::kFsCG * (2 * n - 1) * (size_t)t.SWx;
   oaa::BinGemmParams gp{};
   gp.A = Ga; gp.B = Xb; gp.D = nullptr; gp.F = t.F; gp.M = K; gp.N = 2 * C; gp.Kc = t.Kc; gp.RTA = t.RTA;
   gp.RTB = t.RTB; gp.ldd = 0; gp.strideD = 0; gp.S = t.S; gp.kps = t.kps; gp.mode = 1; gp.a_split = 0; gp.nohi = std::getenv("OAA_TC_NOHI") != nullptr; gp.Cf = C; gp.H = n;

@@ -1450,12 +1450,13 @@ struct FiltSpecParams {
   int nch, R, Td, org, b0, Kc, RT, SW;
 };
 
+constexpr int kFsCG = 4;  // channels per CTA of oaa_filter_spectra_kernel (32·kFsCG threads)
 template <int NN, bool XWIN>
-__global__ void __launch_bounds__(256) oaa_filter_spectra_kernel(const FiltSpecParams p) {
-  constexpr int P = 2 * NN - 1, H = NN, ROWS = XWIN ? P : NN, CG = 8;
+__global__ void __launch_bounds__(32 * kFsCG) oaa_filter_spectra_kernel(const FiltSpecParams p) {
+  constexpr int P = 2 * NN - 1, H = NN, ROWS = XWIN ? P : NN, CG = kFsCG;
   extern __shared__ __align__(16) float band[];  // [CG][ROWS][SW]
   const int tid = threadIdx.x;
-  const int kl = tid & 7, grp = tid >> 3;        // channel within group, lane group
+  const int kl = tid % CG, grp = tid / CG;       // channel within group, lane group
   const int f1 = grp % H, tsub = grp / H, nsub = 32 / H;
   const int item = blockIdx.x;
   const int bl = item / p.Td, t1 = item - (item / p.Td) * p.Td;
@@ -1480,7 +1481,7 @@ __global__ void __launch_bounds__(256) oaa_filter_spectra_kernel(const FiltSpecP
     {
       const int lane = tid & 31, warp = tid >> 5;
       const float* base = p.src + ((size_t)b * p.nch + c0) * plane;  // 32-bit offsets below
-      for (int sg = warp; sg < ncg * ROWS; sg += 8) {
+      for (int sg = warp; sg < ncg * ROWS; sg += CG) {
         const int ch = sg / ROWS, rr = sg - (sg / ROWS) * ROWS;
         const int r = r0 + rr;
         const bool rok = r >= 0 && r < p.R;

@@ -127,7 +127,7 @@ cudaError_t launch_filter_spectra_n(const oaa::FiltSpecParams& p, bool xwin, int
   auto k = xwin ? oaa::oaa_filter_spectra_kernel<NN, true> : oaa::oaa_filter_spectra_kernel<NN, false>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  k<<<dim3(items, (p.nch + 7) / 8), 256, smem, s>>>(p);
+  k<<<dim3(items, (p.nch + oaa::kFsCG - 1) / oaa::kFsCG), 32 * oaa::kFsCG, smem, s>>>(p);
   g_launches++;
   return cudaGetLastError();
 }
