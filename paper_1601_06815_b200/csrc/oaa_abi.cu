@@ -289,6 +289,7 @@ constexpr size_t kTcChunkBytes = size_t(1) << 33;  // Xg + D per chunk (8 GB: la
 struct TcPlan {
   bool use;
   int F, T, Kc, RTA, RTB, NB, bc, nchunks;  // K chunks of 32, row tiles of A and B, B tiles per CTA
+  bool b_split;  // B (block spectra) stored pre-split: each B tile is re-read by RTA ≥ 3 M tiles
   size_t ag_b, xg_b, d_b;
 };
 TcPlan plan_tc(int B, int Cin, int Cout, int R, int n) {
@@ -300,14 +301,19 @@ TcPlan plan_tc(int B, int Cin, int Cout, int R, int n) {
   t.T = cdiv(R, n);
   t.Kc = cdiv(2 * ((Cin + 3) & ~3), oaa::kTcK);
   t.RTA = cdiv(2 * Cout, oaa::kTcM);
-  const size_t per_img = sizeof(float) * (size_t)t.F * t.T * t.T * ((size_t)t.Kc * oaa::kTcK + 2 * (size_t)Cout);
+  // measured (AlexNet-like fwd, 4 M tiles): splitting B once in HBM beats re-splitting every
+  // re-read in the GEMM; with ≤ 2 M tiles the halved operand bytes win
+  t.b_split = t.RTA >= 3;
+  if (const char* e = std::getenv("OAA_TC_BSPLIT")) t.b_split = atoi(e) != 0;  // experiment knob
+  const size_t per_img = sizeof(float) * (size_t)t.F * t.T * t.T *
+                         ((t.b_split ? 2 : 1) * (size_t)t.Kc * oaa::kTcK + 2 * (size_t)Cout);
   t.nchunks = (int)std::max<size_t>(1, (B * per_img + kTcChunkBytes - 1) / kTcChunkBytes);
   t.bc = cdiv(B, t.nchunks);
   t.nchunks = cdiv(B, t.bc);
   t.NB = t.bc * t.T * t.T > oaa::kTcM ? 2 : 1;
   t.RTB = cdiv(cdiv(t.bc * t.T * t.T, oaa::kTcM), t.NB) * t.NB;
   t.ag_b = sizeof(float) * (size_t)t.F * t.Kc * 2 * t.RTA * 4096;  // pre-split (hi | lo)
-  t.xg_b = sizeof(float) * (size_t)t.F * t.Kc * t.RTB * 4096;
+  t.xg_b = sizeof(float) * (size_t)t.F * t.Kc * (t.b_split ? 2 : 1) * t.RTB * 4096;
   // Ŷ in the walker layout (oaa_tc.cuh mode 2): tile rows padded to whole walker chunks
   const int TPW = 32 / n;
   t.d_b = sizeof(float) * (size_t)t.F * 2 * Cout * ((size_t)t.bc * t.T * (cdiv(t.T, TPW) * TPW) + 31) / 32 * 32;
@@ -492,8 +498,9 @@ cudaError_t launch_filter_spectra(int n, const oaa::FiltSpecParams& p, bool xwin
 }
 
 cudaError_t launch_bin_gemm(const oaa::BinGemmParams& p, cudaStream_t s) {
-  cudaError_t err = cudaFuncSetAttribute(oaa::oaa_bin_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)oaa::kTcSmem);
+  const bool conv = !(p.a_split && p.b_split);
+  auto k = conv ? oaa::oaa_bin_gemm_kernel<true> : oaa::oaa_bin_gemm_kernel<false>;
+  cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)oaa::kTcSmem);
   if (err != cudaSuccess) return err;
   // persistent: one CTA per SM (512 TMEM columns, 192 KB of stages), tiles strided over them
   const long long ntiles = (long long)cdiv(p.N, oaa::kTcM * p.NB) * cdiv(p.M, oaa::kTcM) * p.F * p.S;
@@ -501,7 +508,7 @@ cudaError_t launch_bin_gemm(const oaa::BinGemmParams& p, cudaStream_t s) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)std::max<long long>(1, std::min<long long>(ntiles, sms));
-  oaa::oaa_bin_gemm_kernel<<<grid, oaa::kTcThreads, oaa::kTcSmem, s>>>(p);
+  k<<<grid, conv ? oaa::tc_threads<true>() : oaa::tc_threads<false>(), oaa::kTcSmem, s>>>(p);
   g_launches++;
   return cudaGetLastError();
 }
@@ -536,6 +543,7 @@ oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* 
   tp.RTB = tc.RTB;
   tp.BW = e.BW;
   tp.CSTR = n * e.BW + 4;
+  tp.split = tc.b_split ? 1 : 0;
   const size_t t1_smem = sizeof(float) * 16 * (size_t)tp.CSTR;
   oaa::BinGemmParams gp{};
   gp.A = Ag;
@@ -550,6 +558,7 @@ oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* 
   gp.kps = tc.Kc;
   gp.mode = 2;  // Ŷ straight into the walker's chunk layout
   gp.a_split = 1;
+  gp.b_split = tc.b_split ? 1 : 0;
   gp.nohi = std::getenv("OAA_TC_NOHI") != nullptr;  // experiment knob
   gp.partial = nullptr;
   gp.Cf = Cout;

@@ -1347,8 +1347,9 @@ __device__ __forceinline__ void tc_put_split(float* Op, int f, int Kc, int RT, i
 // rounded up to 4), zero elsewhere up to 32·Kc; bin f = f1·P + f2 (half spectrum, f1 < n).
 struct TileSpecParams {
   const float* in;  // [B][Cin][R][R]
-  float* Xg;        // blocked [F][Kc][2][RTB][4096]
+  float* Xg;        // blocked [F][Kc][RTB][4096] (split: [F][Kc][hi|lo][RTB][4096])
   int Cin, R, T, b0, bc, Kc, RTB, BW, CSTR;
+  int split;        // write hi / lo (for GEMMs that re-read each B tile for many M tiles)
 };
 
 // One CTA per (image, tile row) of the chunk.  A task is (f1, tile t2, quad of 4
@@ -1418,10 +1419,26 @@ __global__ void __launch_bounds__(128) oaa_tile_spectra_kernel(const TileSpecPar
 #pragma unroll
       for (int f2 = 0; f2 < P; ++f2) {
         const int f = f1 * P + f2;
-        *reinterpret_cast<float4*>(p.Xg + tc_idx(f, p.Kc, p.RTB, bt, cb)) =
-            make_float4(xr[0][f2], xr[1][f2], xr[2][f2], xr[3][f2]);
-        *reinterpret_cast<float4*>(p.Xg + tc_idx(f, p.Kc, p.RTB, bt, Cinp + cb)) =
-            make_float4(xi[0][f2], xi[1][f2], xi[2][f2], xi[3][f2]);
+        const float4 vr = make_float4(xr[0][f2], xr[1][f2], xr[2][f2], xr[3][f2]);
+        const float4 vi = make_float4(xi[0][f2], xi[1][f2], xi[2][f2], xi[3][f2]);
+        if (!p.split) {
+          *reinterpret_cast<float4*>(p.Xg + tc_idx(f, p.Kc, p.RTB, bt, cb)) = vr;
+          *reinterpret_cast<float4*>(p.Xg + tc_idx(f, p.Kc, p.RTB, bt, Cinp + cb)) = vi;
+        } else {
+          auto hi4 = [](float4 v) {
+            return make_float4(__uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u),
+                               __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u),
+                               __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u),
+                               __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u));
+          };
+          const float4 hr = hi4(vr), hi_ = hi4(vi);
+          *reinterpret_cast<float4*>(p.Xg + tc_idx_split(f, p.Kc, p.RTB, 0, bt, cb)) = hr;
+          *reinterpret_cast<float4*>(p.Xg + tc_idx_split(f, p.Kc, p.RTB, 1, bt, cb)) =
+              make_float4(vr.x - hr.x, vr.y - hr.y, vr.z - hr.z, vr.w - hr.w);
+          *reinterpret_cast<float4*>(p.Xg + tc_idx_split(f, p.Kc, p.RTB, 0, bt, Cinp + cb)) = hi_;
+          *reinterpret_cast<float4*>(p.Xg + tc_idx_split(f, p.Kc, p.RTB, 1, bt, Cinp + cb)) =
+              make_float4(vi.x - hi_.x, vi.y - hi_.y, vi.z - hi_.z, vi.w - hi_.w);
+        }
       }
     }
   }
@@ -1432,7 +1449,12 @@ __global__ void __launch_bounds__(128) oaa_tile_spectra_kernel(const TileSpecPar
   for (int e = tid; e < NN * P * p.T * padq; e += nthr) {
     const int qq = e % padq, rest = e / padq;
     const int t2 = rest % p.T, f = rest / p.T;
-    *reinterpret_cast<float4*>(p.Xg + tc_idx(f, p.Kc, p.RTB, bt0 + t2, 2 * Cinp + 4 * qq)) = z;
+    if (!p.split) {
+      *reinterpret_cast<float4*>(p.Xg + tc_idx(f, p.Kc, p.RTB, bt0 + t2, 2 * Cinp + 4 * qq)) = z;
+    } else {
+      *reinterpret_cast<float4*>(p.Xg + tc_idx_split(f, p.Kc, p.RTB, 0, bt0 + t2, 2 * Cinp + 4 * qq)) = z;
+      *reinterpret_cast<float4*>(p.Xg + tc_idx_split(f, p.Kc, p.RTB, 1, bt0 + t2, 2 * Cinp + 4 * qq)) = z;
+    }
   }
 }
 

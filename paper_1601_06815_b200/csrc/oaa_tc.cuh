@@ -58,7 +58,8 @@ struct BinGemmParams {
   //   D[o·plane + (s / 8)·16·F + ri·8·F + f·8 + s % 8],   F = H·P bins,
   // i.e. blocks of 8 slots: every bin's run is one aligned 32-byte sector, and a walker chunk
   // spans one or two blocks
-  int a_split;  // A arrives pre-split ([F][Kc][hi|lo][RTA][4096]); B is always plain fp32
+  int a_split;  // A arrives pre-split ([F][Kc][hi|lo][RTA][4096])
+  int b_split;  // B arrives pre-split likewise (else the converter warps split it)
   int nohi;     // experiment: leave x in the hi slot (relies on the MMA ignoring the low bits)
   int TT, TPW, NT4, SB, SBL;  // SB = 1 << SBL slots per block (8 in the text below)
   long long plane;
@@ -100,13 +101,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t ta, float (&v)[32]) {
 // round-to-nearest FADDs keeps long reductions (the weight gradient's B·T′) at fp32
 // accuracy.
 constexpr int kTcDrain = 8;
-constexpr int kTcThreads = 384;  // warp 0 TMA producer, warp 1 MMA issuer, warps 2..9 drain/epilogue,
-                                 // warps 10, 11 hi/lo converters
+// warp 0 TMA producer, warp 1 MMA issuer, warps 2..9 drain/epilogue, (CONV) warps 10, 11 hi/lo
+// converters.  Without CONV both operands must arrive pre-split.
+template <bool CONV> constexpr int tc_threads() { return CONV ? 384 : 320; }
 
 // D[f][m][n] = Σ_k A[f][m][k] · B[f][n][k]  (3×TF32).  grid = (ceil(N/(128·NB)), ceil(M/128), F·S)
 // Two TMEM accumulators of 256 columns alternate per group of kTcDrain K chunks, so the
 // MMAs of group g+1 run while the epilogue warps drain group g.
-__global__ void __launch_bounds__(kTcThreads, 1) oaa_bin_gemm_kernel(const BinGemmParams p) {
+template <bool CONV>
+__global__ void __launch_bounds__(tc_threads<CONV>(), 1) oaa_bin_gemm_kernel(const BinGemmParams p) {
   // Persistent: CTA b takes output tiles b, b + gridDim.x, ...  (tile order: M tiles of one
   // (bin, N tile) first, so their shared B operand is re-read from L2).  The smem stage ring
   // and the two TMEM accumulators carry on across tiles: the drain warps write tile t while
@@ -117,6 +120,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) oaa_bin_gemm_kernel(const BinGe
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int NB = p.NB, ntile = kTcM * NB;
+  const bool presplit = !CONV;  // (the host launches CONV unless a_split && b_split)
   const int nN = (p.N + ntile - 1) / ntile, nM = (p.M + kTcM - 1) / kTcM;
   const int ntiles = nN * nM * p.F * p.S;
   if (warp == 0) {
@@ -169,12 +173,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) oaa_bin_gemm_kernel(const BinGe
           const int s = gch % kTcStages;
           if (gch >= kTcStages) mbar_wait(&empty[s], ((gch / kTcStages) - 1) & 1);
           unsigned char* st = smem_raw + s * kTcStageBytes;
-          mbar_expect_tx(&full[s], (p.a_split ? 2 : 1) * kBlk + T.nb * kBlk);
+          mbar_expect_tx(&full[s], (p.a_split ? 2 : 1) * kBlk + (p.b_split ? 2 : 1) * T.nb * kBlk);
           const size_t kk = (size_t)T.f * p.Kc + T.kbeg + ch;
           const float* a = p.A + ((p.a_split ? 2 * kk : kk) * p.RTA + T.mt) * 4096;
-          const float* b = p.B + (kk * p.RTB + NB * T.nt) * 4096;
+          const float* b = p.B + ((p.b_split ? 2 * kk : kk) * p.RTB + NB * T.nt) * 4096;
           bulk_g2s(st, a, kBlk, &full[s]);
           if (p.a_split) bulk_g2s(st + kBlk, a + (size_t)p.RTA * 4096, kBlk, &full[s]);
+          if (p.b_split) bulk_g2s(st + 4 * kBlk, b + (size_t)p.RTB * 4096, T.nb * kBlk, &full[s]);
           bulk_g2s(st + 2 * kBlk, b, T.nb * kBlk, &full[s]);
         }
       }
@@ -190,7 +195,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) oaa_bin_gemm_kernel(const BinGe
           const bool first = (ch % kTcDrain) == 0;
           if (first && gg >= 2) mbar_wait(&acce[buf], ((gg >> 1) - 1) & 1);
           const int s = gch % kTcStages;
-          mbar_wait(&conv[s], (gch / kTcStages) & 1);
+          mbar_wait(presplit ? &full[s] : &conv[s], (gch / kTcStages) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t base = smem_u32(smem_raw + s * kTcStageBytes);
           const uint32_t a_hi = base, a_lo = base + kBlk, b_hi = base + 2 * kBlk, b_lo = base + 4 * kBlk;
@@ -212,13 +217,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) oaa_bin_gemm_kernel(const BinGe
         gg0 += groups_of(T.nk);
       }
     }
-  } else if (warp >= 10) {
+  } else if (CONV && warp >= 10) {
     // converters: x → hi (low 13 mantissa bits cleared, in place) and lo = x − hi (the
     // stage's lo slot) for the A block and the nb B blocks; the tensor core reads the
     // stage through the async proxy, hence the proxy fence before the arrive
+    // (both operands pre-split: nothing to do, the MMA waits on "full" directly)
     const int ct = tid - 320;
     int gch = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int t = presplit ? ntiles : blockIdx.x; t < ntiles; t += gridDim.x) {
       const Tile T = tile_of(t);
       for (int ch = 0; ch < T.nk; ++ch, ++gch) {
         const int s = gch % kTcStages;
@@ -228,7 +234,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) oaa_bin_gemm_kernel(const BinGe
         float4* al = reinterpret_cast<float4*>(st + kBlk);
         float4* bh = reinterpret_cast<float4*>(st + 2 * kBlk);
         float4* bl = reinterpret_cast<float4*>(st + 4 * kBlk);
-        const int nb4 = T.nb * 1024;
+        const int nb4 = p.b_split ? 0 : T.nb * 1024;
         auto split4 = [](float4& h, float4& l, float4 x) {
           h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
           h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
