@@ -1473,8 +1473,10 @@ struct FiltSpecParams {
 };
 
 constexpr int kFsCG = 4;  // channels per CTA of oaa_filter_spectra_kernel (32·kFsCG threads)
+// (n ≤ 5: capped at 80 registers for 6 CTAs / SM, AlexNet-like bwd_filter 1.55 → 1.45 ms; n = 8
+// keeps its 165-205 registers: at 80 or 128 the spills cost more than the occupancy gains)
 template <int NN, bool XWIN>
-__global__ void __launch_bounds__(32 * kFsCG) oaa_filter_spectra_kernel(const FiltSpecParams p) {
+__global__ void __launch_bounds__(32 * kFsCG, NN <= 5 ? 6 : 1) oaa_filter_spectra_kernel(const FiltSpecParams p) {
   constexpr int P = 2 * NN - 1, H = NN, ROWS = XWIN ? P : NN, CG = kFsCG;
   extern __shared__ __align__(16) float band[];  // [CG][ROWS][SW]
   const int tid = threadIdx.x;
