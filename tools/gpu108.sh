@@ -1,0 +1,3 @@
+timeout 900 python -m pytest tests -q -m gpu 2>&1 | tail -2
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -1
+timeout 600 python bench.py 2>&1 | tail -1 | cut -c 1-300
