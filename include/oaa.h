@@ -98,9 +98,10 @@ oaa_status_t oaa_conv_bwd_filter(const float* x, const float* dy, float* dw, int
 /* Diagnostic entry point of the tensor-core contraction used for large C·K (SURVEY.md
  * §8(a) a4): D[f] = A[f]·B[f]ᵀ for f < F, A[f] M×Kd, B[f] N×Kd, D[f] M×N, all row-major
  * fp32 device arrays, evaluated with tcgen05 3×TF32 (fp32-accurate).  The operands are
- * first packed (split hi/lo, UMMA-blocked) into the caller's workspace of
- * oaa_debug_bin_gemm_workspace_bytes(F, M, N, Kd) bytes.  Exposed so tests can check
- * the tensor-core kernel in isolation. */
+ * first packed (plain fp32, UMMA-blocked) into the caller's workspace of
+ * oaa_debug_bin_gemm_workspace_bytes(F, M, N, Kd) bytes; the kernel's converter warps
+ * split them into TF32 hi/lo in shared memory.  Exposed so tests can check the
+ * tensor-core kernel in isolation. */
 size_t oaa_debug_bin_gemm_workspace_bytes(int F, int M, int N, int Kd);
 oaa_status_t oaa_debug_bin_gemm(const float* A, const float* B, float* D, int F, int M, int N, int Kd,
                                 void* ws, size_t ws_bytes, void* stream);
