@@ -15,18 +15,22 @@ processes B=128 images).  Prints ONE JSON line (rank 0).
   e2e       the same metric through the public API with PINNED HOST buffers: the
             host→device copies of x, w, dy and the device→host copies of y, dx, dw are
             inside the timed region.
-  roofline  the dominant kernel's algorithmic FLOPs per launch (SURVEY.md §8(d)
-            convention) ÷ its CUDA-event duration inside the timed
-            region, against the fp32 FFMA peak derived in DESIGN.md.
-  cpu_baseline  the CPU float64 oracle (direct definition) on the host cores, on a
-            bounded sample of the same workload.
+  roofline  the dominant kernel (largest per-step CUDA-event time inside the timed
+            region, on its launching stream): its algorithmic work (tools/roofline.py,
+            SURVEY.md §8(d)) ÷ its average launch duration, against the measured peak of
+            the resource that bounds it (T_roof = max(T_HBM, T_ALU, T_TC)).  `ops` gives
+            the same per op and `step_frac` = Σ_op T_roof / ms_per_step.
+  cfg5      BASELINE.json configs[4] as north_star states it: global B = 1024 strong-scaled
+            over the N ranks (B/N each), fwd → bwd_filter → async all_reduce(dW) ∥
+            bwd_data, with the all-reduce time.
+  cpu_baseline  the CPU float64 oracle (direct definition) on the host cores (all and
+            one), on a bounded sample of the same workload.
 --impl reference runs that oracle as the reference arm (rank 0 only).
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import subprocess
 import sys
@@ -36,128 +40,101 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from tools import roofline as rl  # noqa: E402
+
 HEAD = dict(name="headline", B=128, C=3, K=64, N=224, n=8, crop="valid")
+CFG5 = dict(name="sharded", B=1024, C=64, K=128, N=224, n=8, crop="valid")
 METRIC = "OaA conv fwd+bwd images/s at N=224,n=8,C=3,K=64; % of HBM/tensor roofline"
 UNIT = "images/s"
-SM_COUNT = 148
-FP32_LANES_PER_SM = 128
+OPS = ("fwd", "bwd_data", "bwd_filter")
 
 
-def workload_name(w):
-    return f"headline N={w['N']} n={w['n']} C={w['C']} K={w['K']} B={w['B']}/gpu crop={w['crop']}"
-
-
-def out_size(N, n, crop):
-    return {"full": N + n - 1, "valid": N - n + 1, "same": N}[crop]
-
-
-# ------------------------------------------------------------------ roofline terms
-def algorithmic_terms(w):
-    """Per-pass algorithmic work, for one GPU's batch.
-
-    bytes  : 4·(B·C·N² + K·C·n² + B·K·M²)  (each pass reads two of x / w / dy and writes
-             the third; spectra are on-chip intermediates, not counted)
-    flops  : FFT convention 5·P²·log2(P) per real P×P transform, B·(Cin+Cout)·T of them,
-             + contraction 8·Cin·Cout·bins per block, + P² overlap-add adds per output
-             block (T = blocks per channel of the transformed side).
-    """
-    B, C, K, N, n, crop = w["B"], w["C"], w["K"], w["N"], w["n"], w["crop"]
-    M = out_size(N, n, crop)
-    P = 2 * n - 1
-    bins = P * n
-    T = math.ceil(N / n) ** 2
-    Td = math.ceil(M / n) ** 2
-    fft = 5 * P * P * math.log2(P) if P > 1 else 1
-    by = 4 * (B * C * N * N + K * C * n * n + B * K * M * M)
-    fwd = B * (C + K) * T * fft + 8 * K * C * B * T * bins + P * P * B * K * T
-    bwd_data = B * (C + K) * Td * fft + 8 * K * C * B * Td * bins + P * P * B * C * Td
-    bwd_filter = B * (C + K) * Td * fft + 8 * K * C * B * Td * bins
-    return {"bytes": {"fwd": by, "bwd_data": by, "bwd_filter": by},
-            "flops": {"fwd": fwd, "bwd_data": bwd_data, "bwd_filter": bwd_filter}}
-
-
-def measured_peaks():
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return json.load(f), "measured"
-    except Exception:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+def workload_name(w, per_gpu=True):
+    return (f"{w['name']} N={w['N']} n={w['n']} C={w['C']} K={w['K']} B={w['B']}"
+            f"{'/gpu' if per_gpu else ' global'} crop={w['crop']}")
 
 
 # ------------------------------------------------------------------ clocks sampler
 class ClockSampler:
-    def __init__(self, index=0, period_ms=50):
+    """SM clock + throttle reasons sampled every `period_ms` through NVML while the
+    timed region runs (falls back to nvidia-smi -lms)."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, index=0, period_ms=5):
         self.index, self.period_ms = index, period_ms
-        self.proc = None
-        self.lines = []
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
 
     def __enter__(self):
-        cmd = ["nvidia-smi", f"--id={self.index}",
-               "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-               "--format=csv,noheader,nounits", f"-lms={self.period_ms}"]
         try:
-            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            def loop():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for nm, bit in self.REASONS.items():
+                            if r & bit:
+                                self.reasons.add(nm)
+                    except Exception:
+                        pass
+                    time.sleep(self.period_ms / 1e3)
+            self.t = threading.Thread(target=loop, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *a):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self.t is not None:
+            self.t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[4:8]):
-                if v.lower() in ("active", "1", "yes"):
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(s), "source": "NVML every 5 ms during the timed region"}
 
 
 # ------------------------------------------------------------------ CPU oracle timing
-def cpu_oracle_rate(w, budget_s=15.0, max_images=512):
-    """Time the float64 direct oracle (fwd + bwd_data + bwd_filter) on a sub-batch of
-    the workload on all host cores; returns (images/s, cores, sample description)."""
-    import numpy as np
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
+
+def cpu_oracle_rate(w, budget_s=15.0, max_images=512):
+    """The float64 direct oracle (fwd + bwd_data + bwd_filter) on a sub-batch of the
+    workload, on all host cores and on one core."""
     import oracle
     from workloads import make_inputs
     cores = oracle.max_threads()
     d = make_inputs(1, w["C"], w["K"], w["N"], w["n"], w["crop"], seed=7)
     t0 = time.perf_counter()
-    oracle.step_f32(d["x"], d["w"], d["dy"], w["crop"])
-    t1 = time.perf_counter() - t0
-    nb = int(max(1, min(max_images, budget_s / max(t1, 1e-3))))
+    oracle.step_f32(d["x"], d["w"], d["dy"], w["crop"], nthreads=1)
+    t_one = time.perf_counter() - t0
+    nb = int(max(1, min(max_images, budget_s * cores / max(t_one, 1e-3))))
     d = make_inputs(nb, w["C"], w["K"], w["N"], w["n"], w["crop"], seed=8)
     t0 = time.perf_counter()
     oracle.step_f32(d["x"], d["w"], d["dy"], w["crop"])
     dt = time.perf_counter() - t0
-    _ = np
-    return nb / dt, cores, f"{nb} images of the headline shape, fwd+bwd_data+bwd_filter fp64 direct, {dt:.1f} s"
+    return {"value": nb / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{nb} images of the headline shape, fwd+bwd_data+bwd_filter fp64 direct "
+                      f"(oracle/oracle.c, OpenMP), {dt:.1f} s on {cores} threads",
+            "value_1thread": 1.0 / t_one, "sample_1thread": f"1 image on 1 thread, {t_one:.2f} s",
+            "cpu_model": cpu_model(), "os_cpu_count": os.cpu_count()}
 
 
 # ------------------------------------------------------------------ reference arm
@@ -183,14 +160,120 @@ def run_reference(args, w):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded uniform [-1,1))",
             "config": {"workload": workload_name(w) + " (bounded CPU sample)", "images_per_step": per_step},
-            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ------------------------------------------------------------------ our arm
+def _inputs(torch, dev, B, C, K, N, n, crop, seed):
+    """Seeded uniform [-1,1) fp32 drawn on the device (SURVEY.md §8(d) recipe)."""
+    M = rl.out_size(N, n, crop)
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    x = torch.rand((B, C, N, N), generator=g, device=dev).mul_(2).sub_(1)
+    wt = torch.rand((K, C, n, n), generator=torch.Generator(device=dev).manual_seed(777), device=dev).mul_(2).sub_(1)
+    dy = torch.rand((B, K, M, M), generator=g, device=dev).mul_(2).sub_(1)
+    return x, wt, dy
+
+
+class Step:
+    """fwd, then bwd_filter (+ all_reduce(dW) when world > 1) on a side stream concurrent
+    with bwd_data: the two backward convolutions of PAPER.md:89 are independent."""
+
+    def __init__(self, torch, dist, oaa, dev, world, x, wt, dy, N, n, crop):
+        self.t, self.dist, self.oaa, self.world = torch, dist, oaa, world
+        self.x, self.wt, self.dy, self.N, self.n, self.crop = x, wt, dy, N, n, crop
+        B, C = x.shape[:2]
+        K, M = dy.shape[1], dy.shape[-1]
+        self.y = torch.empty((B, K, M, M), device=dev)
+        self.dx = torch.empty_like(x)
+        self.dw = torch.empty_like(wt)
+        self.stream = torch.cuda.current_stream(dev)
+        self.side = torch.cuda.Stream(dev)
+        self.ar_ev = []
+
+    def __call__(self, time_allreduce=False):
+        oaa, t = self.oaa, self.t
+        oaa.conv_fwd(self.x, self.wt, self.crop, out=self.y)
+        self.side.wait_stream(self.stream)
+        oaa.conv_bwd_filter(self.x, self.dy, self.n, self.crop, out=self.dw, stream=self.side)
+        if self.world > 1:
+            with t.cuda.stream(self.side):
+                if time_allreduce:
+                    a, b = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+                    a.record(self.side)
+                self.dist.all_reduce(self.dw)
+                if time_allreduce:
+                    b.record(self.side)
+                    self.ar_ev.append((a, b))
+        oaa.conv_bwd_data(self.dy, self.wt, self.N, self.crop, out=self.dx)
+        self.stream.wait_stream(self.side)
+
+
+def _max_over_ranks(torch, dist, world, dev, v):
+    if world == 1:
+        return v
+    t = torch.tensor([v], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _timed(torch, dist, world, dev, fn, steps, stream):
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    return _max_over_ranks(torch, dist, world, dev, e0.elapsed_time(e1))
+
+
+def run_cfg5(args, torch, dist, oaa, dev, world, rank):
+    """BASELINE configs[4] strong-scaled: global B = 1024 split over the ranks."""
+    w = dict(CFG5)
+    from paper_1601_06815_b200.dist import shard_range
+    a, b = shard_range(w["B"], rank, world)
+    Bl = b - a
+    x, wt, dy = _inputs(torch, dev, Bl, w["C"], w["K"], w["N"], w["n"], w["crop"], seed=4242 + rank)
+    st = Step(torch, dist, oaa, dev, world, x, wt, dy, w["N"], w["n"], w["crop"])
+    for _ in range(3):
+        st()
+    oaa.profile_collect()
+    oaa.profile_enable(True)
+    steps = args.cfg5_steps
+    ms = _timed(torch, dist, world, dev, lambda: st(time_allreduce=True), steps, st.stream)
+    oaa.profile_enable(False)
+    op_ms, op_cnt = oaa.profile_collect()
+    oaa.profile_collect_kernels()
+    ar_ms = None
+    if st.ar_ev:
+        ar_ms = _max_over_ranks(torch, dist, world, dev, sum(e0.elapsed_time(e1) for e0, e1 in st.ar_ev) / len(st.ar_ev))
+    ms_step = ms / steps
+    roof_ms = sum(rl.t_roof(rl.op_work(op, Bl, w["C"], w["K"], w["N"], w["n"], w["crop"]))[0] for op in OPS) * 1e3
+    rec = {"workload": workload_name(w, per_gpu=False), "global_batch": w["B"], "B_per_gpu": Bl, "n_gpus": world,
+           "scaling": "strong", "steps": steps, "warmup": 3, "ms_per_step": ms_step,
+           "value": w["B"] / (ms_step / 1e3), "unit": UNIT,
+           "tflop_eq_per_s": rl.direct_flops(w["B"], w["C"], w["K"], w["N"], w["n"], w["crop"]) / (ms_step / 1e3) / 1e12,
+           "op_ms": {k: op_ms[k] / max(1, op_cnt[k]) for k in op_ms},
+           "allreduce_ms": ar_ms, "allreduce_bytes": 4 * w["K"] * w["C"] * w["n"] ** 2,
+           "t_roof_ms_per_gpu": roof_ms, "step_frac": roof_ms / ms_step,
+           "step": "fwd, then bwd_filter -> async NCCL all_reduce(dW) on a side stream, concurrent with bwd_data"}
+    del st, x, wt, dy
+    torch.cuda.empty_cache()
+    return rec
+
+
 def run_ours(args, w):
+    import datetime
+
     import torch
     import torch.distributed as dist
 
@@ -203,69 +286,79 @@ def run_ours(args, w):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    nccl = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # communicator logging to a file (stdout carries only the JSON line), bounded
+        # collectives, async error handling (torch default TORCH_NCCL_ASYNC_ERROR_HANDLING)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,COLL")
+        os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/oaa_nccl.{os.getpid()}.log")
+        os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "1")
+        dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(minutes=10))
+        nccl = {"backend": dist.get_backend(), "comm_nranks": dist.get_world_size(),
+                "nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
+                "log": os.environ.get("NCCL_DEBUG_FILE")}
 
     B, C, K, N, n, crop = w["B"], w["C"], w["K"], w["N"], w["n"], w["crop"]
-    M = out_size(N, n, crop)
-    # seeded synthetic inputs, one shard per rank (uniform [-1,1))
-    g = torch.Generator(device=dev)
-    g.manual_seed(12345 + rank)
-    x = torch.rand((B, C, N, N), generator=g, device=dev) * 2 - 1
-    wt = torch.rand((K, C, n, n), generator=torch.Generator(device=dev).manual_seed(777), device=dev) * 2 - 1
-    dy = torch.rand((B, K, M, M), generator=g, device=dev) * 2 - 1
-    y = torch.empty((B, K, M, M), device=dev)
-    dx = torch.empty((B, C, N, N), device=dev)
-    dw = torch.empty((K, C, n, n), device=dev)
-    stream = torch.cuda.current_stream(dev)
-
-    side = torch.cuda.Stream(dev)
-
-    def step():
-        # the two backward convolutions are independent: bwd_filter and the
-        # dW all-reduce run on a side stream, concurrent with bwd_data
-        oaa.conv_fwd(x, wt, crop, out=y)
-        side.wait_stream(stream)
-        oaa.conv_bwd_filter(x, dy, n, crop, out=dw, stream=side)
-        if world > 1:
-            with torch.cuda.stream(side):
-                dist.all_reduce(dw)
-        oaa.conv_bwd_data(dy, wt, N, crop, out=dx)
-        stream.wait_stream(side)
+    M = rl.out_size(N, n, crop)
+    x, wt, dy = _inputs(torch, dev, B, C, K, N, n, crop, seed=12345 + rank)
+    st = Step(torch, dist, oaa, dev, world, x, wt, dy, N, n, crop)
+    stream = st.stream
 
     for _ in range(args.warmup):
-        step()
+        st()
     torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    oaa.profile_collect()  # clear
+    oaa.profile_collect()
+    oaa.profile_collect_kernels()  # clear
     oaa.profile_enable(True)
     launches0 = oaa.launch_count()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev1.record(stream)
-        torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
+        ms_total = _timed(torch, dist, world, dev, st, args.steps, stream)
     oaa.profile_enable(False)
     launches = oaa.launch_count() - launches0
-    ms_total = ev0.elapsed_time(ev1)
-    kern_ms, kern_cnt = oaa.profile_collect()
-    if world > 1:
-        t = torch.tensor([ms_total], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
+    op_ms, op_cnt = oaa.profile_collect()
+    k_ms, k_cnt = oaa.profile_collect_kernels()
     ms_step = ms_total / args.steps
     value = world * B * args.steps / (ms_total / 1e3)
 
-    # e2e through the public API from pinned host buffers (paper_1601_06815_b200.pipeline:
+    # ---- roofline: the dominant kernel (largest CUDA-event time per step)
+    per_step = {k: v / args.steps for k, v in k_ms.items()}
+    dom = max(per_step, key=per_step.get)
+    kernel_op = {"walk": "fwd", "xspec": "fwd", "bwdd": "bwd_data", "bwdf": "bwd_filter",
+                 "xspec_win": "bwd_filter", "finalize": "bwd_filter", "spectrum": "fwd"}
+    dom_op = kernel_op.get(dom, "fwd")
+    avg_s = k_ms[dom] / k_cnt[dom] / 1e3
+    per_launch_units = k_cnt[dom] / args.steps  # launches of this kernel per step
+    work = rl.kernel_work(dom, dom_op, B, C, K, N, n, crop)
+    if per_launch_units != 1:
+        work = {q: v / per_launch_units for q, v in work.items()}
+    roofline = rl.roofline_record(work, avg_s)
+    roofline["kernel"] = f"oaa {dom} ({dom_op})"
+    traffic = None
+    try:  # ncu dram bytes of this kernel (one --set full capture, profiles/r02_traffic.json)
+        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
+            traffic = json.load(f)["kernels"][dom]["dram_bytes"]
+    except Exception:
+        pass
+    roofline["traffic"] = traffic
+    roofline["traffic_source"] = "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum, profiles/r02_traffic.json"
+    roofline["kernels_ms_per_step"] = per_step
+    roofline["kernel_share_of_step"] = {k: v / ms_step for k, v in per_step.items()}
+    ops = {}
+    roof_sum = 0.0
+    for op in OPS:
+        T, bound, terms = rl.t_roof(rl.op_work(op, B, C, K, N, n, crop))
+        t = op_ms[op] / max(1, op_cnt[op])
+        roof_sum += T * 1e3
+        ops[op] = {"ms": t, "t_roof_ms": T * 1e3, "bound": bound, "frac": T * 1e3 / t,
+                   "terms_ms": {k: v * 1e3 for k, v in terms.items()}}
+    roofline["ops"] = ops
+    roofline["ops_note"] = ("per-op CUDA-event spans on each op's stream; bwd_data and bwd_filter run "
+                            "concurrently, so their spans overlap")
+    roofline["step_t_roof_ms"] = roof_sum
+    roofline["step_frac"] = roof_sum / ms_step
+
+    # ---- e2e through the public API from pinned host buffers (paper_1601_06815_b200.pipeline:
     # chunked H2D / compute / D2H on three streams; bwd_filter over the whole batch)
     e2e = None
     if not args.no_e2e:
@@ -283,67 +376,33 @@ def run_ours(args, w):
 
         for _ in range(2):
             e2e_step()
-        torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
         ne = max(1, min(args.steps, 5))
-        for _ in range(ne):
-            e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        ems = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([ems], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = _timed(torch, dist, world, dev, e2e_step, ne, stream)
         e2e = {"value": world * B * ne / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": hs.h2d_bytes,
                "d2h_bytes_per_step": hs.d2h_bytes, "chunks": len(hs.chunks)}
+        del hs, hx, hw, hdy, hy, hdx, hdw
 
-    # roofline of the dominant kernel
-    terms = algorithmic_terms(w)
-    # the roofline is reported for the fwd op: the largest op that runs alone in the step
-    # (bwd_data and bwd_filter overlap on two streams, so their event spans are shared)
-    dom = "fwd"
-    avg_ms = kern_ms[dom] / max(1, kern_cnt[dom])
-    peaks, src = measured_peaks()
-    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-    alu_peak = 2 * SM_COUNT * FP32_LANES_PER_SM * sm_mhz * 1e6 / 1e12  # TFLOP/s
-    achieved = terms["flops"][dom] / (avg_ms / 1e3) / 1e12
-    hbm_achieved = terms["bytes"][dom] / (avg_ms / 1e3) / 1e9
-    traffic = None
-    try:  # measured DRAM bytes of this op from the committed ncu capture (profiles/r1_ncu.md)
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
-            traffic = json.load(f)[dom]["op_bytes"]
-    except Exception:
-        pass
-    roofline = {"bound": "alu", "kernel": f"oaa {dom} op (all its launches)", "achieved": achieved,
-                "peak": alu_peak, "unit": "TFLOP/s", "frac": achieved / alu_peak, "traffic": traffic,
-                "traffic_unit": "bytes per launch (ncu dram read+write, profiles/r1_traffic.json)",
-                "algorithmic_bytes": terms["bytes"][dom],
-                "peak_source": f"fp32 FFMA 148 SM x 128 lanes x 2 x {sm_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz, {src})",
-                "hbm_achieved_gbs": hbm_achieved, "hbm_peak_gbs": float(peaks.get("hbm_gbs", 6650.0)),
-                "hbm_frac": hbm_achieved / float(peaks.get("hbm_gbs", 6650.0)),
-                "kernel_ms": {k: kern_ms[k] / max(1, kern_cnt[k]) for k in kern_ms},
-                "kernel_share_of_step": {k: (kern_ms[k] / max(1, kern_cnt[k])) / ms_step for k in kern_ms},
-                "kernel_ms_note": "per-op CUDA-event spans on each op's stream; bwd_data and bwd_filter run concurrently, so their spans overlap"}
+    del st
+    torch.cuda.empty_cache()
+    cfg5 = None
+    if not args.no_cfg5:
+        cfg5 = run_cfg5(args, torch, dist, oaa, dev, world, rank)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        rate, cores, sample = cpu_oracle_rate(w, budget_s=args.cpu_budget)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+        cpu = cpu_oracle_rate(w, budget_s=args.cpu_budget)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded uniform [-1,1), on device)",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded uniform [-1,1), drawn on device)",
                 "config": {"workload": workload_name(w), "B_per_gpu": B, "global_batch": B * world,
                            "C": C, "K": K, "N": N, "n": n, "crop": crop, "P": 2 * n - 1,
                            "parallelism": f"dp{world}", "l2": "inputs exceed L2 (dy+y = 3.1 GB/step)",
                            "step": "fwd, then bwd_filter (+ NCCL all_reduce(dW) if N>1) on a side stream concurrent with bwd_data"},
+                "tflop_eq_per_s": world * rl.direct_flops(B, C, K, N, n, crop) / (ms_step / 1e3) / 1e12,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clk.summary()}
+                "clocks": clk.summary(), "cfg5": cfg5, "nccl": nccl}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -358,6 +417,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cfg5", action="store_true")
+    ap.add_argument("--cfg5-steps", type=int, default=3)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-images", type=int, default=1)
     ap.add_argument("--e2e-chunks", type=int, default=8)

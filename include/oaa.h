@@ -124,6 +124,17 @@ uint64_t oaa_launch_count(void);
 void oaa_profile_enable(int on);
 int oaa_profile_collect(double* ms, int* count);
 
+/* Per-kernel timing (same enable switch): every launch records CUDA events on its
+ * stream, labelled with a kernel id in [0, oaa_profile_kernel_count()).
+ * oaa_profile_collect_kernels synchronises them, writes the summed milliseconds and
+ * launch counts of the first n ids into ms[n] / count[n] (either may be NULL), clears
+ * the record and returns the number of launches collected (−1 on a CUDA error).
+ * oaa_profile_kernel_name(id) is a static name ("walk", "bwdd", "bin_gemm", ...), NULL
+ * for an unknown id. */
+int oaa_profile_kernel_count(void);
+const char* oaa_profile_kernel_name(int id);
+int oaa_profile_collect_kernels(double* ms, int* count, int n);
+
 #ifdef __cplusplus
 }
 #endif

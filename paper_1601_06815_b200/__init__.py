@@ -25,6 +25,7 @@ import torch
 __all__ = [
     "conv_fwd", "conv_bwd_data", "conv_bwd_filter", "out_size", "workspace_bytes", "lib",
     "OaAConv2dFunction", "OaAConv2d", "launch_count", "profile_enable", "profile_collect",
+    "profile_collect_kernels",
     "CROPS", "OP_FWD", "OP_BWD_DATA", "OP_BWD_FILTER", "OaAError",
 ]
 
@@ -75,6 +76,12 @@ def lib():
             L.oaa_profile_enable.restype = None
             L.oaa_profile_collect.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]
             L.oaa_profile_collect.restype = I
+            L.oaa_profile_kernel_count.argtypes = []
+            L.oaa_profile_kernel_count.restype = I
+            L.oaa_profile_kernel_name.argtypes = [I]
+            L.oaa_profile_kernel_name.restype = ctypes.c_char_p
+            L.oaa_profile_collect_kernels.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int), I]
+            L.oaa_profile_collect_kernels.restype = I
             _lib = L
     return _lib
 
@@ -107,10 +114,14 @@ _ws_cache: dict = {}
 
 
 def _workspace(nbytes: int, device: torch.device, stream: torch.cuda.Stream) -> torch.Tensor:
+    """Per-(device, stream) cached workspace, allocated ON `stream` so the caching
+    allocator orders its reuse after the kernels that stream runs on it."""
     key = (device.index, stream.cuda_stream)
     ws = _ws_cache.get(key)
     if ws is None or ws.numel() < nbytes:
-        ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        _ws_cache.pop(key, None)  # freed on `stream`: reused only after its kernels
+        with torch.cuda.stream(stream):
+            ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
         _ws_cache[key] = ws
     return ws
 
@@ -134,6 +145,12 @@ def _call(fn, a, b, out, dims, crop, op, stream):
     s = stream if stream is not None else torch.cuda.current_stream(dev)
     nbytes = workspace_bytes(op, B, C, K, N, n, crop)
     ws = _workspace(nbytes, dev, s)
+    if s != torch.cuda.current_stream(dev):
+        # the kernels run on `s`, the tensors were allocated on the current stream: tell
+        # the caching allocator, so a block freed early is not handed out while `s` still
+        # reads or writes it
+        for t in (a, b, out):
+            t.record_stream(s)
     st = fn(ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()),
             ctypes.c_void_p(out.data_ptr()), B, C, K, N, n, _crop_id(crop),
             ctypes.c_void_p(ws.data_ptr()), ctypes.c_size_t(ws.numel()), ctypes.c_void_p(s.cuda_stream))
@@ -249,6 +266,19 @@ def profile_collect():
         raise OaAError("oaa_profile_collect: CUDA error")
     names = ("fwd", "bwd_data", "bwd_filter")
     return {k: ms[i] for i, k in enumerate(names)}, {k: cnt[i] for i, k in enumerate(names)}
+
+
+def profile_collect_kernels():
+    """Summed milliseconds and launch counts per kernel since the last collect:
+    ({'walk': ms, ...}, {'walk': count, ...}), only kernels that ran."""
+    L = lib()
+    n = L.oaa_profile_kernel_count()
+    ms = (ctypes.c_double * n)()
+    cnt = (ctypes.c_int * n)()
+    if L.oaa_profile_collect_kernels(ms, cnt, n) < 0:
+        raise OaAError("oaa_profile_collect_kernels: CUDA error")
+    names = [L.oaa_profile_kernel_name(i).decode() for i in range(n)]
+    return ({names[i]: ms[i] for i in range(n) if cnt[i]}, {names[i]: cnt[i] for i in range(n) if cnt[i]})
 
 
 # --------------------------------------------------------------------- autograd

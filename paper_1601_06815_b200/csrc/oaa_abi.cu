@@ -47,6 +47,13 @@ cudaEvent_t get_event() {
   return e;
 }
 
+// per-kernel records (KTimer, oaa_launch.cuh)
+struct KRec {
+  int kid;
+  cudaEvent_t a, b;
+};
+std::vector<KRec> g_kprof;
+
 struct ProfScope {
   int op;
   cudaStream_t s;
@@ -69,6 +76,26 @@ struct ProfScope {
   }
 };
 
+}  // namespace
+
+namespace oaa_host {
+KTimer::KTimer(int kid_, cudaStream_t s_) : kid(kid_), s(s_), a(nullptr) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  if (!g_prof_on) return;
+  cudaEvent_t e = get_event();
+  cudaEventRecord(e, s);
+  a = e;
+}
+KTimer::~KTimer() {
+  if (!a) return;
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  cudaEvent_t e = get_event();
+  cudaEventRecord(e, s);
+  g_kprof.push_back({kid, static_cast<cudaEvent_t>(a), e});
+}
+}  // namespace oaa_host
+
+namespace {
 // ---------------------------------------------------------------- geometry
 struct Geo {
   int n, P, H, M, o;
@@ -304,7 +331,6 @@ TcPlan plan_tc(int B, int Cin, int Cout, int R, int n) {
   // measured (AlexNet-like fwd, 4 M tiles): splitting B once in HBM beats re-splitting every
   // re-read in the GEMM; with ≤ 2 M tiles the halved operand bytes win
   t.b_split = t.RTA >= 3;
-  if (const char* e = std::getenv("OAA_TC_BSPLIT")) t.b_split = atoi(e) != 0;  // experiment knob
   const size_t per_img = sizeof(float) * (size_t)t.F * t.T * t.T *
                          ((t.b_split ? 2 : 1) * (size_t)t.Kc * oaa::kTcK + 2 * (size_t)Cout);
   t.nchunks = (int)std::max<size_t>(1, (B * per_img + kTcChunkBytes - 1) / kTcChunkBytes);
@@ -329,7 +355,7 @@ struct WalkHostGeo {
 };
 WalkHostGeo plan_walk(bool is_fwd, int B, int Cin, int Cout, int T, int Ro, int off, int n, const TcPlan& tc) {
   WalkHostGeo w{};
-  w.use = is_fwd && !tc.use && Cin <= kWalkMaxCin && std::getenv("OAA_NO_WALK") == nullptr;
+  w.use = is_fwd && !tc.use && Cin <= kWalkMaxCin;
   const int H = n;
   w.TPW = 32 / H;
   w.CW = w.TPW * n;
@@ -351,7 +377,7 @@ struct BwddPlan {
 };
 BwddPlan plan_bwdd(bool is_fwd, int Cout, int R, int n, const TcPlan& tc) {
   BwddPlan d{};
-  d.use = !is_fwd && !tc.use && Cout <= kWalkMaxCin && std::getenv("OAA_NO_BWDD") == nullptr;
+  d.use = !is_fwd && !tc.use && Cout <= kWalkMaxCin;
   const int H = n, P = 2 * n - 1, TPW = 32 / H, CW = TPW * n;
   const int Td = cdiv(R, n);
   d.NCW = cdiv(Td, TPW);
@@ -371,7 +397,7 @@ struct BwdfPlan {
 };
 BwdfPlan plan_bwdf(int B, int C, int K, int M, int n) {
   BwdfPlan f{};
-  f.use = C <= kWalkMaxCin && std::getenv("OAA_NO_BWDF") == nullptr && B > 0;
+  f.use = C <= kWalkMaxCin && B > 0;
   const int H = n, P = 2 * n - 1;
   f.TPW = 32 / H;
   f.CW = f.TPW * n;
@@ -383,9 +409,8 @@ BwdfPlan plan_bwdf(int B, int C, int K, int M, int n) {
   // balanced kernel groups: each CTA takes ⌈K / nkg⌉ kernels rounded up to whole warps
   f.nwb = cdiv(cdiv(K, f.nkg), f.KPW);
   f.KG = f.nwb * f.KPW;
-  f.tm = std::getenv("OAA_BWDF_REG") == nullptr;  // TMEM accumulators, 2 CTAs / SM
+  f.tm = true;  // TMEM accumulators, 2 CTAs / SM (measured faster than registers)
   int slots = f.tm ? 296 : 148;
-  if (const char* e = std::getenv("OAA_BWDF_SLOTS")) slots = std::max(1, atoi(e));  // experiment knob
   f.G = std::max(1, std::min(B * f.Td, slots / f.nkg));
   f.SW = cdiv(f.NCH * f.CW + n - 1, 4) * 4;
   f.xs_b = align_up(sizeof(float4) * (size_t)B * f.Td * f.NCH * C * f.CH4);
@@ -508,7 +533,10 @@ cudaError_t launch_bin_gemm(const oaa::BinGemmParams& p, cudaStream_t s) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)std::max<long long>(1, std::min<long long>(ntiles, sms));
-  k<<<grid, conv ? oaa::tc_threads<true>() : oaa::tc_threads<false>(), oaa::kTcSmem, s>>>(p);
+  {
+    KTimer kt(KID_BIN_GEMM, s);
+    k<<<grid, conv ? oaa::tc_threads<true>() : oaa::tc_threads<false>(), oaa::kTcSmem, s>>>(p);
+  }
   g_launches++;
   return cudaGetLastError();
 }
@@ -529,6 +557,7 @@ oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* 
     const long long total = (long long)tc.F * Cin * Cout;
     const int thr = 256;
     const int blocks = (int)std::min<long long>((total + thr - 1) / thr, 8192);
+    KTimer kt(KID_SPECTRUM, s);
     oaa::oaa_realified_spectrum_kernel<<<blocks, thr, 0, s>>>(w, Ag, K, C, n, is_fwd ? 0 : 1, tc.Kc, tc.RTA);
     g_launches++;
     if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
@@ -559,7 +588,6 @@ oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* 
   gp.mode = 2;  // Ŷ straight into the walker's chunk layout
   gp.a_split = 1;
   gp.b_split = tc.b_split ? 1 : 0;
-  gp.nohi = std::getenv("OAA_TC_NOHI") != nullptr;  // experiment knob
   gp.partial = nullptr;
   gp.Cf = Cout;
   gp.H = n;
@@ -568,7 +596,6 @@ oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* 
   gp.TPW = 32 / n;
   gp.NT4 = cdiv(T, gp.TPW);
   gp.SBL = 5;
-  if (const char* e = std::getenv("OAA_SBL")) gp.SBL = std::max(0, std::min(5, atoi(e)));  // experiment knob
   gp.SB = 1 << gp.SBL;
   gp.NB = tc.NB;
   gp.Kuse = tc.Kc;
@@ -637,7 +664,8 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
   EngineWs L = engine_ws(B, C, K, e.T, g, tc, &wk, &bd);
   if (!ws || ws_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0)
     return OAA_ERR_WORKSPACE;
-  if (overlaps(ws, L.total, out, out_bytes) || overlaps(ws, L.total, in, in_bytes))
+  if (overlaps(ws, L.total, out, out_bytes) || overlaps(ws, L.total, in, in_bytes) ||
+      overlaps(ws, L.total, w, w_bytes))
     return OAA_ERR_INVALID_VALUE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   char* base = static_cast<char*>(ws);
@@ -654,6 +682,7 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
       const long total = (long)K * C * ((g.P + 1) / 2) * g.H;
       const int thr = 256;
       const int blocks = (int)std::min<long>((total + thr - 1) / thr, 4096);
+      KTimer kt(KID_SPECTRUM, s);
       oaa::oaa_spectrum_kernel<<<blocks, thr, 0, s>>>(w, spec, K, C, n, 1, 1);
       g_launches++;
       if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
@@ -679,6 +708,7 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
       const long total = (long)K * C * ((g.P + 1) / 2) * g.H;
       const int thr = 256;
       const int blocks = (int)std::min<long>((total + thr - 1) / thr, 4096);
+      KTimer kt(KID_SPECTRUM, s);
       oaa::oaa_spectrum_kernel<<<blocks, thr, 0, s>>>(w, spec, K, C, n, 0, 1);
       g_launches++;
       if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
@@ -727,6 +757,7 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
     const long total = (long)K * C * ((g.P + 1) / 2) * g.H;
     const int thr = 256;
     const int blocks = (int)std::min<long>((total + thr - 1) / thr, 4096);
+    KTimer kt(KID_SPECTRUM, s);
     oaa::oaa_spectrum_kernel<<<blocks, thr, 0, s>>>(w, spec, K, C, n, is_fwd ? 0 : 1, loop_is_k);
     g_launches++;
     if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
@@ -779,7 +810,7 @@ oaa_status_t run_filter_tc(const float* x, const float* dy, float* dw, int B, in
   const size_t smem_x = sizeof(float) * oaa::kFsCG * (2 * n - 1) * (size_t)t.SWx;
   oaa::BinGemmParams gp{};
   gp.A = Ga; gp.B = Xb; gp.D = nullptr; gp.F = t.F; gp.M = K; gp.N = 2 * C; gp.Kc = t.Kc; gp.RTA = t.RTA;
-  gp.RTB = t.RTB; gp.ldd = 0; gp.strideD = 0; gp.S = t.S; gp.kps = t.kps; gp.mode = 1; gp.a_split = 0; gp.nohi = std::getenv("OAA_TC_NOHI") != nullptr; gp.Cf = C; gp.H = n;
+  gp.RTB = t.RTB; gp.ldd = 0; gp.strideD = 0; gp.S = t.S; gp.kps = t.kps; gp.mode = 1; gp.a_split = 0; gp.Cf = C; gp.H = n;
   gp.P = 2 * n - 1; gp.partial = part; gp.NB = t.NB;
   ProfScope prof(OAA_OP_BWD_FILTER, s);
   prof.start();
@@ -794,6 +825,7 @@ oaa_status_t run_filter_tc(const float* x, const float* dy, float* dw, int B, in
     const int j0 = 2 * bc * t.T2;
     gp.Kuse = cdiv(j0, oaa::kTcK);
     if (j0 < 32 * gp.Kuse) {
+      KTimer kt(KID_AUX, s);
       oaa::oaa_tc_zero_tail_kernel<<<512, 256, 0, s>>>(Ga, t.F, t.Kc, t.RTA, j0, 32 * gp.Kuse);
       oaa::oaa_tc_zero_tail_kernel<<<512, 256, 0, s>>>(Xb, t.F, t.Kc, t.RTB, j0, 32 * gp.Kuse);
       g_launches += 2;
@@ -805,8 +837,11 @@ oaa_status_t run_filter_tc(const float* x, const float* dy, float* dw, int B, in
   }
   prof.stop();
   const int bins = g.P * g.H;
-  oaa::oaa_filter_finalize_kernel<<<K * C, 128, sizeof(double2) * bins, s>>>(
-      reinterpret_cast<const float2*>(part), dw, t.G, K, C, n);
+  {
+    KTimer kt(KID_FINALIZE, s);
+    oaa::oaa_filter_finalize_kernel<<<K * C, 128, sizeof(double2) * bins, s>>>(
+        reinterpret_cast<const float2*>(part), dw, t.G, K, C, n);
+  }
   g_launches++;
   return cudaGetLastError() == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
 }
@@ -873,7 +908,8 @@ oaa_status_t oaa_conv_bwd_filter(const float* x, const float* dy, float* dw, int
   const size_t dw_bytes = sizeof(float) * (size_t)K * C * n * n;
   if (overlaps(dw, dw_bytes, x, x_bytes) || overlaps(dw, dw_bytes, dy, dy_bytes))
     return OAA_ERR_INVALID_VALUE;
-  if (cdiv(g.M, n) * n > 4096) return OAA_ERR_UNSUPPORTED;
+  // the documented v1 limit (include/oaa.h): max(ceil(N/n)·n, M) ≤ 256, as for the forward
+  if (std::max(cdiv(N, n) * n, g.M) > oaa::kMaxThreads) return OAA_ERR_UNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (B == 0) {
     if (cudaMemsetAsync(dw, 0, dw_bytes, s) != cudaSuccess) return OAA_ERR_CUDA;
@@ -914,7 +950,10 @@ oaa_status_t oaa_conv_bwd_filter(const float* x, const float* dy, float* dw, int
     cudaError_t err = launch_bwdf(n, xp, fp, BwdfLaunch{bf.xspec_smem, bf.smem, bf.nkg, bf.tm}, s);
     prof.stop();
     if (err != cudaSuccess) return OAA_ERR_CUDA;
-    oaa::oaa_filter_finalize_kernel<<<K * C, 128, sizeof(double2) * g.P * g.H, s>>>(fp.partial, dw, bf.G, K, C, n);
+    {
+      KTimer kt(KID_FINALIZE, s);
+      oaa::oaa_filter_finalize_kernel<<<K * C, 128, sizeof(double2) * g.P * g.H, s>>>(fp.partial, dw, bf.G, K, C, n);
+    }
     g_launches++;
     return cudaGetLastError() == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
   }
@@ -948,8 +987,11 @@ oaa_status_t oaa_conv_bwd_filter(const float* x, const float* dy, float* dw, int
   prof.stop();
   if (err != cudaSuccess) return OAA_ERR_CUDA;
   const int bins = g.P * g.H;
-  oaa::oaa_filter_finalize_kernel<<<K * C, 128, sizeof(double2) * bins, s>>>(
-      static_cast<const float2*>(ws), dw, f.G, K, C, n);
+  {
+    KTimer kt(KID_FINALIZE, s);
+    oaa::oaa_filter_finalize_kernel<<<K * C, 128, sizeof(double2) * bins, s>>>(
+        static_cast<const float2*>(ws), dw, f.G, K, C, n);
+  }
   g_launches++;
   if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
   return OAA_OK;
@@ -994,6 +1036,44 @@ oaa_status_t oaa_debug_bin_gemm(const float* A, const float* B, float* D, int F,
   if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
   p.A = Ap; p.B = Bp; p.D = D;
   return launch_bin_gemm(p, s) == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
+}
+
+static const char* const kKernelNames[KID_COUNT] = {
+    "spectrum", "xspec", "walk", "bwdd", "xspec_win", "bwdf", "finalize",
+    "tile_spectra", "bin_gemm", "walk_load", "filter_spectra", "engine", "aux"};
+
+int oaa_profile_kernel_count(void) { return KID_COUNT; }
+
+const char* oaa_profile_kernel_name(int id) { return (id >= 0 && id < KID_COUNT) ? kKernelNames[id] : nullptr; }
+
+int oaa_profile_collect_kernels(double* ms, int* count, int n) {
+  std::vector<KRec> recs;
+  {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    recs.swap(g_kprof);
+  }
+  for (int i = 0; i < n; ++i) {
+    if (ms) ms[i] = 0.0;
+    if (count) count[i] = 0;
+  }
+  int bad = 0;
+  for (auto& r : recs) {
+    if (cudaEventSynchronize(r.b) != cudaSuccess) bad = 1;
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) bad = 1;
+    if (r.kid >= 0 && r.kid < n) {
+      if (ms) ms[r.kid] += t;
+      if (count) count[r.kid] += 1;
+    }
+  }
+  {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    for (auto& r : recs) {
+      g_event_pool.push_back(r.a);
+      g_event_pool.push_back(r.b);
+    }
+  }
+  return bad ? -1 : (int)recs.size();
 }
 
 const char* oaa_version(void) { return "oaa-b200 0.1.0 sm_100a"; }

@@ -18,6 +18,32 @@ namespace oaa_host {
 
 extern std::atomic<uint64_t> g_launches;
 
+// Per-kernel timing for the roofline report (oaa_profile_collect_kernels): when profiling
+// is enabled, a KTimer records CUDA events on the launching stream around one launch.
+enum KernelId : int {
+  KID_SPECTRUM = 0,   // kernel spectra Ŵ (a1)
+  KID_XSPEC,          // fwd block spectra X̂ (a2 + a3)
+  KID_WALK,           // fwd walker: contraction + inverse DFT + overlap-add (a4-a6)
+  KID_BWDD,           // bwd_data (a7)
+  KID_XSPEC_WIN,      // bwd_filter x-window spectra Ξ̂ (a8)
+  KID_BWDF,           // bwd_filter dy-block spectra + accumulation (a8)
+  KID_FINALIZE,       // bwd_filter fp64 sum + inverse DFT + lag read-out (a8)
+  KID_TILE_SPECTRA,   // tensor-core path: tile spectra operand (a2 + a3)
+  KID_BIN_GEMM,       // tensor-core path: per-bin 3×TF32 contraction (a4)
+  KID_WALK_LOAD,      // tensor-core path: inverse DFT + overlap-add of Ŷ (a5 + a6)
+  KID_FILTER_SPECTRA, // tensor-core path: bwd_filter operand spectra (a8)
+  KID_ENGINE,         // first-generation flag engine (shapes outside the other kernels)
+  KID_AUX,            // memsets, zero tails, packing
+  KID_COUNT
+};
+struct KTimer {
+  int kid;
+  cudaStream_t s;
+  void* a;
+  KTimer(int kid_, cudaStream_t s_);
+  ~KTimer();
+};
+
 struct EnginePlan {
   int R, Ro, off, T, Cin, Cout, TS, BW, nthreads, ncomp, CR, CIG;
   bool S1;
@@ -41,7 +67,10 @@ cudaError_t launch_engine_t(const oaa::EngineParams& p, const EnginePlan& e, cud
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, e.nthreads, e.smem);
   per_sm = std::max(1, per_sm);
   const int grid = std::max(1, std::min(p.num_items, sms * per_sm));
-  k<<<grid, e.nthreads, e.smem, s>>>(p);
+  {
+    KTimer kt(KID_ENGINE, s);
+    k<<<grid, e.nthreads, e.smem, s>>>(p);
+  }
   g_launches++;
   return cudaGetLastError();
 }
@@ -64,9 +93,10 @@ cudaError_t launch_engine_s1t_t(const oaa::EngineParams& p, const EnginePlan& e,
   per_sm = std::max(1, std::max(per_sm, 2));
   per_sm = std::min(per_sm, 512 / oaa::s1t_alloc_cols(NN, LY ? 0 : CR));
   const int grid = std::max(1, std::min(p.num_items, sms * per_sm));
-  if (std::getenv("OAA_DEBUG"))
-    std::fprintf(stderr, "oaa s1t<%d,%d,%d>: threads %d smem %zu per_sm %d grid %d\n", NN, CR, (int)LY, e.nthreads, e.smem, per_sm, grid);
-  k<<<grid, e.nthreads, e.smem, s>>>(p);
+  {
+    KTimer kt(KID_ENGINE, s);
+    k<<<grid, e.nthreads, e.smem, s>>>(p);
+  }
   g_launches++;
   return cudaGetLastError();
 }
@@ -97,7 +127,10 @@ cudaError_t launch_filter_t(const oaa::FilterParams& p, const FilterPlan& f, cud
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem);
   if (err != cudaSuccess) return err;
   dim3 grid(f.G, f.nkg);
-  k<<<grid, f.nthreads, f.smem, s>>>(p);
+  {
+    KTimer kt(KID_BWDF, s);
+    k<<<grid, f.nthreads, f.smem, s>>>(p);
+  }
   g_launches++;
   return cudaGetLastError();
 }
@@ -117,7 +150,10 @@ cudaError_t launch_tile_spectra_n(const oaa::TileSpecParams& p, size_t smem, cud
   auto k = oaa::oaa_tile_spectra_kernel<NN>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  k<<<dim3(p.bc * p.T, (((p.Cin + 3) & ~3) + 15) / 16), 128, smem, s>>>(p);
+  {
+    KTimer kt(KID_TILE_SPECTRA, s);
+    k<<<dim3(p.bc * p.T, (((p.Cin + 3) & ~3) + 15) / 16), 128, smem, s>>>(p);
+  }
   g_launches++;
   return cudaGetLastError();
 }
@@ -127,7 +163,10 @@ cudaError_t launch_filter_spectra_n(const oaa::FiltSpecParams& p, bool xwin, int
   auto k = xwin ? oaa::oaa_filter_spectra_kernel<NN, true> : oaa::oaa_filter_spectra_kernel<NN, false>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  k<<<dim3(items, (p.nch + oaa::kFsCG - 1) / oaa::kFsCG), 32 * oaa::kFsCG, smem, s>>>(p);
+  {
+    KTimer kt(KID_FILTER_SPECTRA, s);
+    k<<<dim3(items, (p.nch + oaa::kFsCG - 1) / oaa::kFsCG), 32 * oaa::kFsCG, smem, s>>>(p);
+  }
   g_launches++;
   return cudaGetLastError();
 }
@@ -145,7 +184,10 @@ cudaError_t launch_walk_n(const oaa::XSpecParams& xp, const oaa::WalkParams& wp,
     auto k = oaa::oaa_xspec_kernel<NN, false>;
     cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w.xspec_smem);
     if (err != cudaSuccess) return err;
-    k<<<wp.B * wp.T, 256, w.xspec_smem, s>>>(xp);
+    {
+      KTimer kt(KID_XSPEC, s);
+      k<<<wp.B * wp.T, 256, w.xspec_smem, s>>>(xp);
+    }
     g_launches++;
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
   }
@@ -153,21 +195,27 @@ cudaError_t launch_walk_n(const oaa::XSpecParams& xp, const oaa::WalkParams& wp,
          : cr == 3 ? oaa::oaa_walk_kernel<NN, 3> : oaa::oaa_walk_kernel<NN, 4>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w.walk_smem);
   if (err != cudaSuccess) return err;
-  k<<<wp.B * w.ngrp, 32 * w.KG, w.walk_smem, s>>>(wp);
+  {
+    KTimer kt(KID_WALK, s);
+    k<<<wp.B * w.ngrp, 32 * w.KG, w.walk_smem, s>>>(wp);
+  }
   g_launches++;
   return cudaGetLastError();
 }
 
 template <int NN>
 cudaError_t launch_bwdd_n(const oaa::BwdDParams& p, int cr, size_t smem, cudaStream_t s) {
-  const bool tm = std::getenv("OAA_BWDD_REG") == nullptr && smem <= 110 * 1024;
+  const bool tm = smem <= 110 * 1024;  // TMEM accumulators whenever 2 CTAs fit an SM
   auto k = tm ? (cr <= 1 ? oaa::oaa_bwdd_kernel<NN, 1, true> : cr == 2 ? oaa::oaa_bwdd_kernel<NN, 2, true>
                  : cr == 3 ? oaa::oaa_bwdd_kernel<NN, 3, true> : oaa::oaa_bwdd_kernel<NN, 4, true>)
               : (cr <= 1 ? oaa::oaa_bwdd_kernel<NN, 1, false> : cr == 2 ? oaa::oaa_bwdd_kernel<NN, 2, false>
                  : cr == 3 ? oaa::oaa_bwdd_kernel<NN, 3, false> : oaa::oaa_bwdd_kernel<NN, 4, false>);
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  k<<<p.B * p.Td, 32 * (p.NCW == 7 ? 8 : p.NCW), smem, s>>>(p);
+  {
+    KTimer kt(KID_BWDD, s);
+    k<<<p.B * p.Td, 32 * (p.NCW == 7 ? 8 : p.NCW), smem, s>>>(p);
+  }
   g_launches++;
   return cudaGetLastError();
 }
@@ -179,7 +227,10 @@ cudaError_t launch_bwdf_n(const oaa::XSpecParams& xp, const oaa::BwdFParams& p, 
     auto k = oaa::oaa_xspec_kernel<NN, true>;
     cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsmem);
     if (err != cudaSuccess) return err;
-    k<<<p.B * p.Td, 256, xsmem, s>>>(xp);
+    {
+      KTimer kt(KID_XSPEC_WIN, s);
+      k<<<p.B * p.Td, 256, xsmem, s>>>(xp);
+    }
     g_launches++;
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
   }
@@ -189,7 +240,10 @@ cudaError_t launch_bwdf_n(const oaa::XSpecParams& xp, const oaa::BwdFParams& p, 
                 : p.C == 3 ? oaa::oaa_bwdf_kernel<NN, 3, false> : oaa::oaa_bwdf_kernel<NN, 4, false>);
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  k<<<dim3(p.G, nkg), 32 * (p.KG / (32 / NN)), smem, s>>>(p);
+  {
+    KTimer kt(KID_BWDF, s);
+    k<<<dim3(p.G, nkg), 32 * (p.KG / (32 / NN)), smem, s>>>(p);
+  }
   g_launches++;
   return cudaGetLastError();
 }
@@ -199,7 +253,10 @@ cudaError_t launch_walk_load_n(const oaa::WalkParams& wp, size_t smem, int nimg,
   auto k = oaa::oaa_walk_kernel<NN, 1, true>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  k<<<nimg * wp.ngrp, 32 * wp.KG, smem, s>>>(wp);
+  {
+    KTimer kt(KID_WALK_LOAD, s);
+    k<<<nimg * wp.ngrp, 32 * wp.KG, smem, s>>>(wp);
+  }
   g_launches++;
   return cudaGetLastError();
 }

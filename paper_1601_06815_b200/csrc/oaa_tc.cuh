@@ -60,7 +60,6 @@ struct BinGemmParams {
   // spans one or two blocks
   int a_split;  // A arrives pre-split ([F][Kc][hi|lo][RTA][4096])
   int b_split;  // B arrives pre-split likewise (else the converter warps split it)
-  int nohi;     // experiment: leave x in the hi slot (relies on the MMA ignoring the low bits)
   int TT, TPW, NT4, SB, SBL;  // SB = 1 << SBL slots per block (8 in the text below)
   long long plane;
 };
@@ -247,7 +246,7 @@ __global__ void __launch_bounds__(tc_threads<CONV>(), 1) oaa_bin_gemm_kernel(con
           for (int e = ct; e < 1024; e += 64) {
             float4 h, l;
             split4(h, l, ah[e]);
-            if (!p.nohi) ah[e] = h;
+            ah[e] = h;
             al[e] = l;
           }
         }
@@ -255,7 +254,7 @@ __global__ void __launch_bounds__(tc_threads<CONV>(), 1) oaa_bin_gemm_kernel(con
         for (int e = ct; e < nb4; e += 64) {
           float4 h, l;
           split4(h, l, bh[e]);
-          if (!p.nohi) bh[e] = h;
+          bh[e] = h;
           bl[e] = l;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -288,33 +288,6 @@ def _full_size(cfg, crop="valid", n_samples=1500, n_dw=48, seed=0, sub_b=None):
     _adjoint(y, dy, x, dx, w, dw)
 
 
-def test_headline_full_size():
-    """BASELINE config 2 at full size, in the launch configuration bench.py times."""
-    _full_size(CONFIGS["headline"])
-
-
-@pytest.mark.parametrize("crop", ["full", "same"])
-def test_headline_other_crops(crop):
-    _full_size(CONFIGS["headline"], crop=crop, n_samples=600, n_dw=64, seed=1)
-
-
-def test_alexnet_full_size():
-    _full_size(CONFIGS["alexnet"], n_samples=800, n_dw=50, seed=2)
-
-
-@pytest.mark.parametrize("wl", SWEEP, ids=lambda w: w.name)
-def test_sweep_point(wl):
-    _full_size(wl, n_samples=300, n_dw=2 * wl.n * wl.n, seed=3)
-
-
-@pytest.mark.slow
-def test_sharded_config_one_gpu_shard():
-    """BASELINE config 5 per-GPU shard at G=8 (B=128 of the global 1024)."""
-    c = CONFIGS["sharded"]
-    from workloads import Workload
-    _full_size(Workload("sharded_shard", B=128, C=c.C, K=c.K, N=c.N, n=c.n), n_samples=400, n_dw=64, seed=4)
-
-
 def test_host_pipeline_matches_device_calls():
     """pipeline.HostStep (chunked H2D/compute/D2H) gives the same results as the plain
     device calls, bitwise (same kernels, same per-image work)."""
