@@ -30,6 +30,9 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Shares nothing with the CUDA
   (2n−1)² x-windows that overlap them, sums the products in frequency, inverse
   transforms and reads the lags (n−1−u, n−1−v).
 
+* ``oas_conv_fwd`` -- overlap-and-save (textbook segments + circular
+  convolution + discarded aliased samples), the reference for the OaS forward variant.
+
 * ``fft_conv_fwd`` -- "FFTconv", whole-array Hadamard product at next_pow2(N+n−1)
   (SPEC.md:211-214), the third independent implementation.
 
@@ -234,6 +237,59 @@ def oaa_conv_bwd_filter(x, dy, n, crop="valid", P=None, use_numpy_fft=False):
     dw = r[:, :, nr - 1::-1, nc - 1::-1][:, :, :nr, :nc]              # lag (n−1−u, n−1−v)
     del dy_spec
     return np.ascontiguousarray(dw)
+
+
+# ---------------------------------------------------------------- overlap-and-save
+def oas_conv_fwd(x, w, crop="valid", P=None, use_numpy_fft=False, keep_aliased=False):
+    """y = crop(x * w) by OVERLAP-AND-SAVE, the variant PAPER.md:15 (§1) names beside OaA
+    ("the overlap-and-save ... is a similar technique that may be marginally faster but
+    has the same complexity"; the paper gives no further detail, so this follows the
+    textbook method it cites, Oppenheim & Schafer: overlapping input segments, circular
+    convolution by DFT, the aliased samples discarded):
+
+      1. partition the cropped output into ceil(M/n)² n×n blocks (edge blocks clipped);
+      2. output block t (rows/cols t·n .. t·n+n−1 of the crop, i.e. t·n + o of the Full
+         frame) needs the input segment of (2n−1)² samples starting at t·n + o − (n−1)
+         (zero outside x): the segments of neighbouring blocks overlap by n−1;
+      3. P-point circular convolution (P ≥ 2n−1, default 2n−1) of every segment with the
+         kernel: IDFT_P(DFT_P(segment) ⊙ DFT_P(kernel)), summed over the C channels;
+      4. discard the first n−1 samples per axis (wrapped around: aliased) and keep samples
+         n−1 .. 2n−2, which equal the linear convolution; write them to the block.
+    keep_aliased=True instead returns, per block, the circular result's FIRST n samples
+    (the discarded, aliased ones) -- used by the tests to show step 4 is necessary.
+    x[B,C,R,Cc], w[K,C,nr,nc]; square blocks per axis as for OaA."""
+    x = np.asarray(x, dtype=np.float64)
+    w = np.asarray(w, dtype=np.float64)
+    B, C, R, Cc = x.shape
+    K, C2, nr, nc = w.shape
+    assert C == C2
+    Mr, Mc = out_size(R, nr, crop), out_size(Cc, nc, crop)
+    orr, oc = crop_offset(nr, crop), crop_offset(nc, crop)
+    Sr, Sc = 2 * nr - 1, 2 * nc - 1                                   # segment sides
+    P1 = Sr if P is None else (P if np.isscalar(P) else P[0])
+    P2 = Sc if P is None else (P if np.isscalar(P) else P[1])
+    T1, T2 = math.ceil(Mr / nr), math.ceil(Mc / nc)                   # step 1
+    pad_r, pad_c = Sr + T1 * nr, Sc + T2 * nc
+    xpad = np.zeros((B, C, R + 2 * pad_r, Cc + 2 * pad_c))
+    xpad[:, :, pad_r:pad_r + R, pad_c:pad_c + Cc] = x
+    seg = np.zeros((B, C, T1, T2, Sr, Sc))
+    for t1 in range(T1):                                              # step 2
+        for t2 in range(T2):
+            r0 = t1 * nr + orr - (nr - 1) + pad_r
+            c0 = t2 * nc + oc - (nc - 1) + pad_c
+            seg[:, :, t1, t2] = xpad[:, :, r0:r0 + Sr, c0:c0 + Sc]
+    Sh = dft2(seg, P1, P2, use_numpy_fft)                             # step 3
+    Wh = dft2(w, P1, P2, use_numpy_fft)
+    circ = idft2(np.einsum("kcfg,bcstfg->bkstfg", Wh, Sh), use_numpy_fft).real
+    y = np.zeros((B, K, T1 * nr, T2 * nc))
+    for t1 in range(T1):                                              # step 4
+        for t2 in range(T2):
+            if keep_aliased:
+                blk = circ[:, :, t1, t2, 0:nr, 0:nc]
+            else:
+                blk = circ[:, :, t1, t2, nr - 1:nr - 1 + nr, nc - 1:nc - 1 + nc]
+            y[:, :, t1 * nr:(t1 + 1) * nr, t2 * nc:(t2 + 1) * nc] = blk
+    return y[:, :, :Mr, :Mc]
 
 
 # --------------------------------------------------------------------- FFTconv

@@ -174,3 +174,40 @@ def test_complexity_numbers_paper():
     assert ex["n"] ** 2 == ex["space"]
     assert math.log2(ex["N"]) == ex["fft"]
     assert round(math.log2(ex["n"]), 1) == ex["oaa"]
+
+
+# -------------------------------------------------------------- overlap-and-save
+@pytest.mark.parametrize("crop", CROPS)
+@pytest.mark.parametrize("N,n", [(12, 3), (13, 4), (9, 5), (5, 5), (7, 1), (20, 8), (10, 2), (17, 7)])
+def test_oas_equals_direct(N, n, crop):
+    """Overlap-and-save (the variant the paper names beside OaA) reaches the
+    linear convolution exactly: == the direct definition (scipy-pinned) for every crop."""
+    if crop == "valid" and n > N:
+        pytest.skip("Valid needs n <= N")
+    x, w = rnd(2, 3, N, N), rnd(4, 3, n, n)
+    np.testing.assert_allclose(oaa_ref.oas_conv_fwd(x, w, crop), oracle.conv_fwd(x, w, crop), atol=tol(3, n))
+    # a larger (power-of-two) transform gives the identical result (reading R3)
+    P = 1 << (2 * n - 1).bit_length() if n > 1 else 1
+    np.testing.assert_allclose(oaa_ref.oas_conv_fwd(x, w, crop, P=P), oracle.conv_fwd(x, w, crop), atol=tol(3, n))
+
+
+@pytest.mark.parametrize("n", [2, 3, 5, 8])
+def test_oas_discarded_samples_are_aliased(n):
+    """The first n−1 samples of each circular segment convolution wrap around: keeping
+    them instead of the last n breaks the result (so step 4's discard is load-bearing),
+    while n = 1 has nothing to discard."""
+    x, w = rnd(1, 2, 3 * n + 1, 3 * n + 1), rnd(2, 2, n, n)
+    bad = oaa_ref.oas_conv_fwd(x, w, "full", keep_aliased=True)
+    assert np.abs(bad - oracle.conv_fwd(x, w, "full")).max() > 1e-3
+    x1, w1 = rnd(1, 2, 6, 6), rnd(2, 2, 1, 1)
+    np.testing.assert_allclose(oaa_ref.oas_conv_fwd(x1, w1, "full", keep_aliased=True),
+                               oracle.conv_fwd(x1, w1, "full"), atol=1e-13)
+
+
+def test_oas_delta_kernel_shift():
+    """δ at (n−1, n−1) in Valid mode gives x[:M, :M] (a closed form)."""
+    N, n = 11, 4
+    x = rnd(1, 1, N, N)
+    w = np.zeros((1, 1, n, n)); w[0, 0, n - 1, n - 1] = 1.0
+    M = N - n + 1
+    np.testing.assert_allclose(oaa_ref.oas_conv_fwd(x, w, "valid")[0, 0], x[0, 0, :M, :M], atol=1e-14)
