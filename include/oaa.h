@@ -72,7 +72,7 @@ typedef enum {
   OAA_ERR_CUDA = 4           /* a kernel launch or memset failed (cudaGetLastError) */
 } oaa_status_t;
 
-typedef enum { OAA_OP_FWD = 0, OAA_OP_BWD_DATA = 1, OAA_OP_BWD_FILTER = 2 } oaa_op_t;
+typedef enum { OAA_OP_FWD = 0, OAA_OP_BWD_DATA = 1, OAA_OP_BWD_FILTER = 2, OAA_OP_FWD_OAS = 3 } oaa_op_t;
 
 /* Output side M for input side N and kernel side n; −1 if invalid. */
 int oaa_conv_out_size(int N, int n, oaa_crop_t crop);
@@ -85,6 +85,18 @@ size_t oaa_conv_workspace_bytes(oaa_op_t op, int B, int C, int K, int N, int n, 
 oaa_status_t oaa_conv_fwd(const float* x, const float* w, float* y, int B, int C, int K, int N,
                           int n, oaa_crop_t crop, void* ws, size_t ws_bytes, void* stream);
 
+/* The same y as oaa_conv_fwd, computed by OVERLAP-AND-SAVE (§1: "the
+ * overlap-and-save ... is a similar technique that may be marginally faster but has the same
+ * complexity").  Output block t (n×n, at t·n in the cropped
+ * output) is the last n rows and columns of the P-point CIRCULAR convolution (P = 2n−1)
+ * of the kernel with the (2n−1)² input window starting at t·n + o − (n−1) (zero outside
+ * x): those outputs have no wrap-around, so they equal the linear convolution and every
+ * output is written once, with no overlap-add.  Workspace: op OAA_OP_FWD_OAS.  Supported
+ * for C ≤ 4 (the SIMT walker family); larger C returns OAA_ERR_UNSUPPORTED.  Other
+ * arguments, layouts, limits and errors as oaa_conv_fwd. */
+oaa_status_t oaa_conv_fwd_oas(const float* x, const float* w, float* y, int B, int C, int K, int N,
+                              int n, oaa_crop_t crop, void* ws, size_t ws_bytes, void* stream);
+
 /* dx[B][C][N][N] from dy[B][K][M][M] and w.  dy, w, dx: device pointers. */
 oaa_status_t oaa_conv_bwd_data(const float* dy, const float* w, float* dx, int B, int C, int K,
                                int N, int n, oaa_crop_t crop, void* ws, size_t ws_bytes,
@@ -94,6 +106,28 @@ oaa_status_t oaa_conv_bwd_data(const float* dy, const float* w, float* dx, int B
 oaa_status_t oaa_conv_bwd_filter(const float* x, const float* dy, float* dw, int B, int C, int K,
                                  int N, int n, oaa_crop_t crop, void* ws, size_t ws_bytes,
                                  void* stream);
+
+/* Prepared (cached) weight spectra -- SURVEY.md §8(f) NEXT-4, SPEC.md:266 ("a caller-
+ * visible 'prepared kernel' cache ... for layer-level reuse across many inputs").  Every
+ * fwd / bwd_data call first transforms the kernels (a1: Ŵ = DFT_P(w), or of flip180(w)
+ * for bwd_data) into its workspace; with fixed weights (inference, or many calls per
+ * optimizer step) that stage can be done once:
+ *   bytes = oaa_weight_spectra_bytes(op, C, K, N, n, crop);       op: FWD or BWD_DATA
+ *   oaa_weight_spectra(op, w, spec, bytes, C, K, N, n, crop, stream);
+ *   oaa_conv_fwd_prepared(x, spec, y, B, C, K, N, n, crop, ws, ws_bytes, stream);  (×many)
+ * The layout is internal (it depends on which kernel family the arguments select) and
+ * is valid only for the same (op, C, K, N, n, crop); results are bitwise those of the
+ * unprepared call.  spec: caller-owned device buffer, 256-byte aligned, never written
+ * by the *_prepared calls; the caller re-prepares after changing w.  Workspace sizes as
+ * for the unprepared op.  Errors as for the conv calls (OAA_ERR_WORKSPACE if spec_bytes
+ * is too small; op other than FWD / BWD_DATA is OAA_ERR_INVALID_VALUE). */
+size_t oaa_weight_spectra_bytes(oaa_op_t op, int C, int K, int N, int n, oaa_crop_t crop);
+oaa_status_t oaa_weight_spectra(oaa_op_t op, const float* w, void* spec, size_t spec_bytes, int C, int K, int N,
+                                int n, oaa_crop_t crop, void* stream);
+oaa_status_t oaa_conv_fwd_prepared(const float* x, const void* spec, float* y, int B, int C, int K, int N, int n,
+                                   oaa_crop_t crop, void* ws, size_t ws_bytes, void* stream);
+oaa_status_t oaa_conv_bwd_data_prepared(const float* dy, const void* spec, float* dx, int B, int C, int K, int N,
+                                        int n, oaa_crop_t crop, void* ws, size_t ws_bytes, void* stream);
 
 /* Diagnostic entry point of the tensor-core contraction used for large C·K (SURVEY.md
  * §8(a) a4): D[f] = A[f]·B[f]ᵀ for f < F, A[f] M×Kd, B[f] N×Kd, D[f] M×N, all row-major

@@ -26,13 +26,13 @@ __all__ = [
     "conv_fwd", "conv_bwd_data", "conv_bwd_filter", "out_size", "workspace_bytes", "lib",
     "OaAConv2dFunction", "OaAConv2d", "launch_count", "profile_enable", "profile_collect",
     "profile_collect_kernels",
-    "CROPS", "OP_FWD", "OP_BWD_DATA", "OP_BWD_FILTER", "OaAError",
+    "CROPS", "OP_FWD", "OP_BWD_DATA", "OP_BWD_FILTER", "OP_FWD_OAS", "OaAError", "conv_fwd_oas", "PreparedWeights",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.environ.get("OAA_LIB") or os.path.join(_PKG, "liboaa.so")  # OAA_LIB: experiment builds
 CROPS = {"full": 0, "valid": 1, "same": 2}
-OP_FWD, OP_BWD_DATA, OP_BWD_FILTER = 0, 1, 2
+OP_FWD, OP_BWD_DATA, OP_BWD_FILTER, OP_FWD_OAS = 0, 1, 2, 3
 _STATUS = {0: "OAA_OK", 1: "OAA_ERR_INVALID_VALUE", 2: "OAA_ERR_UNSUPPORTED",
            3: "OAA_ERR_WORKSPACE", 4: "OAA_ERR_CUDA"}
 
@@ -58,9 +58,17 @@ def lib():
             L.oaa_conv_out_size.restype = I
             L.oaa_conv_workspace_bytes.argtypes = [I, I, I, I, I, I, I]
             L.oaa_conv_workspace_bytes.restype = Z
-            for name in ("oaa_conv_fwd", "oaa_conv_bwd_data", "oaa_conv_bwd_filter"):
+            for name in ("oaa_conv_fwd", "oaa_conv_bwd_data", "oaa_conv_bwd_filter", "oaa_conv_fwd_oas"):
                 f = getattr(L, name)
                 f.argtypes = [F, F, F, I, I, I, I, I, I, V, Z, V]
+                f.restype = I
+            L.oaa_weight_spectra_bytes.argtypes = [I, I, I, I, I, I]
+            L.oaa_weight_spectra_bytes.restype = Z
+            L.oaa_weight_spectra.argtypes = [I, F, V, Z, I, I, I, I, I, V]
+            L.oaa_weight_spectra.restype = I
+            for name in ("oaa_conv_fwd_prepared", "oaa_conv_bwd_data_prepared"):
+                f = getattr(L, name)
+                f.argtypes = [F, V, F, I, I, I, I, I, I, V, Z, V]
                 f.restype = I
             L.oaa_debug_bin_gemm_workspace_bytes.argtypes = [I, I, I, I]
             L.oaa_debug_bin_gemm_workspace_bytes.restype = Z
@@ -184,6 +192,28 @@ def conv_fwd(x: torch.Tensor, w: torch.Tensor, crop="valid", out: Optional[torch
     return _call(lib().oaa_conv_fwd, x, w, out, (B, C, K, N, n), crop, OP_FWD, stream)
 
 
+def conv_fwd_oas(x: torch.Tensor, w: torch.Tensor, crop="valid", out: Optional[torch.Tensor] = None,
+                 stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """The same y as conv_fwd, by overlap-and-save (include/oaa.h): each
+    n×n output block is the alias-free part of a (2n−1)-point circular convolution of its
+    input window.  C ≤ 4."""
+    _check(x, "x"); _check(w, "w")
+    B, C, N, N2 = x.shape
+    K, C2, n, n2 = w.shape
+    if N != N2 or n != n2:
+        raise ValueError("square images and kernels only")
+    if C != C2:
+        raise ValueError(f"channel mismatch: x has C={C}, w has C={C2}")
+    M = out_size(N, n, crop)
+    if out is None:
+        out = torch.empty((B, K, M, M), dtype=torch.float32, device=x.device)
+    else:
+        _check(out, "out")
+        if tuple(out.shape) != (B, K, M, M):
+            raise ValueError(f"out must have shape {(B, K, M, M)}")
+    return _call(lib().oaa_conv_fwd_oas, x, w, out, (B, C, K, N, n), crop, OP_FWD_OAS, stream)
+
+
 def conv_bwd_data(dy: torch.Tensor, w: torch.Tensor, N: int, crop="valid",
                   out: Optional[torch.Tensor] = None,
                   stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
@@ -279,6 +309,59 @@ def profile_collect_kernels():
         raise OaAError("oaa_profile_collect_kernels: CUDA error")
     names = [L.oaa_profile_kernel_name(i).decode() for i in range(n)]
     return ({names[i]: ms[i] for i in range(n) if cnt[i]}, {names[i]: cnt[i] for i in range(n) if cnt[i]})
+
+
+# ------------------------------------------------------------ prepared weight spectra
+class PreparedWeights:
+    """Weight spectra computed once and reused across calls (include/oaa.h, NEXT-4 of
+    SURVEY.md §8(f)): ``pw = PreparedWeights(w, N, op="fwd")`` then ``pw.fwd(x)`` (or
+    ``pw.bwd_data(dy)`` for op="bwd_data").  Results are bitwise those of conv_fwd /
+    conv_bwd_data with the same w.  Re-create after changing w."""
+
+    def __init__(self, w: torch.Tensor, N: int, op: str = "fwd", crop="valid",
+                 stream: Optional[torch.cuda.Stream] = None):
+        _check(w, "w")
+        if op not in ("fwd", "bwd_data"):
+            raise ValueError("op must be 'fwd' or 'bwd_data'")
+        self.op, self.crop, self.N = op, crop, int(N)
+        self.K, self.C, self.n = w.shape[0], w.shape[1], w.shape[2]
+        opc = OP_FWD if op == "fwd" else OP_BWD_DATA
+        nbytes = int(lib().oaa_weight_spectra_bytes(opc, self.C, self.K, self.N, self.n, _crop_id(crop)))
+        if nbytes == 0:
+            raise ValueError("unsupported arguments")
+        s = stream if stream is not None else torch.cuda.current_stream(w.device)
+        with torch.cuda.stream(s):
+            self.spec = torch.empty(nbytes, dtype=torch.uint8, device=w.device)
+        st = lib().oaa_weight_spectra(opc, ctypes.c_void_p(w.data_ptr()), ctypes.c_void_p(self.spec.data_ptr()),
+                                      ctypes.c_size_t(nbytes), self.C, self.K, self.N, self.n, _crop_id(crop),
+                                      ctypes.c_void_p(s.cuda_stream))
+        if st != 0:
+            raise OaAError(lib().oaa_status_string(st).decode())
+
+    def fwd(self, x: torch.Tensor, out: Optional[torch.Tensor] = None,
+            stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        if self.op != "fwd":
+            raise ValueError("prepared for bwd_data")
+        _check(x, "x")
+        B, C, N, _ = x.shape
+        if C != self.C or N != self.N:
+            raise ValueError("x does not match the prepared (C, N)")
+        M = out_size(N, self.n, self.crop)
+        out = out if out is not None else torch.empty((B, self.K, M, M), device=x.device)
+        return _call(lib().oaa_conv_fwd_prepared, x, self.spec, out, (B, self.C, self.K, N, self.n),
+                     self.crop, OP_FWD, stream)
+
+    def bwd_data(self, dy: torch.Tensor, out: Optional[torch.Tensor] = None,
+                 stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        if self.op != "bwd_data":
+            raise ValueError("prepared for fwd")
+        _check(dy, "dy")
+        B, K, M, _ = dy.shape
+        if K != self.K or M != out_size(self.N, self.n, self.crop):
+            raise ValueError("dy does not match the prepared (K, N)")
+        out = out if out is not None else torch.empty((B, self.C, self.N, self.N), device=dy.device)
+        return _call(lib().oaa_conv_bwd_data_prepared, dy, self.spec, out, (B, self.C, self.K, self.N, self.n),
+                     self.crop, OP_BWD_DATA, stream)
 
 
 # --------------------------------------------------------------------- autograd

@@ -369,6 +369,48 @@ WalkHostGeo plan_walk(bool is_fwd, int B, int Cin, int Cout, int T, int Ro, int 
   return w;
 }
 
+// overlap-and-save forward (NEXT-2; the walker in OAS mode) -----------------------------
+struct OasPlan {
+  bool use;
+  int Td, TPW, CW, CH4, NCH, KG, ngrp, SW;
+  size_t spec_b, xs_b, xspec_smem, walk_smem;
+};
+OasPlan plan_oas(int B, int C, int K, int N, int n, const Geo& g) {
+  OasPlan o{};
+  o.use = C <= kWalkMaxCin;
+  const int P = 2 * n - 1;
+  o.Td = cdiv(g.M, n);
+  o.TPW = 32 / n;
+  o.CW = o.TPW * n;
+  o.CH4 = o.TPW * n * (n | 1);
+  o.NCH = cdiv(g.M, o.CW);
+  o.KG = std::min(8, K);
+  o.ngrp = cdiv(K, o.KG);
+  o.SW = cdiv(o.NCH * o.CW + n - 1, 4) * 4;
+  o.spec_b = align_up(sizeof(float4) * (size_t)C * K * n * n);
+  o.xs_b = align_up(sizeof(float4) * (size_t)B * o.Td * o.NCH * C * o.CH4);
+  o.xspec_smem = oaa::xspec_smem_bytes(C, P, o.SW, o.CH4);
+  const int QSZ = ((2 * o.TPW + 1) * n * P + 1) & ~1;
+  o.walk_smem = sizeof(float4) * (size_t)oaa::kWalkRing * C * o.CH4 + sizeof(float2) * (size_t)o.KG * QSZ;
+  if (o.walk_smem > 220 * 1024 || o.xspec_smem > 220 * 1024) o.use = false;
+  (void)N;
+  return o;
+}
+cudaError_t launch_walk_oas(int n, const oaa::XSpecParams& xp, const oaa::WalkParams& wp, const OasPlan& o, int cr,
+                            cudaStream_t s) {
+  switch (n) {
+    case 1: return launch_walk_oas_n<1>(xp, wp, o.xspec_smem, o.walk_smem, cr, s);
+    case 2: return launch_walk_oas_n<2>(xp, wp, o.xspec_smem, o.walk_smem, cr, s);
+    case 3: return launch_walk_oas_n<3>(xp, wp, o.xspec_smem, o.walk_smem, cr, s);
+    case 4: return launch_walk_oas_n<4>(xp, wp, o.xspec_smem, o.walk_smem, cr, s);
+    case 5: return launch_walk_oas_n<5>(xp, wp, o.xspec_smem, o.walk_smem, cr, s);
+    case 6: return launch_walk_oas_n<6>(xp, wp, o.xspec_smem, o.walk_smem, cr, s);
+    case 7: return launch_walk_oas_n<7>(xp, wp, o.xspec_smem, o.walk_smem, cr, s);
+    case 8: return launch_walk_oas_n<8>(xp, wp, o.xspec_smem, o.walk_smem, cr, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 // bwd_data for few output channels (oaa_bwdd.cuh) ------------------------------------
 struct BwddPlan {
   bool use;
@@ -545,15 +587,15 @@ cudaError_t launch_bin_gemm(const oaa::BinGemmParams& p, cudaStream_t s) {
 // GEMM (3×TF32 tcgen05) → walker in load mode (inverse DFT + overlap-add + crop).
 oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* out, int B, int C, int K, int n,
                            const Geo& g, const EnginePlan& e, const TcPlan& tc, const EngineWs& L, char* base,
-                           cudaStream_t s) {
+                           cudaStream_t s, const void* prepared) {
   const int Cin = e.Cin, Cout = e.Cout, T = e.T, T2 = T * T;
-  float* Ag = reinterpret_cast<float*>(base + L.spec_off);
+  float* Ag = prepared ? static_cast<float*>(const_cast<void*>(prepared)) : reinterpret_cast<float*>(base + L.spec_off);
   int* flags = reinterpret_cast<int*>(base + L.flags_off);
   int* counter = reinterpret_cast<int*>(base + L.counter_off);
   float* Xg = reinterpret_cast<float*>(base + L.xg_off);
   float* D = reinterpret_cast<float*>(base + L.d_off);
-  if (cudaMemsetAsync(Ag, 0, tc.ag_b, s) != cudaSuccess) return OAA_ERR_CUDA;
-  {
+  if (!prepared && cudaMemsetAsync(Ag, 0, tc.ag_b, s) != cudaSuccess) return OAA_ERR_CUDA;
+  if (!prepared) {
     const long long total = (long long)tc.F * Cin * Cout;
     const int thr = 256;
     const int blocks = (int)std::min<long long>((total + thr - 1) / thr, 8192);
@@ -640,20 +682,23 @@ oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* 
   return OAA_OK;
 }
 
+// prepared != NULL: the weight spectra were computed by oaa_weight_spectra (cached across
+// calls, NEXT-4 of SURVEY.md §8(f)); w is then unused and may be NULL
 oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out, int B, int C,
                         int K, int N, int n, oaa_crop_t crop, void* ws, size_t ws_bytes,
-                        void* stream) {
+                        void* stream, const void* prepared = nullptr) {
   Geo g;
   oaa_status_t st = validate(B, C, K, N, n, crop, &g);
   if (st != OAA_OK) return st;
-  if (!w || (B > 0 && (!in || !out))) return OAA_ERR_INVALID_VALUE;
+  if ((!w && !prepared) || (B > 0 && (!in || !out))) return OAA_ERR_INVALID_VALUE;
+  if (prepared && (reinterpret_cast<uintptr_t>(prepared) % kAlign) != 0) return OAA_ERR_INVALID_VALUE;
   const int R = is_fwd ? N : g.M, Ro = is_fwd ? g.M : N;
   const int Cin = is_fwd ? C : K, Cout = is_fwd ? K : C;
   const int off = is_fwd ? g.o : (n - 1 - g.o);
   const size_t in_bytes = sizeof(float) * (size_t)B * Cin * R * R;
   const size_t out_bytes = sizeof(float) * (size_t)B * Cout * Ro * Ro;
   const size_t w_bytes = sizeof(float) * (size_t)K * C * n * n;
-  if (B > 0 && (overlaps(in, in_bytes, out, out_bytes) || overlaps(w, w_bytes, out, out_bytes)))
+  if (B > 0 && (overlaps(in, in_bytes, out, out_bytes) || (w && overlaps(w, w_bytes, out, out_bytes))))
     return OAA_ERR_INVALID_VALUE;
   const TcPlan tc = plan_tc(B, Cin, Cout, R, n);
   EnginePlan e;
@@ -665,20 +710,21 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
   if (!ws || ws_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0)
     return OAA_ERR_WORKSPACE;
   if (overlaps(ws, L.total, out, out_bytes) || overlaps(ws, L.total, in, in_bytes) ||
-      overlaps(ws, L.total, w, w_bytes))
+      (w && overlaps(ws, L.total, w, w_bytes)))
     return OAA_ERR_INVALID_VALUE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   char* base = static_cast<char*>(ws);
-  float4* spec = reinterpret_cast<float4*>(base + L.spec_off);
+  float4* spec = prepared ? static_cast<float4*>(const_cast<void*>(prepared))
+                          : reinterpret_cast<float4*>(base + L.spec_off);
   int* flags = reinterpret_cast<int*>(base + L.flags_off);
   int* counter = reinterpret_cast<int*>(base + L.counter_off);
 
-  if (tc.use) return run_engine_tc(is_fwd, in, w, out, B, C, K, n, g, e, tc, L, base, s);
+  if (tc.use) return run_engine_tc(is_fwd, in, w, out, B, C, K, n, g, e, tc, L, base, s, prepared);
   if (bd.use) {
     ProfScope prof(OAA_OP_BWD_DATA, s);
     prof.start();
     if (cudaMemsetAsync(out, 0, out_bytes, s) != cudaSuccess) return OAA_ERR_CUDA;
-    {
+    if (!prepared) {
       const long total = (long)K * C * ((g.P + 1) / 2) * g.H;
       const int thr = 256;
       const int blocks = (int)std::min<long>((total + thr - 1) / thr, 4096);
@@ -704,7 +750,7 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
     return err == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
   }
   if (wk.use) {
-    {
+    if (!prepared) {
       const long total = (long)K * C * ((g.P + 1) / 2) * g.H;
       const int thr = 256;
       const int blocks = (int)std::min<long>((total + thr - 1) / thr, 4096);
@@ -753,7 +799,7 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
   }
   // kernel spectra: loop-major layout [Cloop][Cinner][P][H]
   const int loop_is_k = (is_fwd == e.S1) ? 1 : 0;  // fwd S1 / bwd_data S2 loop over k
-  {
+  if (!prepared) {
     const long total = (long)K * C * ((g.P + 1) / 2) * g.H;
     const int thr = 256;
     const int blocks = (int)std::min<long>((total + thr - 1) / thr, 4096);
@@ -873,6 +919,10 @@ size_t oaa_conv_workspace_bytes(oaa_op_t op, int B, int C, int K, int N, int n, 
     const BwddPlan bd = plan_bwdd(fwd, fwd ? K : C, R, n, tc);
     return engine_ws(B, C, K, cdiv(R, n), g, tc, &wk, &bd).total;
   }
+  if (op == OAA_OP_FWD_OAS) {
+    const OasPlan o = plan_oas(B, C, K, N, n, g);
+    return o.use ? o.spec_b + o.xs_b : 0;
+  }
   if (op == OAA_OP_BWD_FILTER) {
     const TcFiltPlan t = plan_tc_filter(B, C, K, N, g.M, n);
     if (t.use) return t.a_b + t.b_b + t.part_b;
@@ -885,9 +935,94 @@ size_t oaa_conv_workspace_bytes(oaa_op_t op, int B, int C, int K, int N, int n, 
   return 0;
 }
 
+// Prepared weight spectra ("a caller-visible 'prepared
+// kernel' cache ... for layer-level reuse across many inputs"): the spectra a fwd /
+// bwd_data call with these arguments computes first, written once into a caller buffer.
+struct SpecPlan {
+  bool ok;
+  size_t bytes;
+};
+SpecPlan spec_plan(bool is_fwd, int C, int K, int N, int n, const Geo& g) {
+  SpecPlan sp{};
+  const int R = is_fwd ? N : g.M, Ro = is_fwd ? g.M : N;
+  const int Cin = is_fwd ? C : K, Cout = is_fwd ? K : C;
+  const int off = is_fwd ? g.o : (n - 1 - g.o);
+  const TcPlan tc = plan_tc(1, Cin, Cout, R, n);
+  EnginePlan e;
+  if (!plan_engine(R, Ro, off, n, Cin, Cout, &e, tc.use)) return sp;
+  const WalkHostGeo wk = plan_walk(is_fwd, 1, Cin, Cout, e.T, Ro, off, n, tc);
+  const BwddPlan bd = plan_bwdd(is_fwd, Cout, R, n, tc);
+  (void)wk;
+  (void)bd;
+  sp.ok = true;
+  // the TC path's real-ified, pre-split UMMA-blocked weights, else the float4 bin-pair
+  // spectra [.][.][n][n] of the walker / bwd_data / engine kernels (same size, own order)
+  sp.bytes = tc.use ? align_up(tc.ag_b) : align_up(sizeof(float4) * (size_t)K * C * n * n);
+  return sp;
+}
+
 oaa_status_t oaa_conv_fwd(const float* x, const float* w, float* y, int B, int C, int K, int N,
                           int n, oaa_crop_t crop, void* ws, size_t ws_bytes, void* stream) {
   return run_engine(true, x, w, y, B, C, K, N, n, crop, ws, ws_bytes, stream);
+}
+
+oaa_status_t oaa_conv_fwd_oas(const float* x, const float* w, float* y, int B, int C, int K, int N, int n,
+                              oaa_crop_t crop, void* ws, size_t ws_bytes, void* stream) {
+  Geo g;
+  oaa_status_t st = validate(B, C, K, N, n, crop, &g);
+  if (st != OAA_OK) return st;
+  if (!w || (B > 0 && (!x || !y))) return OAA_ERR_INVALID_VALUE;
+  const size_t x_bytes = sizeof(float) * (size_t)B * C * N * N;
+  const size_t y_bytes = sizeof(float) * (size_t)B * K * g.M * g.M;
+  const size_t w_bytes = sizeof(float) * (size_t)K * C * n * n;
+  if (B > 0 && (overlaps(x, x_bytes, y, y_bytes) || overlaps(w, w_bytes, y, y_bytes))) return OAA_ERR_INVALID_VALUE;
+  if (std::max(cdiv(N, n) * n, g.M) > oaa::kMaxThreads) return OAA_ERR_UNSUPPORTED;
+  const OasPlan o = plan_oas(B, C, K, N, n, g);
+  if (!o.use) return OAA_ERR_UNSUPPORTED;
+  if (B == 0) return OAA_OK;
+  const size_t need = o.spec_b + o.xs_b;
+  if (!ws || ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0) return OAA_ERR_WORKSPACE;
+  if (overlaps(ws, need, y, y_bytes) || overlaps(ws, need, x, x_bytes) || overlaps(ws, need, w, w_bytes))
+    return OAA_ERR_INVALID_VALUE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* base = static_cast<char*>(ws);
+  float4* spec = reinterpret_cast<float4*>(base);
+  ProfScope prof(OAA_OP_FWD, s);
+  prof.start();
+  {
+    const long total = (long)K * C * ((g.P + 1) / 2) * g.H;
+    const int thr = 256;
+    const int blocks = (int)std::min<long>((total + thr - 1) / thr, 4096);
+    KTimer kt(KID_SPECTRUM, s);
+    oaa::oaa_spectrum_kernel<<<blocks, thr, 0, s>>>(w, spec, K, C, n, 0, 1);
+    g_launches++;
+    if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
+  }
+  oaa::XSpecParams xp;
+  xp.in = x;
+  xp.S = reinterpret_cast<float4*>(base + o.spec_b);
+  xp.Cin = C;
+  xp.R = N;
+  xp.T = o.Td;
+  xp.NCH = o.NCH;
+  xp.SW = o.SW;
+  xp.org = g.o - (n - 1);  // window of output block t: input rows from t·n + o − (n−1)
+  oaa::WalkParams wp{};
+  wp.S = xp.S;
+  wp.spec = spec;
+  wp.out = y;
+  wp.B = B;
+  wp.Cin = C;
+  wp.Cout = K;
+  wp.T = o.Td;
+  wp.Ro = g.M;
+  wp.off = 0;
+  wp.NCH = o.NCH;
+  wp.KG = o.KG;
+  wp.ngrp = o.ngrp;
+  cudaError_t err = launch_walk_oas(n, xp, wp, o, C, s);
+  prof.stop();
+  return err == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
 }
 
 oaa_status_t oaa_conv_bwd_data(const float* dy, const float* w, float* dx, int B, int C, int K,
@@ -997,6 +1132,67 @@ oaa_status_t oaa_conv_bwd_filter(const float* x, const float* dy, float* dw, int
   return OAA_OK;
 }
 
+size_t oaa_weight_spectra_bytes(oaa_op_t op, int C, int K, int N, int n, oaa_crop_t crop) {
+  Geo g;
+  if (op != OAA_OP_FWD && op != OAA_OP_BWD_DATA) return 0;
+  if (validate(1, C, K, N, n, crop, &g) != OAA_OK) return 0;
+  const SpecPlan sp = spec_plan(op == OAA_OP_FWD, C, K, N, n, g);
+  return sp.ok ? sp.bytes : 0;
+}
+
+oaa_status_t oaa_weight_spectra(oaa_op_t op, const float* w, void* spec, size_t spec_bytes, int C, int K, int N,
+                                int n, oaa_crop_t crop, void* stream) {
+  Geo g;
+  if (op != OAA_OP_FWD && op != OAA_OP_BWD_DATA) return OAA_ERR_INVALID_VALUE;
+  oaa_status_t st = validate(1, C, K, N, n, crop, &g);
+  if (st != OAA_OK) return st;
+  if (!w || !spec || (reinterpret_cast<uintptr_t>(spec) % kAlign) != 0) return OAA_ERR_INVALID_VALUE;
+  const bool is_fwd = op == OAA_OP_FWD;
+  const SpecPlan sp = spec_plan(is_fwd, C, K, N, n, g);
+  if (!sp.ok) return OAA_ERR_UNSUPPORTED;
+  if (spec_bytes < sp.bytes) return OAA_ERR_WORKSPACE;
+  if (overlaps(spec, sp.bytes, w, sizeof(float) * (size_t)K * C * n * n)) return OAA_ERR_INVALID_VALUE;
+  // run the call's own spectrum stage into `spec`: a B = 1 call with the spectra as its
+  // workspace prefix would also launch the main kernels, so the stage is issued directly
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int R = is_fwd ? N : g.M, Ro = is_fwd ? g.M : N;
+  const int Cin = is_fwd ? C : K, Cout = is_fwd ? K : C;
+  const int off = is_fwd ? g.o : (n - 1 - g.o);
+  const TcPlan tc = plan_tc(1, Cin, Cout, R, n);
+  KTimer kt(KID_SPECTRUM, s);
+  if (tc.use) {
+    if (cudaMemsetAsync(spec, 0, tc.ag_b, s) != cudaSuccess) return OAA_ERR_CUDA;
+    const long long total = (long long)tc.F * Cin * Cout;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 8192);
+    oaa::oaa_realified_spectrum_kernel<<<blocks, 256, 0, s>>>(w, static_cast<float*>(spec), K, C, n, is_fwd ? 0 : 1,
+                                                              tc.Kc, tc.RTA);
+  } else {
+    EnginePlan e;
+    plan_engine(R, Ro, off, n, Cin, Cout, &e, false);
+    const WalkHostGeo wk = plan_walk(is_fwd, 1, Cin, Cout, e.T, Ro, off, n, tc);
+    const BwddPlan bd = plan_bwdd(is_fwd, Cout, R, n, tc);
+    const int loop_is_k = (wk.use || bd.use) ? 1 : ((is_fwd == e.S1) ? 1 : 0);
+    const long total = (long)K * C * ((g.P + 1) / 2) * g.H;
+    const int blocks = (int)std::min<long>((total + 255) / 256, 4096);
+    oaa::oaa_spectrum_kernel<<<blocks, 256, 0, s>>>(w, static_cast<float4*>(spec), K, C, n, is_fwd ? 0 : 1,
+                                                    loop_is_k);
+  }
+  g_launches++;
+  return cudaGetLastError() == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
+}
+
+oaa_status_t oaa_conv_fwd_prepared(const float* x, const void* spec, float* y, int B, int C, int K, int N, int n,
+                                   oaa_crop_t crop, void* ws, size_t ws_bytes, void* stream) {
+  if (!spec) return OAA_ERR_INVALID_VALUE;
+  return run_engine(true, x, nullptr, y, B, C, K, N, n, crop, ws, ws_bytes, stream, spec);
+}
+
+oaa_status_t oaa_conv_bwd_data_prepared(const float* dy, const void* spec, float* dx, int B, int C, int K, int N,
+                                        int n, oaa_crop_t crop, void* ws, size_t ws_bytes, void* stream) {
+  if (!spec) return OAA_ERR_INVALID_VALUE;
+  return run_engine(false, dy, nullptr, dx, B, C, K, N, n, crop, ws, ws_bytes, stream, spec);
+}
+
 const char* oaa_status_string(oaa_status_t s) {
   switch (s) {
     case OAA_OK: return "OAA_OK";
@@ -1040,7 +1236,7 @@ oaa_status_t oaa_debug_bin_gemm(const float* A, const float* B, float* D, int F,
 
 static const char* const kKernelNames[KID_COUNT] = {
     "spectrum", "xspec", "walk", "bwdd", "xspec_win", "bwdf", "finalize",
-    "tile_spectra", "bin_gemm", "walk_load", "filter_spectra", "engine", "aux"};
+    "tile_spectra", "bin_gemm", "walk_load", "filter_spectra", "engine", "aux", "walk_oas"};
 
 int oaa_profile_kernel_count(void) { return KID_COUNT; }
 

@@ -34,6 +34,7 @@ enum KernelId : int {
   KID_FILTER_SPECTRA, // tensor-core path: bwd_filter operand spectra (a8)
   KID_ENGINE,         // first-generation flag engine (shapes outside the other kernels)
   KID_AUX,            // memsets, zero tails, packing
+  KID_WALK_OAS,       // overlap-and-save forward: contraction + inverse DFT + crop (NEXT-2)
   KID_COUNT
 };
 struct KTimer {
@@ -203,6 +204,33 @@ cudaError_t launch_walk_n(const oaa::XSpecParams& xp, const oaa::WalkParams& wp,
   return cudaGetLastError();
 }
 
+// Overlap-and-save forward (NEXT-2): (2n−1)² input-window spectra, then the walker in OAS mode.
+template <int NN>
+cudaError_t launch_walk_oas_n(const oaa::XSpecParams& xp, const oaa::WalkParams& wp, size_t xspec_smem,
+                              size_t walk_smem, int cr, cudaStream_t s) {
+  {
+    auto k = oaa::oaa_xspec_kernel<NN, true>;
+    cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xspec_smem);
+    if (err != cudaSuccess) return err;
+    {
+      KTimer kt(KID_XSPEC_WIN, s);
+      k<<<wp.B * wp.T, 256, xspec_smem, s>>>(xp);
+    }
+    g_launches++;
+    if ((err = cudaGetLastError()) != cudaSuccess) return err;
+  }
+  auto k = cr <= 1 ? oaa::oaa_walk_kernel<NN, 1, false, true> : cr == 2 ? oaa::oaa_walk_kernel<NN, 2, false, true>
+         : cr == 3 ? oaa::oaa_walk_kernel<NN, 3, false, true> : oaa::oaa_walk_kernel<NN, 4, false, true>;
+  cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)walk_smem);
+  if (err != cudaSuccess) return err;
+  {
+    KTimer kt(KID_WALK_OAS, s);
+    k<<<wp.B * wp.ngrp, 32 * wp.KG, walk_smem, s>>>(wp);
+  }
+  g_launches++;
+  return cudaGetLastError();
+}
+
 template <int NN>
 cudaError_t launch_bwdd_n(const oaa::BwdDParams& p, int cr, size_t smem, cudaStream_t s) {
   const bool tm = smem <= 110 * 1024;  // TMEM accumulators whenever 2 CTAs fit an SM
@@ -270,6 +298,7 @@ cudaError_t launch_walk_load_n(const oaa::WalkParams& wp, size_t smem, int nimg,
   extern template cudaError_t launch_filter_spectra_n<NN>(const oaa::FiltSpecParams&, bool, int, size_t, cudaStream_t); \
   extern template cudaError_t launch_walk_n<NN>(const oaa::XSpecParams&, const oaa::WalkParams&, const WalkPlan&, int, cudaStream_t); \
   extern template cudaError_t launch_bwdd_n<NN>(const oaa::BwdDParams&, int, size_t, cudaStream_t); \
+  extern template cudaError_t launch_walk_oas_n<NN>(const oaa::XSpecParams&, const oaa::WalkParams&, size_t, size_t, int, cudaStream_t); \
   extern template cudaError_t launch_walk_load_n<NN>(const oaa::WalkParams&, size_t, int, cudaStream_t); \
   extern template cudaError_t launch_bwdf_n<NN>(const oaa::XSpecParams&, const oaa::BwdFParams&, size_t, size_t, int, bool, cudaStream_t);
 #define OAA_INSTANTIATE_N(NN)                                                                 \
@@ -281,6 +310,7 @@ cudaError_t launch_walk_load_n(const oaa::WalkParams& wp, size_t smem, int nimg,
   template cudaError_t launch_filter_spectra_n<NN>(const oaa::FiltSpecParams&, bool, int, size_t, cudaStream_t); \
   template cudaError_t launch_walk_n<NN>(const oaa::XSpecParams&, const oaa::WalkParams&, const WalkPlan&, int, cudaStream_t); \
   template cudaError_t launch_bwdd_n<NN>(const oaa::BwdDParams&, int, size_t, cudaStream_t); \
+  template cudaError_t launch_walk_oas_n<NN>(const oaa::XSpecParams&, const oaa::WalkParams&, size_t, size_t, int, cudaStream_t); \
   template cudaError_t launch_walk_load_n<NN>(const oaa::WalkParams&, size_t, int, cudaStream_t); \
   template cudaError_t launch_bwdf_n<NN>(const oaa::XSpecParams&, const oaa::BwdFParams&, size_t, size_t, int, bool, cudaStream_t);
 

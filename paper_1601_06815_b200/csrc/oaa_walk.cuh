@@ -218,7 +218,13 @@ constexpr int kWalkRing = 4;  // spectrum chunk slots per CTA
 // carry[KG][TRP/4][NCH·CW][4] floats (TRP = n−1 rounded up to 4: a column's carry rows are
 // two float4, consecutive lanes' float4 contiguous).
 __host__ __device__ constexpr int walk_trp(int n) { return ((n - 1) + 3) & ~3; }
-template <int NN, int CR, bool LOAD = false>
+// OAS = true: the overlap-and-save variant (NEXT-2 of SURVEY.md §8(f)).  S holds
+// the spectra of the (2n−1)² input WINDOWS of the output blocks (oaa_xspec_kernel<n, true>,
+// window origin t·n + o − (n−1)); the P-point circular convolution of a window with the
+// kernel is the linear convolution on its last n rows and columns (no wrap-around), so
+// stage B keeps Q column n−1+p2 and c2r rows [n−1, 2n−1) and stores them: no horizontal
+// sum, no vertical carry, every output written once.
+template <int NN, int CR, bool LOAD = false, bool OAS = false>
 __global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
   using G = WalkGeo<NN>;
   constexpr int P = G::P, H = G::H, P2 = G::P2, TPW = G::TPW, CW = G::CW, RS4 = G::RS4, QT = G::QT;
@@ -250,7 +256,8 @@ __global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
   }
   // zero tile of Q and the carry rows
   for (int e = lane; e < QT; e += 32) Q[G::QS * QT + e] = make_float2(0.f, 0.f);
-  for (int e = lane; e < TRP * CWT; e += 32) carry[e] = 0.f;
+  if constexpr (!OAS)
+    for (int e = lane; e < TRP * CWT; e += 32) carry[e] = 0.f;
   __syncthreads();
   if (!LOAD && tid == 0) {
     for (int s = 0; s < kWalkRing && s < nseq; ++s) {
@@ -385,8 +392,30 @@ __global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
           }
         }
       }
+      // ---- stage B (overlap-and-save): the block's last n columns and rows, stored directly
+      if constexpr (OAS) {
+        if (active && laneB) {
+          const int offA = (half * TPW + lq) * QT + (NN - 1) + pA;
+          float zr[H], zi[H];
+#pragma unroll
+          for (int k = 0; k < H; ++k) {
+            const float2 a = Q[offA + k * P];
+            zr[k] = a.x;
+            zi[k] = a.y;
+          }
+          float y[P];
+          c2r_half<P>(zr, zi, y);
+          const int j = i * CW + lane;
+          if (j < p.Ro) {
+            float* op = outp + (ptrdiff_t)(t1 * NN) * p.Ro + j;
+#pragma unroll
+            for (int r = 0; r < NN; ++r)
+              if (t1 * NN + r < p.Ro) __stcs(op + (ptrdiff_t)r * p.Ro, y[NN - 1 + r]);
+          }
+        }
+      }
       // ---- stage B: horizontal overlap-add, c2r along f1, vertical carry, stores
-      if (active && laneB) {
+      if (!OAS && active && laneB) {
         const int tA = i * TPW + lq;
         const int offA = (half * TPW + lq) * QT + pA;
         int offB = G::QS * QT;  // zero tile
@@ -443,7 +472,7 @@ __global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
     }
   }
   // flush: the carry holds the last tile row's bottom rows (final)
-  if (active && laneB) {
+  if (!OAS && active && laneB) {
     const int r0 = p.T * NN - p.off;
     for (int i = 0; i < p.NCH; ++i) {
       const int J = i * CW + lane, j = J - p.off;

@@ -106,6 +106,20 @@ def test_headline_every_element(crop):
     all_elements(CONFIGS["headline"], crop, seed=10, chunk=16)
 
 
+def test_headline_oas_every_element():
+    """NEXT-2 overlap-and-save forward at the headline size: all 385 M elements of y."""
+    wl = CONFIGS["headline"]
+    B, C, K, N, n, crop = wl.B, wl.C, wl.K, wl.N, wl.n, "valid"
+    x, w, _ = gpu_inputs(B, C, K, N, n, crop, seed=15)
+    y = oaa.conv_fwd_oas(x, w, crop)
+    torch.cuda.synchronize()
+    wh = w.cpu().numpy()
+    e = Err("headline oas y")
+    for b0 in range(0, B, 16):
+        e.add(y[b0:b0 + 16].double().cpu().numpy(), oracle.conv_fwd(x[b0:b0 + 16].cpu().numpy(), wh, crop))
+    e.check()
+
+
 def test_alexnet_every_element():
     """BASELINE configs[3] (N=27, n=5, C=96, K=256, B=256): the tensor-core path, every
     element; dw sums a 6 400-term reduction per element (split-K + fp64 finalize)."""

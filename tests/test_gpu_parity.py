@@ -319,3 +319,54 @@ def test_tcgen05_bin_gemm_3xtf32(F, M, N, Kd):
     D = oaa.debug_bin_gemm(A, B)
     ref = torch.matmul(A.double(), B.double().transpose(1, 2))
     check(D.cpu().numpy(), ref.cpu().numpy(), "bin_gemm")
+
+
+# ----------------------------------------------------------- overlap-and-save forward
+@pytest.mark.parametrize("crop", CROPS)
+@pytest.mark.parametrize("N,n", [(N, n) for n in range(1, 9) for N in sorted({n, n + 1, 2 * n - 1, 3 * n + 2, 20, 33})])
+def test_oas_forward_small_grid(N, n, crop):
+    """NEXT-2: conv_fwd_oas == the direct oracle, every element, all crops,
+    ragged output tiles, C ≤ 4 (the SIMT walker family)."""
+    if crop == "valid" and n > N:
+        pytest.skip("Valid needs n <= N")
+    for (B, C, K) in [(1, 1, 1), (2, 3, 5), (3, 4, 9)]:
+        d = make_inputs(B, C, K, N, n, crop, seed=N * 13 + n * 5 + B)
+        x = torch.from_numpy(d["x"]).cuda()
+        w = torch.from_numpy(d["w"]).cuda()
+        y = oaa.conv_fwd_oas(x, w, crop)
+        torch.cuda.synchronize()
+        check(y.cpu().numpy(), oracle.conv_fwd(d["x"], d["w"], crop), f"oas N={N} n={n} {crop} BCK={B,C,K}")
+
+
+def test_oas_matches_oaa_and_rejects_large_C():
+    d = make_inputs(2, 3, 64, 60, 8, "valid", seed=5)
+    x = torch.from_numpy(d["x"]).cuda(); w = torch.from_numpy(d["w"]).cuda()
+    a = oaa.conv_fwd_oas(x, w); b = oaa.conv_fwd(x, w)
+    assert (a - b).abs().max().item() <= 1e-4 * b.abs().max().item()
+    with pytest.raises(ValueError):
+        oaa.conv_fwd_oas(torch.zeros(1, 5, 16, 16, device="cuda"), torch.zeros(2, 5, 3, 3, device="cuda"))
+
+
+# ------------------------------------------------------ prepared (cached) weight spectra
+@pytest.mark.parametrize("B,C,K,N,n,crop", [(2, 3, 8, 40, 8, "valid"), (2, 3, 5, 23, 5, "same"),
+                                            (1, 6, 7, 19, 4, "full"), (2, 16, 20, 17, 3, "same"),
+                                            (2, 24, 16, 20, 8, "valid"), (1, 2, 3, 250, 3, "valid")])
+def test_prepared_weight_spectra_bitwise(B, C, K, N, n, crop):
+    """NEXT-4: spectra prepared once give bitwise the unprepared results,
+    for every kernel family (walker, bwd_data, flag engine, tensor-core path), and the
+    prepared buffer is read-only across many calls."""
+    d = make_inputs(B, C, K, N, n, crop, seed=B + C + K + N + n)
+    x = torch.from_numpy(d["x"]).cuda(); w = torch.from_numpy(d["w"]).cuda()
+    dy = torch.from_numpy(d["dy"]).cuda()
+    pf = oaa.PreparedWeights(w, N, "fwd", crop)
+    pb = oaa.PreparedWeights(w, N, "bwd_data", crop)
+    snap_f, snap_b = pf.spec.clone(), pb.spec.clone()
+    y0, dx0 = oaa.conv_fwd(x, w, crop), oaa.conv_bwd_data(dy, w, N, crop)
+    for _ in range(2):
+        assert torch.equal(pf.fwd(x), y0)
+        assert torch.equal(pb.bwd_data(dy), dx0)
+    torch.cuda.synchronize()
+    assert torch.equal(pf.spec, snap_f) and torch.equal(pb.spec, snap_b)
+    check(y0.cpu().numpy(), oracle.conv_fwd(d["x"], d["w"], crop), "prepared fwd")
+    with pytest.raises(ValueError):
+        pf.bwd_data(dy)
