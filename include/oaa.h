@@ -72,7 +72,13 @@ typedef enum {
   OAA_ERR_CUDA = 4           /* a kernel launch or memset failed (cudaGetLastError) */
 } oaa_status_t;
 
-typedef enum { OAA_OP_FWD = 0, OAA_OP_BWD_DATA = 1, OAA_OP_BWD_FILTER = 2, OAA_OP_FWD_OAS = 3 } oaa_op_t;
+typedef enum {
+  OAA_OP_FWD = 0,
+  OAA_OP_BWD_DATA = 1,
+  OAA_OP_BWD_FILTER = 2,
+  OAA_OP_FWD_OAS = 3, /* oaa_conv_fwd_oas */
+  OAA_OP_BWD = 4      /* oaa_conv_bwd (fused backward) */
+} oaa_op_t;
 
 /* Output side M for input side N and kernel side n; −1 if invalid. */
 int oaa_conv_out_size(int N, int n, oaa_crop_t crop);
@@ -128,6 +134,21 @@ oaa_status_t oaa_conv_fwd_prepared(const float* x, const void* spec, float* y, i
                                    oaa_crop_t crop, void* ws, size_t ws_bytes, void* stream);
 oaa_status_t oaa_conv_bwd_data_prepared(const float* dy, const void* spec, float* dx, int B, int C, int K, int N,
                                         int n, oaa_crop_t crop, void* ws, size_t ws_bytes, void* stream);
+
+/* The whole backward pass in one call (§3.2: "the backward propagation
+ * contains two actual convolutions per kernel: one convolution to propagate the error
+ * through the layer and another to calculate the change in weight"; SURVEY.md §8(f)
+ * NEXT-1): dx as oaa_conv_bwd_data(dy, w) and dw as oaa_conv_bwd_filter(x, dy), both
+ * written.  On the tensor-core path (C, K ≥ 16) the dy blocks are read and transformed
+ * ONCE per batch chunk: the same spectra Ĝ feed the data-gradient contraction (Σ over
+ * k) and the weight-gradient accumulation (Σ over blocks).  Elsewhere the two
+ * convolutions run back to back on `stream`.  dw may differ from a separate
+ * oaa_conv_bwd_filter call in rounding (the fused path's batch chunks set its split-K
+ * order); results are deterministic for given arguments.  Workspace: op OAA_OP_BWD.
+ * Arguments, layouts, limits and errors as the two separate calls; all of x, dy, w, dx,
+ * dw and ws must be pairwise disjoint. */
+oaa_status_t oaa_conv_bwd(const float* x, const float* dy, const float* w, float* dx, float* dw, int B, int C,
+                          int K, int N, int n, oaa_crop_t crop, void* ws, size_t ws_bytes, void* stream);
 
 /* Diagnostic entry point of the tensor-core contraction used for large C·K (SURVEY.md
  * §8(a) a4): D[f] = A[f]·B[f]ᵀ for f < F, A[f] M×Kd, B[f] N×Kd, D[f] M×N, all row-major

@@ -26,13 +26,13 @@ __all__ = [
     "conv_fwd", "conv_bwd_data", "conv_bwd_filter", "out_size", "workspace_bytes", "lib",
     "OaAConv2dFunction", "OaAConv2d", "launch_count", "profile_enable", "profile_collect",
     "profile_collect_kernels",
-    "CROPS", "OP_FWD", "OP_BWD_DATA", "OP_BWD_FILTER", "OP_FWD_OAS", "OaAError", "conv_fwd_oas", "PreparedWeights",
+    "CROPS", "OP_FWD", "OP_BWD_DATA", "OP_BWD_FILTER", "OP_FWD_OAS", "OP_BWD", "OaAError", "conv_fwd_oas", "PreparedWeights", "conv_bwd",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.environ.get("OAA_LIB") or os.path.join(_PKG, "liboaa.so")  # OAA_LIB: experiment builds
 CROPS = {"full": 0, "valid": 1, "same": 2}
-OP_FWD, OP_BWD_DATA, OP_BWD_FILTER, OP_FWD_OAS = 0, 1, 2, 3
+OP_FWD, OP_BWD_DATA, OP_BWD_FILTER, OP_FWD_OAS, OP_BWD = 0, 1, 2, 3, 4
 _STATUS = {0: "OAA_OK", 1: "OAA_ERR_INVALID_VALUE", 2: "OAA_ERR_UNSUPPORTED",
            3: "OAA_ERR_WORKSPACE", 4: "OAA_ERR_CUDA"}
 
@@ -62,6 +62,8 @@ def lib():
                 f = getattr(L, name)
                 f.argtypes = [F, F, F, I, I, I, I, I, I, V, Z, V]
                 f.restype = I
+            L.oaa_conv_bwd.argtypes = [F, F, F, F, F, I, I, I, I, I, I, V, Z, V]
+            L.oaa_conv_bwd.restype = I
             L.oaa_weight_spectra_bytes.argtypes = [I, I, I, I, I, I]
             L.oaa_weight_spectra_bytes.restype = Z
             L.oaa_weight_spectra.argtypes = [I, F, V, Z, I, I, I, I, I, V]
@@ -256,6 +258,40 @@ def conv_bwd_filter(x: torch.Tensor, dy: torch.Tensor, n: int, crop="valid",
         if tuple(out.shape) != (K, C, n, n):
             raise ValueError(f"out must have shape {(K, C, n, n)}")
     return _call(lib().oaa_conv_bwd_filter, x, dy, out, (B, C, K, N, n), crop, OP_BWD_FILTER, stream)
+
+
+def conv_bwd(x: torch.Tensor, dy: torch.Tensor, w: torch.Tensor, crop="valid",
+             dx: Optional[torch.Tensor] = None, dw: Optional[torch.Tensor] = None,
+             stream: Optional[torch.cuda.Stream] = None):
+    """(dx, dw) in one call -- the two backward convolutions of PAPER.md:89 (include/oaa.h
+    oaa_conv_bwd; on the tensor-core path the dy spectra are computed once for both)."""
+    _check(x, "x"); _check(dy, "dy"); _check(w, "w")
+    B, C, N, N2 = x.shape
+    B2, K, M, M2 = dy.shape
+    K2, C2, n, n2 = w.shape
+    if B != B2 or K != K2 or C != C2 or N != N2 or M != M2 or n != n2:
+        raise ValueError("shape mismatch")
+    if M != out_size(N, n, crop):
+        raise ValueError(f"dy side {M} != out_size(N={N}, n={n}, {crop})")
+    dx = torch.empty_like(x) if dx is None else dx
+    dw = torch.empty_like(w) if dw is None else dw
+    _check(dx, "dx"); _check(dw, "dw")
+    if dx.shape != x.shape or dw.shape != w.shape:
+        raise ValueError("dx / dw shapes")
+    dev = x.device
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    ws = _workspace(workspace_bytes(OP_BWD, B, C, K, N, n, crop), dev, s)
+    if s != torch.cuda.current_stream(dev):
+        for t in (x, dy, w, dx, dw):
+            t.record_stream(s)
+    P = ctypes.c_void_p
+    st = lib().oaa_conv_bwd(P(x.data_ptr()), P(dy.data_ptr()), P(w.data_ptr()), P(dx.data_ptr()), P(dw.data_ptr()),
+                            B, C, K, N, n, _crop_id(crop), P(ws.data_ptr()), ctypes.c_size_t(ws.numel()),
+                            P(s.cuda_stream))
+    if st != 0:
+        msg = lib().oaa_status_string(st).decode()
+        raise (ValueError if st in (1, 2, 3) else OaAError)(msg)
+    return dx, dw
 
 
 def debug_bin_gemm(A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:

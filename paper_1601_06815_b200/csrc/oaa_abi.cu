@@ -517,7 +517,7 @@ struct TcFiltPlan {
   int F, Td, T2, RTA, RTB, NB, bc, nchunks, Kc, S, kps, G, SWg, SWx;
   size_t a_b, b_b, part_b;
 };
-TcFiltPlan plan_tc_filter(int B, int C, int K, int N, int M, int n) {
+TcFiltPlan plan_tc_filter(int B, int C, int K, int N, int M, int n, int bc_force = 0) {
   TcFiltPlan t{};
   t.use = C >= kTcMinChannels && K >= kTcMinChannels;
   if (!t.use || B < 1) return t;
@@ -531,6 +531,7 @@ TcFiltPlan plan_tc_filter(int B, int C, int K, int N, int M, int n) {
   const size_t per_img = sizeof(float) * (size_t)t.F * 2 * t.T2 * 128 * (size_t)(t.RTA + t.RTB);
   t.nchunks = (int)std::max<size_t>(1, (B * per_img + kTcChunkBytes - 1) / kTcChunkBytes);
   t.bc = cdiv(B, t.nchunks);
+  if (bc_force > 0) t.bc = std::min(t.bc, bc_force);  // (fused backward: the data path's chunks)
   t.nchunks = cdiv(B, t.bc);
   t.Kc = cdiv(2 * t.bc * t.T2, oaa::kTcK);
   // split-K for parallelism (≥ ~4 CTAs per SM); the splits are summed in fp64 by the
@@ -585,17 +586,20 @@ cudaError_t launch_bin_gemm(const oaa::BinGemmParams& p, cudaStream_t s) {
 
 // Tensor-core evaluation of fwd / bwd_data: per batch chunk, T1 (tile spectra) → bin
 // GEMM (3×TF32 tcgen05) → walker in load mode (inverse DFT + overlap-add + crop).
-oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* out, int B, int C, int K, int n,
-                           const Geo& g, const EnginePlan& e, const TcPlan& tc, const EngineWs& L, char* base,
+struct TcData {
+  oaa::TileSpecParams tp;
+  oaa::BinGemmParams gp;
+  oaa::WalkParams wp;
+  size_t t1_smem, walk_smem;
+  int n, T;
+  long long F;
+};
+oaa_status_t tc_data_setup(TcData& d, bool is_fwd, const float* in, const float* w, float* out, int K, int C, int n,
+                           const Geo& g, const EnginePlan& e, const TcPlan& tc, float* Ag, float* Xg, float* D,
                            cudaStream_t s, const void* prepared) {
-  const int Cin = e.Cin, Cout = e.Cout, T = e.T, T2 = T * T;
-  float* Ag = prepared ? static_cast<float*>(const_cast<void*>(prepared)) : reinterpret_cast<float*>(base + L.spec_off);
-  int* flags = reinterpret_cast<int*>(base + L.flags_off);
-  int* counter = reinterpret_cast<int*>(base + L.counter_off);
-  float* Xg = reinterpret_cast<float*>(base + L.xg_off);
-  float* D = reinterpret_cast<float*>(base + L.d_off);
-  if (!prepared && cudaMemsetAsync(Ag, 0, tc.ag_b, s) != cudaSuccess) return OAA_ERR_CUDA;
+  const int Cin = e.Cin, Cout = e.Cout, T = e.T;
   if (!prepared) {
+    if (cudaMemsetAsync(Ag, 0, tc.ag_b, s) != cudaSuccess) return OAA_ERR_CUDA;
     const long long total = (long long)tc.F * Cin * Cout;
     const int thr = 256;
     const int blocks = (int)std::min<long long>((total + thr - 1) / thr, 8192);
@@ -604,7 +608,11 @@ oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* 
     g_launches++;
     if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
   }
-  oaa::TileSpecParams tp;
+  d.n = n;
+  d.T = T;
+  d.F = tc.F;
+  oaa::TileSpecParams& tp = d.tp;
+  tp = oaa::TileSpecParams{};
   tp.in = in;
   tp.Xg = Xg;
   tp.Cin = Cin;
@@ -615,8 +623,10 @@ oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* 
   tp.BW = e.BW;
   tp.CSTR = n * e.BW + 4;
   tp.split = tc.b_split ? 1 : 0;
-  const size_t t1_smem = sizeof(float) * 16 * (size_t)tp.CSTR;
-  oaa::BinGemmParams gp{};
+  tp.Ga = nullptr;
+  d.t1_smem = sizeof(float) * 16 * (size_t)tp.CSTR;
+  oaa::BinGemmParams& gp = d.gp;
+  gp = oaa::BinGemmParams{};
   gp.A = Ag;
   gp.B = Xg;
   gp.D = D;
@@ -643,7 +653,8 @@ oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* 
   gp.Kuse = tc.Kc;
   // walker in LOAD mode: inverse DFT + overlap-add of Ŷ straight from the GEMM output
   const int TPW = 32 / n, CW = TPW * n;
-  oaa::WalkParams wp{};
+  oaa::WalkParams& wp = d.wp;
+  wp = oaa::WalkParams{};
   wp.out = out;
   wp.Cin = 0;
   wp.Cout = Cout;
@@ -655,30 +666,44 @@ oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* 
   wp.ngrp = cdiv(Cout, wp.KG);
   wp.D = D;
   const int QSZ = ((2 * TPW + 1) * n * g.P + 1) & ~1;
-  const size_t walk_smem = sizeof(float2) * (size_t)wp.KG * QSZ + sizeof(float) * (size_t)wp.KG * oaa::walk_trp(n) * wp.NCH * CW;
-  (void)flags;
-  (void)counter;
+  d.walk_smem = sizeof(float2) * (size_t)wp.KG * QSZ + sizeof(float) * (size_t)wp.KG * oaa::walk_trp(n) * wp.NCH * CW;
+  return OAA_OK;
+}
+// one batch chunk [b0, b0 + bc): operand producer, bin GEMM, walker
+oaa_status_t tc_data_chunk(TcData& d, int b0, int bc, cudaStream_t s) {
+  const int n = d.n, T = d.T;
+  const long long btc = (long long)bc * T * T;
+  d.tp.b0 = b0;
+  d.tp.bc = bc;
+  if (launch_tile_spectra(n, d.tp, d.t1_smem, s) != cudaSuccess) return OAA_ERR_CUDA;
+  oaa::BinGemmParams& gp = d.gp;
+  gp.N = (int)btc;
+  gp.ldd = (int)btc;
+  gp.strideD = (long long)gp.M * btc;
+  gp.plane = ((long long)bc * T * gp.NT4 * gp.TPW + gp.SB - 1) / gp.SB * 2 * d.F * gp.SB;
+  if (launch_bin_gemm(gp, s) != cudaSuccess) return OAA_ERR_CUDA;
+  d.wp.B = bc;
+  d.wp.b0 = b0;
+  d.wp.BTc = (int)btc;
+  d.wp.SBL = gp.SBL;
+  if (launch_walk_load(n, d.wp, d.walk_smem, bc, s) != cudaSuccess) return OAA_ERR_CUDA;
+  return OAA_OK;
+}
+
+oaa_status_t run_engine_tc(bool is_fwd, const float* in, const float* w, float* out, int B, int C, int K, int n,
+                           const Geo& g, const EnginePlan& e, const TcPlan& tc, const EngineWs& L, char* base,
+                           cudaStream_t s, const void* prepared) {
+  float* Ag = prepared ? static_cast<float*>(const_cast<void*>(prepared)) : reinterpret_cast<float*>(base + L.spec_off);
+  float* Xg = reinterpret_cast<float*>(base + L.xg_off);
+  float* D = reinterpret_cast<float*>(base + L.d_off);
+  TcData d;
+  oaa_status_t st = tc_data_setup(d, is_fwd, in, w, out, K, C, n, g, e, tc, Ag, Xg, D, s, prepared);
+  if (st != OAA_OK) return st;
   ProfScope prof(is_fwd ? OAA_OP_FWD : OAA_OP_BWD_DATA, s);
   prof.start();
-  for (int b0 = 0; b0 < B; b0 += tc.bc) {
-    const int bc = std::min(tc.bc, B - b0);
-    const long long btc = (long long)bc * T2;
-    tp.b0 = b0;
-    tp.bc = bc;
-    if (launch_tile_spectra(n, tp, t1_smem, s) != cudaSuccess) return OAA_ERR_CUDA;
-    gp.N = (int)btc;
-    gp.ldd = (int)btc;
-    gp.strideD = (long long)2 * Cout * btc;
-    gp.plane = ((long long)bc * T * gp.NT4 * gp.TPW + gp.SB - 1) / gp.SB * 2 * tc.F * gp.SB;
-    if (launch_bin_gemm(gp, s) != cudaSuccess) return OAA_ERR_CUDA;
-    wp.B = bc;
-    wp.b0 = b0;
-    wp.BTc = (int)btc;
-    wp.SBL = gp.SBL;
-    if (launch_walk_load(n, wp, walk_smem, bc, s) != cudaSuccess) return OAA_ERR_CUDA;
-  }
+  for (int b0 = 0; b0 < B; b0 += tc.bc)
+    if ((st = tc_data_chunk(d, b0, std::min(tc.bc, B - b0), s)) != OAA_OK) return st;
   prof.stop();
-  (void)g;
   return OAA_OK;
 }
 
@@ -835,6 +860,71 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
   return err == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
 }
 
+// tensor-core weight gradient: per batch chunk the Ĝ / Ξ̂ operand spectra, then the split-K
+// bin GEMM accumulating per-split partial dŴ; after the last chunk the fp64 finalize
+struct TcFilt {
+  oaa::FiltSpecParams gs, xs;
+  oaa::BinGemmParams gp;
+  size_t smem_g, smem_x;
+  TcFiltPlan t;
+  float *Ga, *Xb, *part;
+  int n;
+};
+void tc_filt_setup(TcFilt& f, const float* x, const float* dy, int C, int K, int N, int n, const Geo& g,
+                   const TcFiltPlan& t, char* base) {
+  f.t = t;
+  f.n = n;
+  f.Ga = reinterpret_cast<float*>(base);
+  f.Xb = reinterpret_cast<float*>(base + t.a_b);
+  f.part = reinterpret_cast<float*>(base + t.a_b + t.b_b);
+  f.gs = oaa::FiltSpecParams{};
+  f.gs.src = dy; f.gs.Op = f.Ga; f.gs.nch = K; f.gs.R = g.M; f.gs.Td = t.Td; f.gs.org = 0; f.gs.Kc = t.Kc;
+  f.gs.RT = t.RTA; f.gs.SW = t.SWg;
+  f.xs = oaa::FiltSpecParams{};
+  f.xs.src = x; f.xs.Op = f.Xb; f.xs.nch = C; f.xs.R = N; f.xs.Td = t.Td; f.xs.org = g.o - (n - 1); f.xs.Kc = t.Kc;
+  f.xs.RT = t.RTB; f.xs.SW = t.SWx;
+  f.smem_g = sizeof(float) * oaa::kFsCG * n * (size_t)t.SWg;
+  f.smem_x = sizeof(float) * oaa::kFsCG * (2 * n - 1) * (size_t)t.SWx;
+  oaa::BinGemmParams& gp = f.gp;
+  gp = oaa::BinGemmParams{};
+  gp.A = f.Ga; gp.B = f.Xb; gp.D = nullptr; gp.F = t.F; gp.M = K; gp.N = 2 * C; gp.Kc = t.Kc; gp.RTA = t.RTA;
+  gp.RTB = t.RTB; gp.ldd = 0; gp.strideD = 0; gp.S = t.S; gp.kps = t.kps; gp.mode = 1; gp.a_split = 0; gp.Cf = C;
+  gp.H = n; gp.P = 2 * n - 1; gp.partial = f.part; gp.NB = t.NB;
+}
+// chunk ci = images [b0, b0 + bc); g_done: Ĝ already written by the fused dy producer
+oaa_status_t tc_filt_chunk(TcFilt& f, int ci, int b0, int bc, bool g_done, cudaStream_t s) {
+  const TcFiltPlan& t = f.t;
+  const int n = f.n;
+  f.gs.b0 = b0;
+  f.xs.b0 = b0;
+  if (!g_done && launch_filter_spectra(n, f.gs, false, bc * t.Td, f.smem_g, s) != cudaSuccess) return OAA_ERR_CUDA;
+  if (launch_filter_spectra(n, f.xs, true, bc * t.Td, f.smem_x, s) != cudaSuccess) return OAA_ERR_CUDA;
+  // a short last chunk: the GEMM reduces only the K chunks holding data, and only the
+  // ragged end of the last one is zeroed
+  const int j0 = 2 * bc * t.T2;
+  f.gp.Kuse = cdiv(j0, oaa::kTcK);
+  if (j0 < 32 * f.gp.Kuse) {
+    KTimer kt(KID_AUX, s);
+    oaa::oaa_tc_zero_tail_kernel<<<512, 256, 0, s>>>(f.Ga, t.F, t.Kc, t.RTA, j0, 32 * f.gp.Kuse);
+    oaa::oaa_tc_zero_tail_kernel<<<512, 256, 0, s>>>(f.Xb, t.F, t.Kc, t.RTB, j0, 32 * f.gp.Kuse);
+    g_launches += 2;
+    if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
+  }
+  f.gp.g0 = 0;
+  f.gp.accumulate = ci > 0;
+  return launch_bin_gemm(f.gp, s) == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
+}
+oaa_status_t tc_filt_finalize(TcFilt& f, float* dw, int K, int C, cudaStream_t s) {
+  const int n = f.n, bins = (2 * n - 1) * n;
+  {
+    KTimer kt(KID_FINALIZE, s);
+    oaa::oaa_filter_finalize_kernel<<<K * C, 128, sizeof(double2) * bins, s>>>(
+        reinterpret_cast<const float2*>(f.part), dw, f.t.G, K, C, n);
+  }
+  g_launches++;
+  return cudaGetLastError() == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
+}
+
 oaa_status_t run_filter_tc(const float* x, const float* dy, float* dw, int B, int C, int K, int N, int n,
                            const Geo& g, const TcFiltPlan& t, void* ws, size_t ws_bytes, cudaStream_t s,
                            size_t x_bytes, size_t dy_bytes, size_t dw_bytes) {
@@ -842,54 +932,46 @@ oaa_status_t run_filter_tc(const float* x, const float* dy, float* dw, int B, in
   if (!ws || ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0) return OAA_ERR_WORKSPACE;
   if (overlaps(ws, need, dw, dw_bytes) || overlaps(ws, need, x, x_bytes) || overlaps(ws, need, dy, dy_bytes))
     return OAA_ERR_INVALID_VALUE;
-  char* base = static_cast<char*>(ws);
-  float* Ga = reinterpret_cast<float*>(base);
-  float* Xb = reinterpret_cast<float*>(base + t.a_b);
-  float* part = reinterpret_cast<float*>(base + t.a_b + t.b_b);
-  oaa::FiltSpecParams gs{};
-  gs.src = dy; gs.Op = Ga; gs.nch = K; gs.R = g.M; gs.Td = t.Td; gs.org = 0; gs.Kc = t.Kc; gs.RT = t.RTA;
-  gs.SW = t.SWg;
-  oaa::FiltSpecParams xs{};
-  xs.src = x; xs.Op = Xb; xs.nch = C; xs.R = N; xs.Td = t.Td; xs.org = g.o - (n - 1); xs.Kc = t.Kc;
-  xs.RT = t.RTB; xs.SW = t.SWx;
-  const size_t smem_g = sizeof(float) * oaa::kFsCG * n * (size_t)t.SWg;
-  const size_t smem_x = sizeof(float) * oaa::kFsCG * (2 * n - 1) * (size_t)t.SWx;
-  oaa::BinGemmParams gp{};
-  gp.A = Ga; gp.B = Xb; gp.D = nullptr; gp.F = t.F; gp.M = K; gp.N = 2 * C; gp.Kc = t.Kc; gp.RTA = t.RTA;
-  gp.RTB = t.RTB; gp.ldd = 0; gp.strideD = 0; gp.S = t.S; gp.kps = t.kps; gp.mode = 1; gp.a_split = 0; gp.Cf = C; gp.H = n;
-  gp.P = 2 * n - 1; gp.partial = part; gp.NB = t.NB;
+  TcFilt f;
+  tc_filt_setup(f, x, dy, C, K, N, n, g, t, static_cast<char*>(ws));
   ProfScope prof(OAA_OP_BWD_FILTER, s);
   prof.start();
   for (int ci = 0; ci < t.nchunks; ++ci) {
-    const int b0 = ci * t.bc, bc = std::min(t.bc, B - b0);
-    gs.b0 = b0;
-    xs.b0 = b0;
-    if (launch_filter_spectra(n, gs, false, bc * t.Td, smem_g, s) != cudaSuccess) return OAA_ERR_CUDA;
-    if (launch_filter_spectra(n, xs, true, bc * t.Td, smem_x, s) != cudaSuccess) return OAA_ERR_CUDA;
-    // a short last chunk: the GEMM reduces only the K chunks holding data, and only the
-    // ragged end of the last one is zeroed
-    const int j0 = 2 * bc * t.T2;
-    gp.Kuse = cdiv(j0, oaa::kTcK);
-    if (j0 < 32 * gp.Kuse) {
-      KTimer kt(KID_AUX, s);
-      oaa::oaa_tc_zero_tail_kernel<<<512, 256, 0, s>>>(Ga, t.F, t.Kc, t.RTA, j0, 32 * gp.Kuse);
-      oaa::oaa_tc_zero_tail_kernel<<<512, 256, 0, s>>>(Xb, t.F, t.Kc, t.RTB, j0, 32 * gp.Kuse);
-      g_launches += 2;
-      if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
-    }
-    gp.g0 = 0;
-    gp.accumulate = ci > 0;
-    if (launch_bin_gemm(gp, s) != cudaSuccess) return OAA_ERR_CUDA;
+    const int b0 = ci * t.bc;
+    oaa_status_t st = tc_filt_chunk(f, ci, b0, std::min(t.bc, B - b0), false, s);
+    if (st != OAA_OK) return st;
   }
   prof.stop();
-  const int bins = g.P * g.H;
-  {
-    KTimer kt(KID_FINALIZE, s);
-    oaa::oaa_filter_finalize_kernel<<<K * C, 128, sizeof(double2) * bins, s>>>(
-        reinterpret_cast<const float2*>(part), dw, t.G, K, C, n);
+  return tc_filt_finalize(f, dw, K, C, s);
+}
+
+// fused backward (NEXT-1): both backward convolutions of PAPER.md:89 in one call.  On the
+// tensor-core path the dy-block spectra Ĝ are computed ONCE per batch chunk and written
+// both as the data-gradient GEMM's B operand and as the weight-gradient GEMM's A operand
+// (dy read once, one set of dy FFTs); elsewhere the two ops run back to back.
+struct BwdFusedPlan {
+  bool tc;
+  TcPlan td;
+  TcFiltPlan tf;
+  EnginePlan e;
+  size_t data_b, filt_b, total;
+};
+bool plan_bwd_fused(int B, int C, int K, int N, int n, oaa_crop_t crop, const Geo& g, BwdFusedPlan* p) {
+  *p = BwdFusedPlan{};
+  p->td = plan_tc(B, K, C, g.M, n);
+  TcFiltPlan tf0 = plan_tc_filter(B, C, K, N, g.M, n);
+  p->tc = p->td.use && tf0.use && B > 0;
+  if (p->tc) {
+    if (!plan_engine(g.M, N, n - 1 - g.o, n, K, C, &p->e, true)) return false;
+    p->tf = plan_tc_filter(B, C, K, N, g.M, n, p->td.bc);
+    p->data_b = align_up(engine_ws(B, C, K, p->e.T, g, p->td).total);
+    p->filt_b = align_up(p->tf.a_b + p->tf.b_b + p->tf.part_b);
+  } else {
+    p->data_b = align_up(oaa_conv_workspace_bytes(OAA_OP_BWD_DATA, B, C, K, N, n, crop));
+    p->filt_b = align_up(oaa_conv_workspace_bytes(OAA_OP_BWD_FILTER, B, C, K, N, n, crop));
   }
-  g_launches++;
-  return cudaGetLastError() == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
+  p->total = p->data_b + p->filt_b;
+  return true;
 }
 
 }  // namespace
@@ -918,6 +1000,11 @@ size_t oaa_conv_workspace_bytes(oaa_op_t op, int B, int C, int K, int N, int n, 
     const WalkHostGeo wk = plan_walk(fwd, B, fwd ? C : K, fwd ? K : C, cdiv(R, n), Ro, off, n, tc);
     const BwddPlan bd = plan_bwdd(fwd, fwd ? K : C, R, n, tc);
     return engine_ws(B, C, K, cdiv(R, n), g, tc, &wk, &bd).total;
+  }
+  if (op == OAA_OP_BWD) {
+    BwdFusedPlan fp;
+    if (!plan_bwd_fused(B, C, K, N, n, crop, g, &fp)) return 0;
+    return fp.total;
   }
   if (op == OAA_OP_FWD_OAS) {
     const OasPlan o = plan_oas(B, C, K, N, n, g);
@@ -964,6 +1051,54 @@ SpecPlan spec_plan(bool is_fwd, int C, int K, int N, int n, const Geo& g) {
 oaa_status_t oaa_conv_fwd(const float* x, const float* w, float* y, int B, int C, int K, int N,
                           int n, oaa_crop_t crop, void* ws, size_t ws_bytes, void* stream) {
   return run_engine(true, x, w, y, B, C, K, N, n, crop, ws, ws_bytes, stream);
+}
+
+oaa_status_t oaa_conv_bwd(const float* x, const float* dy, const float* w, float* dx, float* dw, int B, int C,
+                          int K, int N, int n, oaa_crop_t crop, void* ws, size_t ws_bytes, void* stream) {
+  Geo g;
+  oaa_status_t st = validate(B, C, K, N, n, crop, &g);
+  if (st != OAA_OK) return st;
+  if (!w || !dw || (B > 0 && (!x || !dy || !dx))) return OAA_ERR_INVALID_VALUE;
+  const size_t x_bytes = sizeof(float) * (size_t)B * C * N * N;
+  const size_t dy_bytes = sizeof(float) * (size_t)B * K * g.M * g.M;
+  const size_t w_bytes = sizeof(float) * (size_t)K * C * n * n;
+  if (overlaps(dx, x_bytes, dw, w_bytes) || overlaps(dx, x_bytes, dy, dy_bytes) || overlaps(dx, x_bytes, x, x_bytes) ||
+      overlaps(dx, x_bytes, w, w_bytes) || overlaps(dw, w_bytes, x, x_bytes) || overlaps(dw, w_bytes, dy, dy_bytes) ||
+      overlaps(dw, w_bytes, w, w_bytes))
+    return OAA_ERR_INVALID_VALUE;
+  BwdFusedPlan fp;
+  if (!plan_bwd_fused(B, C, K, N, n, crop, g, &fp)) return OAA_ERR_UNSUPPORTED;
+  char* base = static_cast<char*>(ws);
+  if (!fp.tc) {  // the two ops back to back, each with its own part of the workspace
+    if (B > 0 && (!ws || ws_bytes < fp.total || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0))
+      return OAA_ERR_WORKSPACE;
+    st = oaa_conv_bwd_filter(x, dy, dw, B, C, K, N, n, crop, B > 0 ? base + fp.data_b : ws, fp.filt_b, stream);
+    if (st != OAA_OK) return st;
+    return oaa_conv_bwd_data(dy, w, dx, B, C, K, N, n, crop, ws, fp.data_b, stream);
+  }
+  if (std::max(cdiv(N, n) * n, g.M) > oaa::kMaxThreads) return OAA_ERR_UNSUPPORTED;
+  if (!ws || ws_bytes < fp.total || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0) return OAA_ERR_WORKSPACE;
+  if (overlaps(ws, fp.total, dx, x_bytes) || overlaps(ws, fp.total, dw, w_bytes) || overlaps(ws, fp.total, x, x_bytes) ||
+      overlaps(ws, fp.total, dy, dy_bytes) || overlaps(ws, fp.total, w, w_bytes))
+    return OAA_ERR_INVALID_VALUE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const EngineWs L = engine_ws(B, C, K, fp.e.T, g, fp.td);
+  TcData d;
+  st = tc_data_setup(d, false, dy, w, dx, K, C, n, g, fp.e, fp.td, reinterpret_cast<float*>(base + L.spec_off),
+                     reinterpret_cast<float*>(base + L.xg_off), reinterpret_cast<float*>(base + L.d_off), s, nullptr);
+  if (st != OAA_OK) return st;
+  TcFilt f;
+  tc_filt_setup(f, x, dy, C, K, N, n, g, fp.tf, base + fp.data_b);
+  d.tp.Ga = f.Ga;  // the dy producer also writes the weight-gradient operand
+  d.tp.KcG = fp.tf.Kc;
+  d.tp.RTG = fp.tf.RTA;
+  const int bc = fp.tf.bc;  // ≤ the data path's chunk (plan_bwd_fused)
+  for (int ci = 0; ci * bc < B; ++ci) {
+    const int b0 = ci * bc, bcc = std::min(bc, B - b0);
+    if ((st = tc_data_chunk(d, b0, bcc, s)) != OAA_OK) return st;
+    if ((st = tc_filt_chunk(f, ci, b0, bcc, true, s)) != OAA_OK) return st;
+  }
+  return tc_filt_finalize(f, dw, K, C, s);
 }
 
 oaa_status_t oaa_conv_fwd_oas(const float* x, const float* w, float* y, int B, int C, int K, int N, int n,

@@ -1350,6 +1350,12 @@ struct TileSpecParams {
   float* Xg;        // blocked [F][Kc][RTB][4096] (split: [F][Kc][hi|lo][RTB][4096])
   int Cin, R, T, b0, bc, Kc, RTB, BW, CSTR;
   int split;        // write hi / lo (for GEMMs that re-read each B tile for many M tiles)
+  // fused backward (NEXT-1): the same dy-block spectra Ĝ are ALSO written as
+  // the weight-gradient GEMM's A operand (oaa_filter_spectra_kernel's G mode: row k,
+  // reduction j = 2·bt + {re, im}), so dy is read and transformed once for both backward
+  // convolutions.  Ga == nullptr: plain tile spectra.
+  float* Ga;
+  int KcG, RTG;
 };
 
 // One CTA per (image, tile row) of the chunk.  A task is (f1, tile t2, quad of 4
@@ -1416,6 +1422,17 @@ __global__ void __launch_bounds__(128) oaa_tile_spectra_kernel(const TileSpecPar
         }
       }
       const int bt = bt0 + t2;
+      if (p.Ga) {
+#pragma unroll
+        for (int f2 = 0; f2 < P; ++f2) {
+          const int f = f1 * P + f2;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (cb + i < p.Cin)
+              *reinterpret_cast<float2*>(p.Ga + tc_idx(f, p.KcG, p.RTG, cb + i, 2 * bt)) =
+                  make_float2(xr[i][f2], xi[i][f2]);
+        }
+      }
 #pragma unroll
       for (int f2 = 0; f2 < P; ++f2) {
         const int f = f1 * P + f2;

@@ -192,6 +192,26 @@ def test_sharded_shard_full_size():
     _adjoint(y, dy, x, dx, w, dw)
 
 
+def test_alexnet_fused_backward_every_element():
+    """NEXT-1 fused backward at configs[3] (tensor-core path, dy spectra shared by both
+    GEMMs): every element of dx and dw."""
+    wl = CONFIGS["alexnet"]
+    B, C, K, N, n, crop = wl.B, wl.C, wl.K, wl.N, wl.n, "valid"
+    x, w, dy = gpu_inputs(B, C, K, N, n, crop, seed=16)
+    dx, dw = oaa.conv_bwd(x, dy, w, crop)
+    torch.cuda.synchronize()
+    wh = w.cpu().numpy()
+    edx, edw = Err("alexnet fused dx"), Err("alexnet fused dw")
+    dw_ref = np.zeros((K, C, n, n))
+    for b0 in range(0, B, 32):
+        xs, dys = x[b0:b0 + 32].cpu().numpy(), dy[b0:b0 + 32].cpu().numpy()
+        edx.add(dx[b0:b0 + 32].double().cpu().numpy(), oracle.conv_bwd_data(dys, wh, N, crop))
+        dw_ref += oracle.conv_bwd_filter(xs, dys, n, crop)
+    edw.add(dw.double().cpu().numpy(), dw_ref)
+    edx.check()
+    edw.check()
+
+
 def test_config5_global_batch_one_gpu():
     """configs[4] at its global batch B = 1024 on one GPU (N=1 of the strong-scaling run):
     whole images 0, 511 and 1023; dw against the fp64 sum of the eight B = 128 shard calls

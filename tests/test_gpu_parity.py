@@ -370,3 +370,25 @@ def test_prepared_weight_spectra_bitwise(B, C, K, N, n, crop):
     check(y0.cpu().numpy(), oracle.conv_fwd(d["x"], d["w"], crop), "prepared fwd")
     with pytest.raises(ValueError):
         pf.bwd_data(dy)
+
+
+# ------------------------------------------------------------------ fused backward
+@pytest.mark.parametrize("B,C,K,N,n,crop", [(2, 3, 8, 40, 8, "valid"), (3, 2, 5, 23, 5, "full"),
+                                            (2, 16, 20, 17, 3, "same"), (3, 24, 16, 20, 8, "valid"),
+                                            (2, 33, 17, 23, 2, "full"), (1, 200, 16, 10, 5, "same"),
+                                            (5, 17, 33, 29, 5, "valid")])
+def test_fused_backward(B, C, K, N, n, crop):
+    """NEXT-1: oaa_conv_bwd gives dx bitwise equal to oaa_conv_bwd_data and
+    dw within the bar of the oracle (on the tensor-core path it shares the dy spectra
+    between both GEMMs)."""
+    d = make_inputs(B, C, K, N, n, crop, seed=7 * B + C + K + N + n)
+    x = torch.from_numpy(d["x"]).cuda(); w = torch.from_numpy(d["w"]).cuda()
+    dy = torch.from_numpy(d["dy"]).cuda()
+    dx, dw = oaa.conv_bwd(x, dy, w, crop)
+    dx1 = oaa.conv_bwd_data(dy, w, N, crop)
+    torch.cuda.synchronize()
+    assert torch.equal(dx, dx1)
+    check(dx.cpu().numpy(), oracle.conv_bwd_data(d["dy"], d["w"], N, crop), "fused dx")
+    check(dw.cpu().numpy(), oracle.conv_bwd_filter(d["x"], d["dy"], n, crop), "fused dw")
+    dx2, dw2 = oaa.conv_bwd(x, dy, w, crop)
+    assert torch.equal(dx2, dx) and torch.equal(dw2, dw)  # deterministic
