@@ -945,16 +945,34 @@ oaa_status_t run_filter_tc(const float* x, const float* dy, float* dw, int B, in
   return tc_filt_finalize(f, dw, K, C, s);
 }
 
+cudaError_t launch_bwd_fused(int n, const oaa::XSpecParams& xp, const oaa::BwdDParams& pd, const oaa::BwdFParams& pf,
+                             size_t xsmem, size_t smem, int nf, cudaStream_t s) {
+  switch (n) {
+    case 1: return launch_bwd_fused_n<1>(xp, pd, pf, xsmem, smem, nf, s);
+    case 2: return launch_bwd_fused_n<2>(xp, pd, pf, xsmem, smem, nf, s);
+    case 3: return launch_bwd_fused_n<3>(xp, pd, pf, xsmem, smem, nf, s);
+    case 4: return launch_bwd_fused_n<4>(xp, pd, pf, xsmem, smem, nf, s);
+    case 5: return launch_bwd_fused_n<5>(xp, pd, pf, xsmem, smem, nf, s);
+    case 6: return launch_bwd_fused_n<6>(xp, pd, pf, xsmem, smem, nf, s);
+    case 7: return launch_bwd_fused_n<7>(xp, pd, pf, xsmem, smem, nf, s);
+    case 8: return launch_bwd_fused_n<8>(xp, pd, pf, xsmem, smem, nf, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 // fused backward (NEXT-1): both backward convolutions of PAPER.md:89 in one call.  On the
 // tensor-core path the dy-block spectra Ĝ are computed ONCE per batch chunk and written
 // both as the data-gradient GEMM's B operand and as the weight-gradient GEMM's A operand
 // (dy read once, one set of dy FFTs); elsewhere the two ops run back to back.
 struct BwdFusedPlan {
   bool tc;
+  bool simt;  // one launch of both SIMT bodies (oaa_bwd_fused_kernel)
   TcPlan td;
   TcFiltPlan tf;
   EnginePlan e;
-  size_t data_b, filt_b, total;
+  BwddPlan bd;
+  BwdfPlan bf;  // with G = one weight-gradient CTA per SM (nf = G·nkg CTAs)
+  size_t data_b, filt_b, total, smem;
 };
 bool plan_bwd_fused(int B, int C, int K, int N, int n, oaa_crop_t crop, const Geo& g, BwdFusedPlan* p) {
   *p = BwdFusedPlan{};
@@ -969,6 +987,24 @@ bool plan_bwd_fused(int B, int C, int K, int N, int n, oaa_crop_t crop, const Ge
   } else {
     p->data_b = align_up(oaa_conv_workspace_bytes(OAA_OP_BWD_DATA, B, C, K, N, n, crop));
     p->filt_b = align_up(oaa_conv_workspace_bytes(OAA_OP_BWD_FILTER, B, C, K, N, n, crop));
+    // SIMT family: both bodies fit 128 registers, ≤ 110 KB of shared memory and 256 TMEM
+    // columns, and the weight-gradient CTA has the full 8 warps
+    const TcPlan none{};
+    p->bd = plan_bwdd(false, C, g.M, n, none);
+    p->bf = plan_bwdf(B, C, K, g.M, n);
+    const size_t bsm = oaa::bwdd_smem_bytes(n, C, p->bd.NCW);
+    p->simt = B > 0 && p->bd.use && p->bf.use && p->bf.tm && p->bf.nwb == oaa::kBwdfWarps && bsm <= 110 * 1024 &&
+              p->bf.smem <= 110 * 1024;
+    if (p->simt) {
+#ifndef OAA_EXP_FUSED_SLOTS  // experiment builds only: -DOAA_EXP_FUSED_SLOTS=<weight-gradient CTAs>
+#define OAA_EXP_FUSED_SLOTS 296  // measured: 74 → 3.45, 148 → 2.75, 222 → 2.73, 296 → 2.72 ms (headline)
+#endif
+      p->bf.G = std::max(1, std::min(B * p->bf.Td, OAA_EXP_FUSED_SLOTS / p->bf.nkg));
+      p->bf.part_b = align_up(sizeof(float2) * (size_t)p->bf.G * K * C * (2 * n - 1) * n);
+      p->smem = std::max(bsm, p->bf.smem);
+      p->data_b = align_up(sizeof(float4) * (size_t)K * C * n * n);
+      p->filt_b = p->bf.xs_b + p->bf.part_b;
+    }
   }
   p->total = p->data_b + p->filt_b;
   return true;
@@ -1069,6 +1105,41 @@ oaa_status_t oaa_conv_bwd(const float* x, const float* dy, const float* w, float
   BwdFusedPlan fp;
   if (!plan_bwd_fused(B, C, K, N, n, crop, g, &fp)) return OAA_ERR_UNSUPPORTED;
   char* base = static_cast<char*>(ws);
+  if (fp.simt) {  // one launch of both SIMT bodies
+    if (!ws || ws_bytes < fp.total || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0) return OAA_ERR_WORKSPACE;
+    if (overlaps(ws, fp.total, dx, x_bytes) || overlaps(ws, fp.total, dw, w_bytes) ||
+        overlaps(ws, fp.total, x, x_bytes) || overlaps(ws, fp.total, dy, dy_bytes) || overlaps(ws, fp.total, w, w_bytes))
+      return OAA_ERR_INVALID_VALUE;
+    if (std::max(cdiv(N, n) * n, g.M) > oaa::kMaxThreads) return OAA_ERR_UNSUPPORTED;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    float4* spec = reinterpret_cast<float4*>(base);
+    const BwdfPlan& bf = fp.bf;
+    if (cudaMemsetAsync(dx, 0, x_bytes, s) != cudaSuccess) return OAA_ERR_CUDA;
+    {
+      const long total = (long)K * C * ((g.P + 1) / 2) * g.H;
+      const int blocks = (int)std::min<long>((total + 255) / 256, 4096);
+      KTimer kt(KID_SPECTRUM, s);
+      oaa::oaa_spectrum_kernel<<<blocks, 256, 0, s>>>(w, spec, K, C, n, 1, 1);
+      g_launches++;
+      if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
+    }
+    oaa::BwdDParams dp;
+    dp.dy = dy; dp.spec = spec; dp.dx = dx; dp.B = B; dp.K = K; dp.C = C; dp.M = g.M; dp.N = N;
+    dp.Td = cdiv(g.M, n); dp.off = n - 1 - g.o; dp.NCW = fp.bd.NCW;
+    oaa::XSpecParams xp;
+    xp.in = x; xp.S = reinterpret_cast<float4*>(base + fp.data_b); xp.Cin = C; xp.R = N; xp.T = bf.Td;
+    xp.NCH = bf.NCH; xp.SW = bf.SW; xp.org = g.o - (n - 1);
+    oaa::BwdFParams pf;
+    pf.dy = dy; pf.XS = xp.S; pf.partial = reinterpret_cast<float2*>(base + fp.data_b + bf.xs_b); pf.B = B; pf.K = K;
+    pf.C = C; pf.M = g.M; pf.Td = bf.Td; pf.NCH = bf.NCH; pf.G = bf.G; pf.KG = bf.KG;
+    if (launch_bwd_fused(n, xp, dp, pf, bf.xspec_smem, fp.smem, bf.G * bf.nkg, s) != cudaSuccess) return OAA_ERR_CUDA;
+    {
+      KTimer kt(KID_FINALIZE, s);
+      oaa::oaa_filter_finalize_kernel<<<K * C, 128, sizeof(double2) * g.P * g.H, s>>>(pf.partial, dw, bf.G, K, C, n);
+    }
+    g_launches++;
+    return cudaGetLastError() == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
+  }
   if (!fp.tc) {  // the two ops back to back, each with its own part of the workspace
     if (B > 0 && (!ws || ws_bytes < fp.total || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0))
       return OAA_ERR_WORKSPACE;
@@ -1371,7 +1442,7 @@ oaa_status_t oaa_debug_bin_gemm(const float* A, const float* B, float* D, int F,
 
 static const char* const kKernelNames[KID_COUNT] = {
     "spectrum", "xspec", "walk", "bwdd", "xspec_win", "bwdf", "finalize",
-    "tile_spectra", "bin_gemm", "walk_load", "filter_spectra", "engine", "aux", "walk_oas"};
+    "tile_spectra", "bin_gemm", "walk_load", "filter_spectra", "engine", "aux", "walk_oas", "bwd_fused"};
 
 int oaa_profile_kernel_count(void) { return KID_COUNT; }
 

@@ -64,7 +64,7 @@ __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
 // TM = true: the C output spectra are accumulated in tensor memory (96 columns per warp)
 // instead of registers, so the kernel fits 128 registers and two CTAs share an SM.
 template <int NN, int CR, bool TM = false>
-__global__ void __launch_bounds__(256, TM ? 2 : 1) oaa_bwdd_kernel(const BwdDParams p) {
+__device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
   using G = WalkGeo<NN>;
   constexpr int P = G::P, H = G::H, P2 = G::P2, TPW = G::TPW, QT = G::QT, CW = G::CW;
   constexpr int S = kBwddStages, SW = kBwddWStages;
@@ -75,7 +75,6 @@ __global__ void __launch_bounds__(256, TM ? 2 : 1) oaa_bwdd_kernel(const BwdDPar
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NCW = p.NCW;
-  const int item = blockIdx.x;
   const int b = item / p.Td, t1 = item - (item / p.Td) * p.Td;
   const int w4 = p.C * P2 * H;                // float4 of kernel spectra per dy channel
   const int wst = bwdd_w_bytes(NN, p.C);      // bytes per Ŵ stage
@@ -356,6 +355,11 @@ __global__ void __launch_bounds__(256, TM ? 2 : 1) oaa_bwdd_kernel(const BwdDPar
     asm volatile("bar.sync 1, %0;" ::"r"(nthr_c) : "memory");
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(s_tmem));
   }
+}
+
+template <int NN, int CR, bool TM = false>
+__global__ void __launch_bounds__(256, TM ? 2 : 1) oaa_bwdd_kernel(const BwdDParams p) {
+  bwdd_body<NN, CR, TM>(p, blockIdx.x);
 }
 
 }  // namespace oaa

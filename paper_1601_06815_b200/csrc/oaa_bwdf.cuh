@@ -23,6 +23,7 @@
 #include "dft.cuh"
 #include "oaa_kernels.cuh"
 #include "oaa_walk.cuh"
+#include "oaa_bwdd.cuh"
 
 namespace oaa {
 
@@ -47,8 +48,9 @@ __host__ __device__ constexpr size_t bwdf_smem_bytes(int n, int C) {
          (size_t)kBwdfWarps * BwdfCfg<TM>::dy * (32 / n) * (n * ((32 / n) * n) + 4) * 4;
 }
 
+// g: slice of the (image, tile row) items; kgrp: kernel group; nw: warps in the CTA
 template <int NN, int CR, bool TM>
-__global__ void __launch_bounds__(32 * kBwdfWarps, BwdfCfg<TM>::minb) oaa_bwdf_kernel(const BwdFParams p) {
+__device__ __forceinline__ void bwdf_body(const BwdFParams& p, const int g, const int kgrp, const int nw) {
   constexpr int kBwdfRing = BwdfCfg<TM>::ring, kBwdfDy = BwdfCfg<TM>::dy;
   using G = WalkGeo<NN>;
   constexpr int P = G::P, H = G::H, P2 = G::P2, TPW = G::TPW, CW = G::CW, RS4 = G::RS4;
@@ -62,11 +64,9 @@ __global__ void __launch_bounds__(32 * kBwdfWarps, BwdfCfg<TM>::minb) oaa_bwdf_k
   __shared__ int rel[kBwdfRing];
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nw = blockDim.x >> 5;  // ≤ kBwdfWarps: as many as the kernel group needs
   const int slot4 = p.C * G::CH4;
   float4* ring = reinterpret_cast<float4*>(smem_raw);
   float* dyr = reinterpret_cast<float*>(ring + kBwdfRing * slot4) + (size_t)warp * kBwdfDy * DYS;
-  const int g = blockIdx.x;
   const int nitems_all = p.B * p.Td;
   const int nitems = g < nitems_all ? (nitems_all - g + p.G - 1) / p.G : 0;
   const int nseq = nitems * p.NCH;
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(32 * kBwdfWarps, BwdfCfg<TM>::minb) oaa_bwdf_k
   }
 
   const int ks = lane / H, f1 = lane - (lane / H) * H;
-  const int kbase = blockIdx.y * p.KG + warp * KPW;
+  const int kbase = kgrp * p.KG + warp * KPW;
   const int k = kbase + ks;
   const bool laneK = ks < KPW && k < p.K;
   float cf[NN], sf[NN];
@@ -306,6 +306,25 @@ __global__ void __launch_bounds__(32 * kBwdfWarps, BwdfCfg<TM>::minb) oaa_bwdf_k
       }
     }
   }
+}
+
+template <int NN, int CR, bool TM>
+__global__ void __launch_bounds__(32 * kBwdfWarps, BwdfCfg<TM>::minb) oaa_bwdf_kernel(const BwdFParams p) {
+  bwdf_body<NN, CR, TM>(p, blockIdx.x, blockIdx.y, blockDim.x >> 5);  // ≤ kBwdfWarps warps
+}
+
+// Fused backward, SIMT family (C ≤ 4; oaa_conv_bwd, NEXT-1): the two backward convolutions
+// of PAPER.md:89 in ONE launch.  CTAs [0, nf) run the weight-gradient body (persistent
+// slices, ~one per SM), the rest the data-gradient body, so every SM co-runs one CTA of
+// each: the two bodies stress different pipes (bwd_filter TMEM + ring reads, bwd_data
+// the FMA pipe) and fill each other's issue gaps.  Both bodies fit 128 registers and
+// 256 TMEM columns, so two CTAs share an SM.
+template <int NN, int CR>
+__global__ void __launch_bounds__(256, 2) oaa_bwd_fused_kernel(const BwdDParams pd, const BwdFParams pf, int nf,
+                                                                int G) {
+  const int c = blockIdx.x;
+  if (c < nf) bwdf_body<NN, CR, true>(pf, c % G, c / G, kBwdfWarps);
+  else bwdd_body<NN, CR, true>(pd, c - nf);
 }
 
 }  // namespace oaa

@@ -35,6 +35,7 @@ enum KernelId : int {
   KID_ENGINE,         // first-generation flag engine (shapes outside the other kernels)
   KID_AUX,            // memsets, zero tails, packing
   KID_WALK_OAS,       // overlap-and-save forward: contraction + inverse DFT + crop (NEXT-2)
+  KID_BWD_FUSED,      // fused backward (NEXT-1): bwd_filter + bwd_data bodies in one launch
   KID_COUNT
 };
 struct KTimer {
@@ -276,6 +277,33 @@ cudaError_t launch_bwdf_n(const oaa::XSpecParams& xp, const oaa::BwdFParams& p, 
   return cudaGetLastError();
 }
 
+// Fused backward (SIMT family): Ξ̂ x-window spectra, then both backward bodies in one launch
+template <int NN>
+cudaError_t launch_bwd_fused_n(const oaa::XSpecParams& xp, const oaa::BwdDParams& pd, const oaa::BwdFParams& pf,
+                               size_t xsmem, size_t smem, int nf, cudaStream_t s) {
+  {
+    auto k = oaa::oaa_xspec_kernel<NN, true>;
+    cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsmem);
+    if (err != cudaSuccess) return err;
+    {
+      KTimer kt(KID_XSPEC_WIN, s);
+      k<<<pf.B * pf.Td, 256, xsmem, s>>>(xp);
+    }
+    g_launches++;
+    if ((err = cudaGetLastError()) != cudaSuccess) return err;
+  }
+  auto k = pd.C <= 1 ? oaa::oaa_bwd_fused_kernel<NN, 1> : pd.C == 2 ? oaa::oaa_bwd_fused_kernel<NN, 2>
+         : pd.C == 3 ? oaa::oaa_bwd_fused_kernel<NN, 3> : oaa::oaa_bwd_fused_kernel<NN, 4>;
+  cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  {
+    KTimer kt(KID_BWD_FUSED, s);
+    k<<<nf + pd.B * pd.Td, 256, smem, s>>>(pd, pf, nf, pf.G);
+  }
+  g_launches++;
+  return cudaGetLastError();
+}
+
 template <int NN>
 cudaError_t launch_walk_load_n(const oaa::WalkParams& wp, size_t smem, int nimg, cudaStream_t s) {
   auto k = oaa::oaa_walk_kernel<NN, 1, true>;
@@ -300,6 +328,7 @@ cudaError_t launch_walk_load_n(const oaa::WalkParams& wp, size_t smem, int nimg,
   extern template cudaError_t launch_bwdd_n<NN>(const oaa::BwdDParams&, int, size_t, cudaStream_t); \
   extern template cudaError_t launch_walk_oas_n<NN>(const oaa::XSpecParams&, const oaa::WalkParams&, size_t, size_t, int, cudaStream_t); \
   extern template cudaError_t launch_walk_load_n<NN>(const oaa::WalkParams&, size_t, int, cudaStream_t); \
+  extern template cudaError_t launch_bwd_fused_n<NN>(const oaa::XSpecParams&, const oaa::BwdDParams&, const oaa::BwdFParams&, size_t, size_t, int, cudaStream_t); \
   extern template cudaError_t launch_bwdf_n<NN>(const oaa::XSpecParams&, const oaa::BwdFParams&, size_t, size_t, int, bool, cudaStream_t);
 #define OAA_INSTANTIATE_N(NN)                                                                 \
   template cudaError_t launch_engine_n<NN>(const oaa::EngineParams&, const EnginePlan&,       \
@@ -312,6 +341,7 @@ cudaError_t launch_walk_load_n(const oaa::WalkParams& wp, size_t smem, int nimg,
   template cudaError_t launch_bwdd_n<NN>(const oaa::BwdDParams&, int, size_t, cudaStream_t); \
   template cudaError_t launch_walk_oas_n<NN>(const oaa::XSpecParams&, const oaa::WalkParams&, size_t, size_t, int, cudaStream_t); \
   template cudaError_t launch_walk_load_n<NN>(const oaa::WalkParams&, size_t, int, cudaStream_t); \
+  template cudaError_t launch_bwd_fused_n<NN>(const oaa::XSpecParams&, const oaa::BwdDParams&, const oaa::BwdFParams&, size_t, size_t, int, cudaStream_t); \
   template cudaError_t launch_bwdf_n<NN>(const oaa::XSpecParams&, const oaa::BwdFParams&, size_t, size_t, int, bool, cudaStream_t);
 
 }  // namespace oaa_host

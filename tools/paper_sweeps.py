@@ -17,7 +17,8 @@ The comparison systems here are the GPU library paths a B200 user would otherwis
               Hadamard product summed over C, crop.
 The paper timed single images on one CPU thread; a single small image is launch-latency
 bound on a GPU, so every point here is a batch of B images (B stated per table), timed
-with CUDA events (median of 5 after 2 warm-ups), Valid crop.
+with CUDA events (median of 5 after 2 warm-ups), Valid crop, fp32 arithmetic everywhere
+(cuDNN's TF32 mode is switched off).
 
     python tools/paper_sweeps.py [--out profiles/r02_paper_sweeps.md] [--quick]
 """
@@ -150,6 +151,10 @@ def main():
     ap.add_argument("--quick", action="store_true")
     args = ap.parse_args()
     torch.backends.cudnn.benchmark = True
+    # fp32 arithmetic for the comparison systems too (torch lets cuDNN convolutions use
+    # TF32 by default, which is ~1e-3 relative: not the accuracy class of this library)
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
     res = {"k_sweep": [], "n_sweep": [], "N_sweep": []}
     Ks = range(25, 751, 25) if not args.quick else (25, 250, 750)
     for K in Ks:                                            # §3.2
@@ -179,7 +184,7 @@ def main():
                        f"{r['space_bwd'] / r['oaa_bwd']:.2f} / {r['fft_bwd'] / r['oaa_bwd']:.2f} |")
         return out + [""]
     lines = ["# The paper's comparison sweeps on one B200 (tools/paper_sweeps.py)", "",
-             __doc__.split("The comparison systems here")[1].split("    python tools")[0].strip(), "",
+             "The comparison systems " + __doc__.split("The comparison systems ")[1].split("    python tools")[0].strip(), "",
              "Speed-up = comparison time / OaA time (> 1: OaA faster).  The paper's numbers (up to 16.3× "
              "over spaceConv for an 8×8 kernel on 224×224, single CPU thread with FFTW) are context, "
              "not a target: on a GPU the baselines are cuDNN and cuFFT.", ""]
