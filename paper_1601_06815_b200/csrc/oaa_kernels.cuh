@@ -1291,23 +1291,32 @@ __global__ void oaa_spectrum_kernel(const float* __restrict__ w, float4* __restr
     if (loop_is_k) { k = (int)(ab / C); c = (int)(ab % C); }
     else { c = (int)(ab / K); k = (int)(ab % K); }
     const float* wk = w + ((size_t)k * C + c) * n * n;
-    double out[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int h = 0; h < 2; ++h) {
-      const int f2 = 2 * q + h;
-      if (f2 >= P) continue;
-      double sr = 0.0, si = 0.0;
-      for (int p1 = 0; p1 < n; ++p1)
-        for (int p2 = 0; p2 < n; ++p2) {
-          const float v = flip ? wk[(n - 1 - p1) * n + (n - 1 - p2)] : wk[p1 * n + p2];
-          const int m = (f1 * p1 + f2 * p2) % P;
-          sr += (double)v * tc[m];
-          si -= (double)v * ts[m];
-        }
-      const double inv = 1.0 / ((double)P * (double)P);
-      out[2 * h] = sr * inv;
-      out[2 * h + 1] = si * inv;
+    // both bins f2 = 2q, 2q+1 of the pair in one pass (two independent fp64 chains), the
+    // twiddle index (f1·p1 + f2·p2) mod P kept incrementally (no integer division); the
+    // terms are summed in the same (p1, p2) order as the plain double loop
+    const int fa = 2 * q, fb = 2 * q + 1 < P ? 2 * q + 1 : 0;
+    double sra = 0.0, sia = 0.0, srb = 0.0, sib = 0.0;
+    int m1 = 0;
+    for (int p1 = 0; p1 < n; ++p1) {
+      int ma = m1, mb = m1;
+      for (int p2 = 0; p2 < n; ++p2) {
+        const float v = flip ? wk[(n - 1 - p1) * n + (n - 1 - p2)] : wk[p1 * n + p2];
+        sra += (double)v * tc[ma];
+        sia -= (double)v * ts[ma];
+        srb += (double)v * tc[mb];
+        sib -= (double)v * ts[mb];
+        ma += fa;
+        if (ma >= P) ma -= P;
+        mb += fb;
+        if (mb >= P) mb -= P;
+      }
+      m1 += f1;
+      if (m1 >= P) m1 -= P;
     }
-    spec[t] = make_float4((float)out[0], (float)out[1], (float)out[2], (float)out[3]);
+    const double inv = 1.0 / ((double)P * (double)P);
+    const bool hb = 2 * q + 1 < P;
+    spec[t] = make_float4((float)(sra * inv), (float)(sia * inv), hb ? (float)(srb * inv) : 0.f,
+                          hb ? (float)(sib * inv) : 0.f);
   }
 }
 #endif  // OAA_DEFINE_AUX_KERNELS

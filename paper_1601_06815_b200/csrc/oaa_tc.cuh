@@ -397,13 +397,19 @@ __global__ void oaa_realified_spectrum_kernel(const float* __restrict__ w, float
     const int k = flip_bwd ? i : o, c = flip_bwd ? o : i;
     const float* wk = w + ((size_t)k * C + c) * n * n;
     double sr = 0.0, si = 0.0;
-    for (int p1 = 0; p1 < n; ++p1)
+    int m1 = 0;  // (f1·p1 + f2·p2) mod P kept incrementally
+    for (int p1 = 0; p1 < n; ++p1) {
+      int mm = m1;
       for (int p2 = 0; p2 < n; ++p2) {
         const float v = flip_bwd ? wk[(n - 1 - p1) * n + (n - 1 - p2)] : wk[p1 * n + p2];
-        const int mm = (f1 * p1 + f2 * p2) % P;
         sr += (double)v * tc[mm];
         si -= (double)v * ts[mm];
+        mm += f2;
+        if (mm >= P) mm -= P;
       }
+      m1 += f1;
+      if (m1 >= P) m1 -= P;
+    }
     const float re = (float)(sr * inv), im = (float)(si * inv);
     tc_put_split(Ag, f, Kc, RTA, o, i, re);
     tc_put_split(Ag, f, Kc, RTA, o, Cip + i, -im);
