@@ -15,14 +15,15 @@ processes B=128 images).  Prints ONE JSON line (rank 0).
   e2e       the same metric through the public API with PINNED HOST buffers: the
             host→device copies of x, w, dy and the device→host copies of y, dx, dw are
             inside the timed region.
-  roofline  the dominant kernel (largest per-step CUDA-event time inside the timed
-            region, on its launching stream): its algorithmic work (tools/roofline.py,
+  roofline  the dominant kernel (largest CUDA-event time of a serialized pass run right
+            after the timed region; its time is the timed region's own span when it runs
+            alone there, as the fwd kernels do): its algorithmic work (tools/roofline.py,
             SURVEY.md §8(d)) ÷ its average launch duration, against the measured peak of
             the resource that bounds it (T_roof = max(T_HBM, T_ALU, T_TC)).  `ops` gives
             the same per op and `step_frac` = Σ_op T_roof / ms_per_step.
   cfg5      BASELINE.json configs[4] as north_star states it: global B = 1024 strong-scaled
-            over the N ranks (B/N each), fwd → bwd_filter → async all_reduce(dW) ∥
-            bwd_data, with the all-reduce time.
+            over the N ranks (B/N each), fwd → fused backward (dx, dW) → all_reduce(dW),
+            with the all-reduce time.
   cpu_baseline  the CPU float64 oracle (direct definition) on the host cores (all and
             one), on a bounded sample of the same workload.
 --impl reference runs that oracle as the reference arm (rank 0 only).
@@ -183,8 +184,8 @@ class Step:
     """fwd, then bwd_filter (+ all_reduce(dW) when world > 1) on a side stream concurrent
     with bwd_data: the two backward convolutions of PAPER.md:89 are independent."""
 
-    def __init__(self, torch, dist, oaa, dev, world, x, wt, dy, N, n, crop):
-        self.t, self.dist, self.oaa, self.world = torch, dist, oaa, world
+    def __init__(self, torch, dist, oaa, dev, world, x, wt, dy, N, n, crop, fused=False):
+        self.t, self.dist, self.oaa, self.world, self.fused = torch, dist, oaa, world, fused
         self.x, self.wt, self.dy, self.N, self.n, self.crop = x, wt, dy, N, n, crop
         B, C = x.shape[:2]
         K, M = dy.shape[1], dy.shape[-1]
@@ -198,6 +199,19 @@ class Step:
     def __call__(self, time_allreduce=False):
         oaa, t = self.oaa, self.t
         oaa.conv_fwd(self.x, self.wt, self.crop, out=self.y)
+        if self.fused:
+            # one call for both backward convolutions (NEXT-1: on the tensor-core path the
+            # dy spectra are computed once for both GEMMs), then the dW all-reduce
+            oaa.conv_bwd(self.x, self.dy, self.wt, self.crop, dx=self.dx, dw=self.dw)
+            if self.world > 1:
+                if time_allreduce:
+                    a, b = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+                    a.record(self.stream)
+                self.dist.all_reduce(self.dw)
+                if time_allreduce:
+                    b.record(self.stream)
+                    self.ar_ev.append((a, b))
+            return
         self.side.wait_stream(self.stream)
         oaa.conv_bwd_filter(self.x, self.dy, self.n, self.crop, out=self.dw, stream=self.side)
         if self.world > 1:
@@ -243,7 +257,7 @@ def run_cfg5(args, torch, dist, oaa, dev, world, rank):
     a, b = shard_range(w["B"], rank, world)
     Bl = b - a
     x, wt, dy = _inputs(torch, dev, Bl, w["C"], w["K"], w["N"], w["n"], w["crop"], seed=4242 + rank)
-    st = Step(torch, dist, oaa, dev, world, x, wt, dy, w["N"], w["n"], w["crop"])
+    st = Step(torch, dist, oaa, dev, world, x, wt, dy, w["N"], w["n"], w["crop"], fused=True)
     for _ in range(3):
         st()
     oaa.profile_collect()
@@ -265,7 +279,7 @@ def run_cfg5(args, torch, dist, oaa, dev, world, rank):
            "op_ms": {k: op_ms[k] / max(1, op_cnt[k]) for k in op_ms},
            "allreduce_ms": ar_ms, "allreduce_bytes": 4 * w["K"] * w["C"] * w["n"] ** 2,
            "t_roof_ms_per_gpu": roof_ms, "step_frac": roof_ms / ms_step,
-           "step": "fwd, then bwd_filter -> async NCCL all_reduce(dW) on a side stream, concurrent with bwd_data"}
+           "step": "fwd, then the fused backward (oaa_conv_bwd: dy spectra shared by the bwd_data and bwd_filter GEMMs), then NCCL all_reduce(dW) (N>1)"}
     del st, x, wt, dy
     torch.cuda.empty_cache()
     return rec

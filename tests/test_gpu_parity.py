@@ -392,3 +392,34 @@ def test_fused_backward(B, C, K, N, n, crop):
     check(dw.cpu().numpy(), oracle.conv_bwd_filter(d["x"], d["dy"], n, crop), "fused dw")
     dx2, dw2 = oaa.conv_bwd(x, dy, w, crop)
     assert torch.equal(dx2, dx) and torch.equal(dw2, dw)  # deterministic
+
+
+def test_cuda_graph_capture_replays_bitwise():
+    """The library only enqueues kernels, memsets and attribute calls on the caller's
+    stream (no allocation, no synchronisation; include/oaa.h), so a whole step can be
+    captured into a CUDA graph and replayed -- the launch-latency remedy for small
+    layers.  Replays give bitwise the eager results, on both kernel families."""
+    for (B, C, K, N, n, crop) in [(4, 3, 16, 32, 5, "valid"), (2, 16, 20, 17, 3, "same")]:
+        d = make_inputs(B, C, K, N, n, crop, seed=99)
+        x = torch.from_numpy(d["x"]).cuda(); w = torch.from_numpy(d["w"]).cuda()
+        dy = torch.from_numpy(d["dy"]).cuda()
+        M = out_size(N, n, crop)
+        y = torch.empty((B, K, M, M), device="cuda"); dx = torch.empty_like(x); dw = torch.empty_like(w)
+        s = torch.cuda.Stream()
+
+        def step():
+            oaa.conv_fwd(x, w, crop, out=y, stream=s)
+            oaa.conv_bwd(x, dy, w, crop, dx=dx, dw=dw, stream=s)
+
+        with torch.cuda.stream(s):  # warm-up: workspaces allocated, kernels loaded
+            step()
+        torch.cuda.synchronize()
+        y0, dx0, dw0 = y.clone(), dx.clone(), dw.clone()
+        y.zero_(); dx.zero_(); dw.zero_()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            step()
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(y, y0) and torch.equal(dx, dx0) and torch.equal(dw, dw0)

@@ -32,6 +32,27 @@ def time_config(wl, reps):
            "bwd_data": lambda: oaa.conv_bwd_data(dy, w, N, crop, out=dx),
            "bwd_filter": lambda: oaa.conv_bwd_filter(x, dy, n, crop, out=dw)}
     res = {}
+    # the whole step captured once into a CUDA graph and replayed (removes the host launch
+    # latency of the ~8 launches per step, which dominates the small-N points)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for f in ops.values():
+            f()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for f in ops.values():
+            f()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+        a.record(); g.replay(); b.record(); torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
+    ts.sort()
+    res["graph_step"] = ts[len(ts) // 2]
+    del g
     for name, f in ops.items():
         for _ in range(3):
             f()
@@ -63,6 +84,7 @@ def main():
     rows = []
     for wl in wls:
         t = time_config(wl, args.reps)
+        graph_step = t.pop("graph_step")
         step = sum(t.values())
         dims = (wl.B, wl.C, wl.K, wl.N, wl.n, wl.crop)
         roof = {op: rl.t_roof(rl.op_work(op, *dims)) for op in t}
@@ -72,6 +94,7 @@ def main():
                  ms={k: round(v, 4) for k, v in t.items()}, step_ms=round(step, 4),
                  images_per_s=wl.B / (step / 1e3), tflop_eq_per_s=rl.direct_flops(*dims) / (step / 1e3) / 1e12,
                  roofline_bound="/".join(bounds), roofline_frac=t_roof * 1e3 / step,
+                 graph_step_ms=round(graph_step, 4), graph_frac=t_roof * 1e3 / graph_step,
                  op_frac={op: roof[op][0] * 1e3 / t[op] for op in t})
         rows.append(r)
         print(json.dumps(r), flush=True)
@@ -81,15 +104,17 @@ def main():
              "T_roof = max(T_HBM, T_ALU of the FFTs + overlap-add, T_TC of the contraction); "
              f"denominators HBM {hbm:.0f} GB/s ({src['hbm']}), FFMA {ffma:.1f} TFLOP/s ({src['alu']}), "
              f"3xTF32 {tc3:.0f} TFLOP/s ({src['tc']}). frac = Σ_pass T_roof / step time. "
-             "TFLOP-eq/s counts the direct-convolution flops (3 passes × 2·B·K·C·n²·M²).", "",
-             "| config | B | C | K | N | n | fwd ms | bwd_data ms | bwd_filter ms | step ms | images/s | TFLOP-eq/s | bound | step frac | fwd / bwd_d / bwd_f frac |",
-             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
+             "TFLOP-eq/s counts the direct-convolution flops (3 passes × 2·B·K·C·n²·M²). 'graph step': the "
+             "three passes captured once into a CUDA graph and replayed (no host launch latency).", "",
+             "| config | B | C | K | N | n | fwd ms | bwd_data ms | bwd_filter ms | step ms | images/s | TFLOP-eq/s | bound | step frac | fwd / bwd_d / bwd_f frac | graph step ms | graph frac |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         of = r["op_frac"]
         lines.append(f"| {r['config']} | {r['B']} | {r['C']} | {r['K']} | {r['N']} | {r['n']} | {r['ms']['fwd']:.3f} | "
                      f"{r['ms']['bwd_data']:.3f} | {r['ms']['bwd_filter']:.3f} | {r['step_ms']:.3f} | "
                      f"{r['images_per_s']:.0f} | {r['tflop_eq_per_s']:.1f} | {r['roofline_bound']} | "
-                     f"{r['roofline_frac']:.2f} | {of['fwd']:.2f} / {of['bwd_data']:.2f} / {of['bwd_filter']:.2f} |")
+                     f"{r['roofline_frac']:.2f} | {of['fwd']:.2f} / {of['bwd_data']:.2f} / {of['bwd_filter']:.2f} | "
+                     f"{r['graph_step_ms']:.3f} | {r['graph_frac']:.2f} |")
     with open(args.out, "w") as f:
         f.write("\n".join(lines) + "\n")
 
