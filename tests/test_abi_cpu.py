@@ -48,7 +48,8 @@ def _call(name, B=1, C=1, K=1, N=8, n=3, crop=1, ptrs=(0x1000, 0x200000, 0x40000
              B, C, K, N, n, crop, ctypes.c_void_p(ws), ctypes.c_size_t(ws_bytes), None)
 
 
-@pytest.mark.parametrize("name", ["oaa_conv_fwd", "oaa_conv_bwd_data", "oaa_conv_bwd_filter"])
+@pytest.mark.parametrize("name", ["oaa_conv_fwd", "oaa_conv_bwd_data", "oaa_conv_bwd_filter", "oaa_conv_fwd_oas",
+                                  "oaa_conv_fwd_prepared", "oaa_conv_bwd_data_prepared"])
 def test_invalid_arguments_rejected_before_launch(name):
     INVALID, UNSUP = 1, 2
     assert _call(name, B=-1) == INVALID
@@ -60,7 +61,7 @@ def test_invalid_arguments_rejected_before_launch(name):
     assert _call(name, N=3, n=5, crop=1) == INVALID          # Valid needs n <= N
     assert _call(name, ptrs=(0, 0x200000, 0x40000000)) == INVALID
     assert _call(name, n=9, N=20) == UNSUP                      # v1: n <= 8
-    assert _call(name, N=2000, n=3) == UNSUP or name == "oaa_conv_bwd_filter"
+    assert _call(name, N=2000, n=3) == UNSUP                    # max(ceil(N/n)·n, M) ≤ 256
 
 
 def test_aliasing_rejected():
@@ -98,3 +99,41 @@ def test_cpu_tensors_rejected():
     w = torch.zeros(1, 1, 3, 3)
     with pytest.raises(ValueError):
         oaa.conv_fwd(x, w)
+
+
+def _bwd(B=1, C=1, K=1, N=8, n=3, crop=1, ptrs=(0x1000, 0x200000, 0x40000000, 0x80000000, 0xC0000000),
+         ws=0x7000000000, ws_bytes=1 << 30):
+    P = ctypes.c_void_p
+    return oaa.lib().oaa_conv_bwd(*(P(p) for p in ptrs), B, C, K, N, n, crop, P(ws), ctypes.c_size_t(ws_bytes), None)
+
+
+def test_fused_backward_validation():
+    """oaa_conv_bwd (NEXT-1) validates like the two separate calls, plus pairwise
+    disjointness of x, dy, w, dx, dw."""
+    INVALID, UNSUP, WS = 1, 2, 3
+    assert _bwd(B=-1) == INVALID
+    assert _bwd(C=0) == INVALID
+    assert _bwd(N=3, n=5) == INVALID
+    assert _bwd(n=9, N=20) == UNSUP
+    assert _bwd(ptrs=(0x1000, 0x200000, 0, 0x80000000, 0xC0000000)) == INVALID       # null w
+    assert _bwd(ptrs=(0x1000, 0x200000, 0x40000000, 0x1000, 0xC0000000)) == INVALID  # dx aliases x
+    assert _bwd(ptrs=(0x1000, 0x200000, 0x40000000, 0x80000000, 0x40000000)) == INVALID  # dw aliases w
+    assert _bwd(N=32, n=8, ws_bytes=16) == WS
+
+
+def test_new_op_workspace_sizes():
+    for op in (oaa.OP_FWD_OAS, oaa.OP_BWD):
+        assert oaa.workspace_bytes(op, 128, 3, 64, 224, 8, "valid") > 0
+        assert oaa.workspace_bytes(op, 128, 3, 64, 224, 8, "valid") % 256 == 0
+    # the fused backward needs at least what the two separate ops need on the SIMT path
+    assert oaa.workspace_bytes(oaa.OP_BWD, 256, 96, 256, 27, 5, "valid") > 0
+    assert oaa.workspace_bytes(oaa.OP_FWD_OAS, 2, 5, 3, 16, 3, "valid") == 0   # OaS: C ≤ 4 only
+    L = oaa.lib()
+    for op in (oaa.OP_FWD, oaa.OP_BWD_DATA):
+        assert L.oaa_weight_spectra_bytes(op, 3, 64, 224, 8, 1) % 256 == 0
+        assert L.oaa_weight_spectra_bytes(op, 3, 64, 224, 8, 1) >= 16 * 3 * 64 * 64
+    assert L.oaa_weight_spectra_bytes(oaa.OP_BWD_FILTER, 3, 64, 224, 8, 1) == 0
+    # too-small spectra buffer / bad op are reported before any launch
+    P = ctypes.c_void_p
+    assert L.oaa_weight_spectra(oaa.OP_FWD, P(0x1000), P(0x7000000000), 16, 3, 64, 224, 8, 1, None) == 3
+    assert L.oaa_weight_spectra(oaa.OP_BWD_FILTER, P(0x1000), P(0x7000000000), 1 << 20, 3, 64, 224, 8, 1, None) == 1
