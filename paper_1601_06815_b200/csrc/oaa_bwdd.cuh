@@ -95,7 +95,12 @@ __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
   const int ntile_q = NCW * TPW;  // tiles held in Q; tile ntile_q is the zero tile
 
   if (TM && warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&s_tmem)));
+    // warps w < 4 use columns [0, 128): narrow tile rows (≤ 4 chunk warps, N ≲ 128) take half
+    // the columns, so up to 4 CTAs share an SM's 512
+    if (NCW <= 4)
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&s_tmem)));
+    else
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&s_tmem)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -353,7 +358,10 @@ __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
   if constexpr (TM) {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     asm volatile("bar.sync 1, %0;" ::"r"(nthr_c) : "memory");
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(s_tmem));
+    if (warp == 0) {
+      if (NCW <= 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(s_tmem));
+      else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(s_tmem));
+    }
   }
 }
 
