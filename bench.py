@@ -265,8 +265,8 @@ def run_cfg5(args, torch, dist, oaa, dev, world, rank):
     steps = args.cfg5_steps
     ms = _timed(torch, dist, world, dev, lambda: st(time_allreduce=True), steps, st.stream)
     oaa.profile_enable(False)
-    op_ms, op_cnt = oaa.profile_collect()
-    oaa.profile_collect_kernels()
+    oaa.profile_collect()
+    k_ms, _ = oaa.profile_collect_kernels()
     ar_ms = None
     if st.ar_ev:
         ar_ms = _max_over_ranks(torch, dist, world, dev, sum(e0.elapsed_time(e1) for e0, e1 in st.ar_ev) / len(st.ar_ev))
@@ -276,7 +276,7 @@ def run_cfg5(args, torch, dist, oaa, dev, world, rank):
            "scaling": "strong", "steps": steps, "warmup": 3, "ms_per_step": ms_step,
            "value": w["B"] / (ms_step / 1e3), "unit": UNIT,
            "tflop_eq_per_s": rl.direct_flops(w["B"], w["C"], w["K"], w["N"], w["n"], w["crop"]) / (ms_step / 1e3) / 1e12,
-           "op_ms": {k: op_ms[k] / max(1, op_cnt[k]) for k in op_ms},
+           "kernels_ms_per_step": {k: v / steps for k, v in k_ms.items()},
            "allreduce_ms": ar_ms, "allreduce_bytes": 4 * w["K"] * w["C"] * w["n"] ** 2,
            "t_roof_ms_per_gpu": roof_ms, "step_frac": roof_ms / ms_step,
            "step": "fwd, then the fused backward (oaa_conv_bwd: dy spectra shared by the bwd_data and bwd_filter GEMMs), then NCCL all_reduce(dW) (N>1)"}
@@ -354,6 +354,19 @@ def run_ours(args, w):
     oaa.profile_collect()
     s_ms, s_cnt = oaa.profile_collect_kernels()
     serial = {k: v / nser for k, v in s_ms.items()}
+    # the overlap-and-save forward (NEXT-2) beside the OaA forward, same inputs, for context
+    # (the step itself is OaA, the paper's method)
+    def _fwd_ms(f):
+        f()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(nser):
+            f()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) / nser
+    variants = {"fwd_overlap_and_add_ms": _fwd_ms(lambda: oaa.conv_fwd(x, wt, crop, out=st.y)),
+                "fwd_overlap_and_save_ms": _fwd_ms(lambda: oaa.conv_fwd_oas(x, wt, crop, out=st.y))}
     dom = max(serial, key=serial.get)
     kernel_op = {"walk": "fwd", "xspec": "fwd", "bwdd": "bwd_data", "bwdf": "bwd_filter",
                  "xspec_win": "bwd_filter", "finalize": "bwd_filter", "spectrum": "fwd"}
@@ -437,7 +450,7 @@ def run_ours(args, w):
                            "parallelism": f"dp{world}", "l2": "inputs exceed L2 (dy+y = 3.1 GB/step)",
                            "step": "fwd, then bwd_filter (+ NCCL all_reduce(dW) if N>1) on a side stream concurrent with bwd_data"},
                 "tflop_eq_per_s": world * rl.direct_flops(B, C, K, N, n, crop) / (ms_step / 1e3) / 1e12,
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "roofline": roofline, "variants": variants, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(), "cfg5": cfg5, "nccl": nccl}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -662,7 +662,7 @@ oaa_status_t tc_data_setup(TcData& d, bool is_fwd, const float* in, const float*
   wp.Ro = e.Ro;
   wp.off = e.off;
   wp.NCH = cdiv(e.off + e.Ro, CW);
-  wp.KG = std::min(8, Cout);
+  wp.KG = std::min(n <= 6 ? 4 : 8, Cout);  // warps per load-walker CTA (oaa_walk.cuh launch bounds)
   wp.ngrp = cdiv(Cout, wp.KG);
   wp.D = D;
   const int QSZ = ((2 * TPW + 1) * n * g.P + 1) & ~1;

@@ -32,6 +32,12 @@
 
 namespace oaa {
 
+#ifdef OAA_EXP_TC_SPIN  // experiment builds only: the r1 busy-spinning waits
+#define OAA_TC_WAIT mbar_wait
+#else
+#define OAA_TC_WAIT mbar_wait_sleep
+#endif
+
 constexpr int kTcM = 128, kTcN = 256, kTcK = 32;  // CTA tile and K chunk (fp32 elements)
 constexpr int kTcStages = 2;
 constexpr size_t kTcStageBytes = (size_t)(2 * kTcM + 2 * kTcN) * kTcK * sizeof(float);  // 96 KB
@@ -170,7 +176,7 @@ __global__ void __launch_bounds__(tc_threads<CONV>(), 1) oaa_bin_gemm_kernel(con
         const Tile T = tile_of(t);
         for (int ch = 0; ch < T.nk; ++ch, ++gch) {
           const int s = gch % kTcStages;
-          if (gch >= kTcStages) mbar_wait(&empty[s], ((gch / kTcStages) - 1) & 1);
+          if (gch >= kTcStages) OAA_TC_WAIT(&empty[s], ((gch / kTcStages) - 1) & 1);
           unsigned char* st = smem_raw + s * kTcStageBytes;
           mbar_expect_tx(&full[s], (p.a_split ? 2 : 1) * kBlk + (p.b_split ? 2 : 1) * T.nb * kBlk);
           const size_t kk = (size_t)T.f * p.Kc + T.kbeg + ch;
@@ -192,9 +198,9 @@ __global__ void __launch_bounds__(tc_threads<CONV>(), 1) oaa_bin_gemm_kernel(con
         for (int ch = 0; ch < T.nk; ++ch, ++gch) {
           const int gg = gg0 + ch / kTcDrain, buf = gg & 1;
           const bool first = (ch % kTcDrain) == 0;
-          if (first && gg >= 2) mbar_wait(&acce[buf], ((gg >> 1) - 1) & 1);
+          if (first && gg >= 2) OAA_TC_WAIT(&acce[buf], ((gg >> 1) - 1) & 1);
           const int s = gch % kTcStages;
-          mbar_wait(presplit ? &full[s] : &conv[s], (gch / kTcStages) & 1);
+          OAA_TC_WAIT(presplit ? &full[s] : &conv[s], (gch / kTcStages) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t base = smem_u32(smem_raw + s * kTcStageBytes);
           const uint32_t a_hi = base, a_lo = base + kBlk, b_hi = base + 2 * kBlk, b_lo = base + 4 * kBlk;
@@ -227,7 +233,7 @@ __global__ void __launch_bounds__(tc_threads<CONV>(), 1) oaa_bin_gemm_kernel(con
       const Tile T = tile_of(t);
       for (int ch = 0; ch < T.nk; ++ch, ++gch) {
         const int s = gch % kTcStages;
-        mbar_wait(&full[s], (gch / kTcStages) & 1);
+        OAA_TC_WAIT(&full[s], (gch / kTcStages) & 1);
         unsigned char* st = smem_raw + s * kTcStageBytes;
         float4* ah = reinterpret_cast<float4*>(st);
         float4* al = reinterpret_cast<float4*>(st + kBlk);
@@ -276,7 +282,7 @@ __global__ void __launch_bounds__(tc_threads<CONV>(), 1) oaa_bin_gemm_kernel(con
       for (int j = 0; j < 128; ++j) acc[j] = 0.f;
       for (int gl = 0; gl < ngroups; ++gl) {
         const int gg = gg0 + gl, buf = gg & 1;
-        mbar_wait(&accf[buf], (gg >> 1) & 1);
+        OAA_TC_WAIT(&accf[buf], (gg >> 1) & 1);
         __syncwarp();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (active) {

@@ -224,8 +224,12 @@ __host__ __device__ constexpr int walk_trp(int n) { return ((n - 1) + 3) & ~3; }
 // kernel is the linear convolution on its last n rows and columns (no wrap-around), so
 // stage B keeps Q column n−1+p2 and c2r rows [n−1, 2n−1) and stores them: no horizontal
 // sum, no vertical carry, every output written once.
+// (LOAD with n ≤ 6: no kernel spectra in registers, capped at 128 registers so that CTAs of
+// 4 warps run 3 per SM -- the load walker is latency bound on its Ŷ reads; measured
+// AlexNet-like fwd 0.323 → 0.304 ms, bwd_data 0.117 → 0.107 ms.  For n ≥ 7 the cap cost
+// more than the occupancy gained: sharded-config fwd 4.53 → 5.29 ms per chunk.)
 template <int NN, int CR, bool LOAD = false, bool OAS = false>
-__global__ void __launch_bounds__(256, 1) oaa_walk_kernel(const WalkParams p) {
+__global__ void __launch_bounds__(256, (LOAD && NN <= 6) ? 2 : 1) oaa_walk_kernel(const WalkParams p) {
   using G = WalkGeo<NN>;
   constexpr int P = G::P, H = G::H, P2 = G::P2, TPW = G::TPW, CW = G::CW, RS4 = G::RS4, QT = G::QT;
   constexpr int TR = NN - 1;
