@@ -414,10 +414,10 @@ cudaError_t launch_walk_oas(int n, const oaa::XSpecParams& xp, const oaa::WalkPa
 // bwd_data for few output channels (oaa_bwdd.cuh) ------------------------------------
 struct BwddPlan {
   bool use;
-  int NCW, BW;
+  int NCW, BW, RPC, WSL;
   size_t spec_b, smem;
 };
-BwddPlan plan_bwdd(bool is_fwd, int Cout, int R, int n, const TcPlan& tc) {
+BwddPlan plan_bwdd(bool is_fwd, int B, int Cout, int R, int n, const TcPlan& tc) {
   BwddPlan d{};
   d.use = !is_fwd && !tc.use && Cout <= kWalkMaxCin;
   const int H = n, P = 2 * n - 1, TPW = 32 / H, CW = TPW * n;
@@ -425,7 +425,13 @@ BwddPlan plan_bwdd(bool is_fwd, int Cout, int R, int n, const TcPlan& tc) {
   d.NCW = cdiv(Td, TPW);
   if (d.NCW > 8) d.use = false;  // ≤ 8 warps (256 threads)
   d.BW = d.NCW * CW;
-  d.smem = oaa::bwdd_smem_bytes(n, Cout, d.NCW);
+  // narrow images: several (image, tile row) pairs per CTA so that it has 8 compute warps
+  // sharing one Ŵ ring (a half-depth ring keeps two such CTAs per SM); the headline's 7
+  // chunk warps keep one pair and the 16-deep ring
+  // while keeping ≥ 2 CTAs per SM of work
+  d.RPC = (d.NCW >= 1 && d.NCW <= 4) ? std::max(1, std::min(8 / d.NCW, B * Td / 296)) : 1;
+  d.WSL = d.RPC > 1 ? 3 : 4;
+  d.smem = oaa::bwdd_smem_bytes(n, Cout, d.NCW, d.RPC, d.WSL);
   if (d.smem > 220 * 1024) d.use = false;
   return d;
 }
@@ -730,7 +736,7 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
   if (!plan_engine(R, Ro, off, n, Cin, Cout, &e, tc.use)) return OAA_ERR_UNSUPPORTED;
   if (B == 0) return OAA_OK;
   const WalkHostGeo wk = plan_walk(is_fwd, B, Cin, Cout, e.T, Ro, off, n, tc);
-  const BwddPlan bd = plan_bwdd(is_fwd, Cout, R, n, tc);
+  const BwddPlan bd = plan_bwdd(is_fwd, B, Cout, R, n, tc);
   EngineWs L = engine_ws(B, C, K, e.T, g, tc, &wk, &bd);
   if (!ws || ws_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0)
     return OAA_ERR_WORKSPACE;
@@ -750,11 +756,8 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
     prof.start();
     if (cudaMemsetAsync(out, 0, out_bytes, s) != cudaSuccess) return OAA_ERR_CUDA;
     if (!prepared) {
-      const long total = (long)K * C * ((g.P + 1) / 2) * g.H;
-      const int thr = 256;
-      const int blocks = (int)std::min<long>((total + thr - 1) / thr, 4096);
       KTimer kt(KID_SPECTRUM, s);
-      oaa::oaa_spectrum_kernel<<<blocks, thr, 0, s>>>(w, spec, K, C, n, 1, 1);
+      oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, spec, K, C, n, 1, 1);
       g_launches++;
       if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
     }
@@ -770,17 +773,16 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
     dp.Td = e.T;
     dp.off = off;
     dp.NCW = bd.NCW;
+    dp.RPC = bd.RPC;
+    dp.WSL = bd.WSL;
     cudaError_t err = launch_bwdd(n, dp, C, bd.smem, s);
     prof.stop();
     return err == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
   }
   if (wk.use) {
     if (!prepared) {
-      const long total = (long)K * C * ((g.P + 1) / 2) * g.H;
-      const int thr = 256;
-      const int blocks = (int)std::min<long>((total + thr - 1) / thr, 4096);
       KTimer kt(KID_SPECTRUM, s);
-      oaa::oaa_spectrum_kernel<<<blocks, thr, 0, s>>>(w, spec, K, C, n, 0, 1);
+      oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, spec, K, C, n, 0, 1);
       g_launches++;
       if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
     }
@@ -825,11 +827,8 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
   // kernel spectra: loop-major layout [Cloop][Cinner][P][H]
   const int loop_is_k = (is_fwd == e.S1) ? 1 : 0;  // fwd S1 / bwd_data S2 loop over k
   if (!prepared) {
-    const long total = (long)K * C * ((g.P + 1) / 2) * g.H;
-    const int thr = 256;
-    const int blocks = (int)std::min<long>((total + thr - 1) / thr, 4096);
     KTimer kt(KID_SPECTRUM, s);
-    oaa::oaa_spectrum_kernel<<<blocks, thr, 0, s>>>(w, spec, K, C, n, is_fwd ? 0 : 1, loop_is_k);
+    oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, spec, K, C, n, is_fwd ? 0 : 1, loop_is_k);
     g_launches++;
     if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
   }
@@ -918,7 +917,7 @@ oaa_status_t tc_filt_finalize(TcFilt& f, float* dw, int K, int C, cudaStream_t s
   const int n = f.n, bins = (2 * n - 1) * n;
   {
     KTimer kt(KID_FINALIZE, s);
-    oaa::oaa_filter_finalize_kernel<<<K * C, 128, sizeof(double2) * bins, s>>>(
+    oaa::oaa_filter_finalize_kernel<<<K * C, 512, sizeof(double2) * bins, s>>>(
         reinterpret_cast<const float2*>(f.part), dw, f.t.G, K, C, n);
   }
   g_launches++;
@@ -990,9 +989,9 @@ bool plan_bwd_fused(int B, int C, int K, int N, int n, oaa_crop_t crop, const Ge
     // SIMT family: both bodies fit 128 registers, ≤ 110 KB of shared memory and 256 TMEM
     // columns, and the weight-gradient CTA has the full 8 warps
     const TcPlan none{};
-    p->bd = plan_bwdd(false, C, g.M, n, none);
+    p->bd = plan_bwdd(false, B, C, g.M, n, none);
     p->bf = plan_bwdf(B, C, K, g.M, n);
-    const size_t bsm = oaa::bwdd_smem_bytes(n, C, p->bd.NCW);
+    const size_t bsm = oaa::bwdd_smem_bytes(n, C, p->bd.NCW, p->bd.RPC, p->bd.WSL);
     p->simt = B > 0 && p->bd.use && p->bf.use && p->bf.tm && p->bf.nwb == oaa::kBwdfWarps && bsm <= 110 * 1024 &&
               p->bf.smem <= 110 * 1024;
     if (p->simt) {
@@ -1034,7 +1033,7 @@ size_t oaa_conv_workspace_bytes(oaa_op_t op, int B, int C, int K, int N, int n, 
     const TcPlan tc = plan_tc(B, fwd ? C : K, fwd ? K : C, R, n);
     const int Ro = fwd ? g.M : N, off = fwd ? g.o : (n - 1 - g.o);
     const WalkHostGeo wk = plan_walk(fwd, B, fwd ? C : K, fwd ? K : C, cdiv(R, n), Ro, off, n, tc);
-    const BwddPlan bd = plan_bwdd(fwd, fwd ? K : C, R, n, tc);
+    const BwddPlan bd = plan_bwdd(fwd, B, fwd ? K : C, R, n, tc);
     return engine_ws(B, C, K, cdiv(R, n), g, tc, &wk, &bd).total;
   }
   if (op == OAA_OP_BWD) {
@@ -1074,7 +1073,7 @@ SpecPlan spec_plan(bool is_fwd, int C, int K, int N, int n, const Geo& g) {
   EnginePlan e;
   if (!plan_engine(R, Ro, off, n, Cin, Cout, &e, tc.use)) return sp;
   const WalkHostGeo wk = plan_walk(is_fwd, 1, Cin, Cout, e.T, Ro, off, n, tc);
-  const BwddPlan bd = plan_bwdd(is_fwd, Cout, R, n, tc);
+  const BwddPlan bd = plan_bwdd(is_fwd, 1, Cout, R, n, tc);
   (void)wk;
   (void)bd;
   sp.ok = true;
@@ -1116,16 +1115,15 @@ oaa_status_t oaa_conv_bwd(const float* x, const float* dy, const float* w, float
     const BwdfPlan& bf = fp.bf;
     if (cudaMemsetAsync(dx, 0, x_bytes, s) != cudaSuccess) return OAA_ERR_CUDA;
     {
-      const long total = (long)K * C * ((g.P + 1) / 2) * g.H;
-      const int blocks = (int)std::min<long>((total + 255) / 256, 4096);
       KTimer kt(KID_SPECTRUM, s);
-      oaa::oaa_spectrum_kernel<<<blocks, 256, 0, s>>>(w, spec, K, C, n, 1, 1);
+      oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, spec, K, C, n, 1, 1);
       g_launches++;
       if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
     }
     oaa::BwdDParams dp;
     dp.dy = dy; dp.spec = spec; dp.dx = dx; dp.B = B; dp.K = K; dp.C = C; dp.M = g.M; dp.N = N;
     dp.Td = cdiv(g.M, n); dp.off = n - 1 - g.o; dp.NCW = fp.bd.NCW;
+    dp.RPC = fp.bd.RPC; dp.WSL = fp.bd.WSL;
     oaa::XSpecParams xp;
     xp.in = x; xp.S = reinterpret_cast<float4*>(base + fp.data_b); xp.Cin = C; xp.R = N; xp.T = bf.Td;
     xp.NCH = bf.NCH; xp.SW = bf.SW; xp.org = g.o - (n - 1);
@@ -1135,7 +1133,7 @@ oaa_status_t oaa_conv_bwd(const float* x, const float* dy, const float* w, float
     if (launch_bwd_fused(n, xp, dp, pf, bf.xspec_smem, fp.smem, bf.G * bf.nkg, s) != cudaSuccess) return OAA_ERR_CUDA;
     {
       KTimer kt(KID_FINALIZE, s);
-      oaa::oaa_filter_finalize_kernel<<<K * C, 128, sizeof(double2) * g.P * g.H, s>>>(pf.partial, dw, bf.G, K, C, n);
+      oaa::oaa_filter_finalize_kernel<<<K * C, 512, sizeof(double2) * g.P * g.H, s>>>(pf.partial, dw, bf.G, K, C, n);
     }
     g_launches++;
     return cudaGetLastError() == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
@@ -1196,11 +1194,8 @@ oaa_status_t oaa_conv_fwd_oas(const float* x, const float* w, float* y, int B, i
   ProfScope prof(OAA_OP_FWD, s);
   prof.start();
   {
-    const long total = (long)K * C * ((g.P + 1) / 2) * g.H;
-    const int thr = 256;
-    const int blocks = (int)std::min<long>((total + thr - 1) / thr, 4096);
     KTimer kt(KID_SPECTRUM, s);
-    oaa::oaa_spectrum_kernel<<<blocks, thr, 0, s>>>(w, spec, K, C, n, 0, 1);
+    oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, spec, K, C, n, 0, 1);
     g_launches++;
     if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
   }
@@ -1293,7 +1288,7 @@ oaa_status_t oaa_conv_bwd_filter(const float* x, const float* dy, float* dw, int
     if (err != cudaSuccess) return OAA_ERR_CUDA;
     {
       KTimer kt(KID_FINALIZE, s);
-      oaa::oaa_filter_finalize_kernel<<<K * C, 128, sizeof(double2) * g.P * g.H, s>>>(fp.partial, dw, bf.G, K, C, n);
+      oaa::oaa_filter_finalize_kernel<<<K * C, 512, sizeof(double2) * g.P * g.H, s>>>(fp.partial, dw, bf.G, K, C, n);
     }
     g_launches++;
     return cudaGetLastError() == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
@@ -1330,7 +1325,7 @@ oaa_status_t oaa_conv_bwd_filter(const float* x, const float* dy, float* dw, int
   const int bins = g.P * g.H;
   {
     KTimer kt(KID_FINALIZE, s);
-    oaa::oaa_filter_finalize_kernel<<<K * C, 128, sizeof(double2) * bins, s>>>(
+    oaa::oaa_filter_finalize_kernel<<<K * C, 512, sizeof(double2) * bins, s>>>(
         static_cast<const float2*>(ws), dw, f.G, K, C, n);
   }
   g_launches++;
@@ -1376,11 +1371,9 @@ oaa_status_t oaa_weight_spectra(oaa_op_t op, const float* w, void* spec, size_t 
     EnginePlan e;
     plan_engine(R, Ro, off, n, Cin, Cout, &e, false);
     const WalkHostGeo wk = plan_walk(is_fwd, 1, Cin, Cout, e.T, Ro, off, n, tc);
-    const BwddPlan bd = plan_bwdd(is_fwd, Cout, R, n, tc);
+    const BwddPlan bd = plan_bwdd(is_fwd, 1, Cout, R, n, tc);
     const int loop_is_k = (wk.use || bd.use) ? 1 : ((is_fwd == e.S1) ? 1 : 0);
-    const long total = (long)K * C * ((g.P + 1) / 2) * g.H;
-    const int blocks = (int)std::min<long>((total + 255) / 256, 4096);
-    oaa::oaa_spectrum_kernel<<<blocks, 256, 0, s>>>(w, static_cast<float4*>(spec), K, C, n, is_fwd ? 0 : 1,
+    oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, static_cast<float4*>(spec), K, C, n, is_fwd ? 0 : 1,
                                                     loop_is_k);
   }
   g_launches++;

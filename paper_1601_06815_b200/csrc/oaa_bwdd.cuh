@@ -33,24 +33,27 @@ struct BwdDParams {
   const float4* spec;  // [K][C][P2][H] float4: DFT_P(flip180 w_kc)/P² (oaa_spectrum_kernel, flip, loop over k)
   float* dx;           // [B][C][N][N], zero on entry
   int B, K, C, M, N, Td, off;  // off = n−1−o: full-frame column/row of dx element 0
-  int NCW;                     // compute warps (chunks of the tile row)
+  int NCW;                     // chunk warps per tile row
+  int RPC;                     // (image, tile row) pairs per CTA: RPC·NCW ≤ 8 compute warps
+  int WSL;                     // log2 of the Ŵ ring depth (≤ kBwddWStages)
 };
 
 constexpr int kBwddStages = 8;    // per-warp dy ring depth (covers HBM latency)
-constexpr int kBwddWStages = 16;  // shared Ŵ ring depth: how far the fastest warp may run ahead
+constexpr int kBwddWStages = 16;  // max shared Ŵ ring depth: how far the fastest warp may run ahead
 
-__host__ __device__ constexpr size_t bwdd_dy_bytes(int n, int NCW) {
-  return (size_t)NCW * kBwddStages * n * ((32 / n) * n) * 4;
+__host__ __device__ constexpr size_t bwdd_dy_bytes(int n, int NCW, int RPC) {
+  return (size_t)RPC * NCW * kBwddStages * n * ((32 / n) * n) * 4;
 }
-__host__ __device__ constexpr size_t bwdd_q_bytes(int n, int NCW) {
-  return (size_t)(NCW * (32 / n) + 1) * n * (2 * n - 1) * 8;
+__host__ __device__ constexpr size_t bwdd_q_bytes(int n, int NCW, int RPC) {
+  return (size_t)RPC * (NCW * (32 / n) + 1) * n * (2 * n - 1) * 8;
 }
 // bytes of one Ŵ ring stage ([C][n][n] float4, padded to 128 B)
 __host__ __device__ constexpr int bwdd_w_bytes(int n, int C) { return (C * n * n * 16 + 127) & ~127; }
 // Ŵ ring | dy ring (the epilogue's Q buffer reuses the dy ring: the k loop is over by then)
-__host__ __device__ constexpr size_t bwdd_smem_bytes(int n, int C, int NCW) {
-  return (size_t)kBwddWStages * bwdd_w_bytes(n, C) +
-         (bwdd_dy_bytes(n, NCW) > bwdd_q_bytes(n, NCW) ? bwdd_dy_bytes(n, NCW) : bwdd_q_bytes(n, NCW));
+__host__ __device__ constexpr size_t bwdd_smem_bytes(int n, int C, int NCW, int RPC, int WSL) {
+  return ((size_t)1 << WSL) * bwdd_w_bytes(n, C) +
+         (bwdd_dy_bytes(n, NCW, RPC) > bwdd_q_bytes(n, NCW, RPC) ? bwdd_dy_bytes(n, NCW, RPC)
+                                                                  : bwdd_q_bytes(n, NCW, RPC));
 }
 
 __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
@@ -58,24 +61,32 @@ __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
 }
 
 // Shared memory: Ŵ ring [kBwddWStages][C][P2][H] float4 (bulk copies, refilled by the last
-// warp to release a stage) | per-warp dy ring [NCW][kBwddStages][n][CW] floats (each warp
-// stages the n rows of its own CW columns); the epilogue's Q [(NCW·TPW + 1) tiles][H][P]
-// float2 (last tile zero) reuses the dy ring.
+// warp to release a stage) | per-warp dy ring [RPC·NCW][kBwddStages][n][CW] floats (each warp
+// stages the n rows of its own CW columns); the epilogue's Q [RPC][(NCW·TPW + 1) tiles][H][P]
+// float2 (last tile of each pair zero) reuses the dy ring.
+// A CTA covers RPC consecutive (image, tile row) pairs (narrow images: several tile rows
+// or images per CTA, so that every CTA has up to 8 compute warps sharing one Ŵ ring);
+// compute warp w works on pair w / NCW, chunk w mod NCW.
 // TM = true: the C output spectra are accumulated in tensor memory (96 columns per warp)
 // instead of registers, so the kernel fits 128 registers and two CTAs share an SM.
 template <int NN, int CR, bool TM = false>
 __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
   using G = WalkGeo<NN>;
   constexpr int P = G::P, H = G::H, P2 = G::P2, TPW = G::TPW, QT = G::QT, CW = G::CW;
-  constexpr int S = kBwddStages, SW = kBwddWStages;
+  constexpr int S = kBwddStages;
   constexpr int DYS = NN * CW;                // floats per warp stage
+  const int SW = 1 << p.WSL, SWM = SW - 1;    // Ŵ ring depth (power of two)
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ uint64_t wfull[SW];
-  __shared__ int wrel[SW];
+  __shared__ uint64_t wfull[kBwddWStages];
+  __shared__ int wrel[kBwddWStages];
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int NCW = p.NCW;
-  const int b = item / p.Td, t1 = item - (item / p.Td) * p.Td;
+  const int NCW = p.NCW, NCWT = p.RPC * p.NCW;  // chunk warps per pair, compute warps
+  const int npairs = p.B * p.Td;
+  const int wpair = warp / NCW, wchunk = warp - (warp / NCW) * NCW;  // this warp's pair, chunk
+  const int pair = item * p.RPC + wpair;
+  const bool pair_ok = pair < npairs;
+  const int b = pair_ok ? pair / p.Td : 0, t1 = pair_ok ? pair - (pair / p.Td) * p.Td : 0;
   const int w4 = p.C * P2 * H;                // float4 of kernel spectra per dy channel
   const int wst = bwdd_w_bytes(NN, p.C);      // bytes per Ŵ stage
   unsigned char* Wring = smem_raw;
@@ -92,12 +103,12 @@ __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   float2* Q = reinterpret_cast<float2*>(dyring);  // epilogue only (aliases the dy ring)
-  const int ntile_q = NCW * TPW;  // tiles held in Q; tile ntile_q is the zero tile
+  const int ntile_q = NCW * TPW;  // tiles of one pair held in Q; tile ntile_q is its zero tile
 
   if (TM && warp == 0) {
     // warps w < 4 use columns [0, 128): narrow tile rows (≤ 4 chunk warps, N ≲ 128) take half
     // the columns, so up to 4 CTAs share an SM's 512
-    if (NCW <= 4)
+    if (NCWT <= 4)
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&s_tmem)));
     else
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&s_tmem)));
@@ -114,17 +125,17 @@ __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
   }
   // a CTA of 7 chunks is launched with one extra, idle warp (both CTAs of an SM then put
   // exactly two warps on each SMSP)
-  if (warp >= NCW) return;
-  auto w_wait = [&](int k) { mbar_wait(&wfull[k % SW], (k / SW) & 1); };
+  if (warp >= NCWT) return;
+  auto w_wait = [&](int k) { mbar_wait(&wfull[k & SWM], (k >> p.WSL) & 1); };
   auto w_release = [&](int k) {  // after __syncwarp: this warp is done with stage k % SW
     if (lane == 0) {
       // no membar here: it would also wait for this lane's in-flight dy cp.asyncs.  The
       // warp's reads of the stage are complete (their values were consumed before the
       // __syncwarp), and the atomic orders the warps' releases.
-      const int s = k % SW;
+      const int s = k & SWM;
       int old;
-      asm volatile("atom.shared.inc.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(&wrel[s])), "r"(NCW - 1) : "memory");
-      if (old == NCW - 1 && k + SW < p.K) {
+      asm volatile("atom.shared.inc.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(&wrel[s])), "r"(NCWT - 1) : "memory");
+      if (old == NCWT - 1 && k + SW < p.K) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&wfull[s], wbytes);
         bulk_g2s(Wring + (size_t)s * wst, p.spec + (size_t)(k + SW) * w4, wbytes, &wfull[s]);
@@ -136,8 +147,8 @@ __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
 
   // ---------------- compute warps: each stages its own columns of the n dy rows
   const size_t planeM = (size_t)p.M * p.M;
-  const int col = warp * CW + lane;                     // staged column (lane < CW)
-  const bool cok = lane < CW && col < p.M;
+  const int col = wchunk * CW + lane;                   // staged column (lane < CW)
+  const bool cok = pair_ok && lane < CW && col < p.M;
   int nrow = p.M - t1 * NN;                             // dy rows of this tile row inside dy
   nrow = nrow < NN ? nrow : NN;
   const float* src0 = p.dy + (size_t)b * p.K * planeM + (size_t)(t1 * NN) * p.M + (cok ? col : 0);
@@ -170,7 +181,7 @@ __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
 
   const int tt = lane / H, f1 = lane - (lane / H) * H;
   const bool laneA = tt < TPW;
-  const int t2 = warp * TPW + tt;
+  const int t2 = wchunk * TPW + tt;
   float cf[NN], sf[NN];
 #pragma unroll
   for (int p1 = 0; p1 < NN; ++p1) {
@@ -195,7 +206,7 @@ __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
 
   // TM: acc[c] row in TMEM (re at columns f, im at 16 + f) += Ŵᶠ·Ĝ; warp-collective
   auto accum_tm = [&](int k, const float (&gr)[P], const float (&gi)[P]) {
-    const float4* W = reinterpret_cast<const float4*>(Wring + (size_t)(k % SW) * wst) + f1;
+    const float4* W = reinterpret_cast<const float4*>(Wring + (size_t)(k & SWM) * wst) + f1;
     __syncwarp();
     tmem_wait_st();
 #pragma unroll
@@ -224,7 +235,7 @@ __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
     }
   };
   auto accum = [&](int k, const float (&gr)[P], const float (&gi)[P]) {
-    const float4* W = reinterpret_cast<const float4*>(Wring + (size_t)(k % SW) * wst) + f1;
+    const float4* W = reinterpret_cast<const float4*>(Wring + (size_t)(k & SWM) * wst) + f1;
 #pragma unroll
     for (int c = 0; c < CR; ++c) {
       if (c < p.C) {
@@ -299,13 +310,16 @@ __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
   cp_async_wait_all();
 
   // ---------------- epilogue: per output channel, inverse DFT + overlap-add into dx
-  const int nthr_c = 32 * NCW;
+  const int nthr_c = 32 * NCWT;
   // Q reuses the dy ring: every compute warp is past its last dy stage first
   asm volatile("bar.sync 1, %0;" ::"r"(nthr_c) : "memory");
-  for (int e = tid; e < QT; e += nthr_c) Q[ntile_q * QT + e] = make_float2(0.f, 0.f);
+  const int QP = (ntile_q + 1) * QT;  // float2 per pair in Q
+  for (int e = tid; e < p.RPC * QT; e += nthr_c) {
+    const int r = e / QT;
+    Q[r * QP + ntile_q * QT + (e - r * QT)] = make_float2(0.f, 0.f);
+  }
   const int FW = p.Td * NN + NN - 1;  // full-frame width
   const size_t planeN = (size_t)p.N * p.N;
-  const int I0 = t1 * NN - p.off;     // dx row of block row 0
 #pragma unroll
   for (int c = 0; c < CR; ++c) {
     if (c >= p.C) break;
@@ -326,19 +340,23 @@ __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
     if (laneA) {
       float qr[P], qi[P];
       dft<P, +1>(er, ei, qr, qi);
-      float2* qd = Q + t2 * QT + f1 * P;
-      const bool real_tile = t2 < p.Td;
+      float2* qd = Q + wpair * QP + t2 * QT + f1 * P;
+      const bool real_tile = pair_ok && t2 < p.Td;
 #pragma unroll
       for (int p2 = 0; p2 < P; ++p2) qd[p2] = real_tile ? make_float2(qr[p2], qi[p2]) : make_float2(0.f, 0.f);
     }
     asm volatile("bar.sync 1, %0;" ::"r"(nthr_c) : "memory");  // Q complete
-    float* dxc = p.dx + ((size_t)b * p.C + c) * planeN;
-    for (int J = tid; J < FW; J += nthr_c) {
+    for (int e = tid; e < p.RPC * FW; e += nthr_c) {
+      const int r = e / FW, J = e - (e / FW) * FW;
+      const int pr = item * p.RPC + r;
       const int j = J - p.off;
-      if (j < 0 || j >= p.N) continue;
+      if (pr >= npairs || j < 0 || j >= p.N) continue;
+      const int pb = pr / p.Td, pt1 = pr - (pr / p.Td) * p.Td;
+      float* dxc = p.dx + ((size_t)pb * p.C + c) * planeN;
+      const int I0 = pt1 * NN - p.off;  // dx row of block row 0
       const int tA = J / NN, pA = J - (J / NN) * NN;
-      const int offA = (tA < p.Td ? tA : ntile_q) * QT + pA;
-      const int offB = (pA <= NN - 2 && tA >= 1) ? (tA - 1) * QT + pA + NN : ntile_q * QT;
+      const int offA = r * QP + (tA < p.Td ? tA : ntile_q) * QT + pA;
+      const int offB = r * QP + ((pA <= NN - 2 && tA >= 1) ? (tA - 1) * QT + pA + NN : ntile_q * QT);
       float zr[H], zi[H];
 #pragma unroll
       for (int f = 0; f < H; ++f) {
@@ -359,7 +377,7 @@ __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     asm volatile("bar.sync 1, %0;" ::"r"(nthr_c) : "memory");
     if (warp == 0) {
-      if (NCW <= 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(s_tmem));
+      if (NCWT <= 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(s_tmem));
       else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(s_tmem));
     }
   }

@@ -1250,36 +1250,65 @@ __global__ void __launch_bounds__(kMaxThreads, 1) oaa_bwd_filter_kernel(const Fi
 }
 
 #ifdef OAA_DEFINE_AUX_KERNELS  // defined in exactly one translation unit (oaa_abi.cu)
-// partial[G][K][C][P][H] → dw[K][C][n][n].  One CTA per (k, c).
-__global__ void oaa_filter_finalize_kernel(const float2* __restrict__ partial, float* __restrict__ dw,
-                                           int G, int K, int C, int n) {
+// partial[G][K][C][P][H] → dw[K][C][n][n].  One CTA of 512 threads per (k, c): thread
+// (j, t) sums the partial spectra g ≡ j (mod 4) of bin t in fp64 (four interleaved chains,
+// so 16 L2 loads per bin are in flight), the four sums are combined in a fixed order --
+// bitwise reproducible -- then the inverse DFT and lag read-out.
+__global__ void __launch_bounds__(512) oaa_filter_finalize_kernel(const float2* __restrict__ partial,
+                                                                  float* __restrict__ dw, int G, int K, int C,
+                                                                  int n) {
   const int P = 2 * n - 1, H = n, bins = P * H;
   const int kc = blockIdx.x;
   extern __shared__ double2 S[];  // [P][H]
   __shared__ double tc[16], ts[16];  // cos / sin (2π m / P)
+  __shared__ double2 part[4][128];
   if (threadIdx.x < P) sincospi(2.0 * (double)threadIdx.x / (double)P, &ts[threadIdx.x], &tc[threadIdx.x]);
-  for (int t = threadIdx.x; t < bins; t += blockDim.x) {
-    double sr = 0.0, si = 0.0;
-    for (int g = 0; g < G; ++g) {
-      const float2 v = partial[((size_t)g * K * C + kc) * bins + t];
-      sr += (double)v.x;
-      si += (double)v.y;
+  const size_t gstride = (size_t)K * C * bins;
+  {
+    const int j = threadIdx.x >> 7, t = threadIdx.x & 127;
+    if (t < bins) {
+      const float2* src = partial + (size_t)kc * bins + t;
+      double sr[4] = {0.0, 0.0, 0.0, 0.0}, si[4] = {0.0, 0.0, 0.0, 0.0};
+      int g = j;
+      for (; g + 12 < G; g += 16) {
+        float2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldg(src + (size_t)(g + 4 * u) * gstride);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { sr[u] += (double)v[u].x; si[u] += (double)v[u].y; }
+      }
+      for (int u = 0; g < G; g += 4, ++u) {
+        const float2 v = __ldg(src + (size_t)g * gstride);
+        sr[u] += (double)v.x;
+        si[u] += (double)v.y;
+      }
+      part[j][t] = make_double2((sr[0] + sr[1]) + (sr[2] + sr[3]), (si[0] + si[1]) + (si[2] + si[3]));
     }
-    S[t] = make_double2(sr, si);
   }
+  __syncthreads();
+  for (int t = threadIdx.x; t < bins; t += blockDim.x)
+    S[t] = make_double2((part[0][t].x + part[1][t].x) + (part[2][t].x + part[3][t].x),
+                        (part[0][t].y + part[1][t].y) + (part[2][t].y + part[3][t].y));
   __syncthreads();
   const double inv = 1.0 / ((double)P * (double)P);
   for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
     const int u = t / n, v = t - (t / n) * n;
     const int l1 = n - 1 - u, l2 = n - 1 - v;
     double acc = 0.0;
+    int m1 = 0;  // f1·l1 mod P, kept incrementally
     for (int f1 = 0; f1 < H; ++f1) {
       const double wgt = (f1 == 0) ? 1.0 : 2.0;
+      double a = 0.0;
+      int m = m1;  // (f1·l1 + f2·l2) mod P
       for (int f2 = 0; f2 < P; ++f2) {
-        const int m = (f1 * l1 + f2 * l2) % P;
         const double2 z = S[f2 * H + f1];
-        acc += wgt * (z.x * tc[m] - z.y * ts[m]);
+        a += z.x * tc[m] - z.y * ts[m];
+        m += l2;
+        if (m >= P) m -= P;
       }
+      acc += wgt * a;
+      m1 += l1;
+      if (m1 >= P) m1 -= P;
     }
     dw[(size_t)kc * n * n + t] = (float)(acc * inv);
   }
@@ -1287,48 +1316,66 @@ __global__ void oaa_filter_finalize_kernel(const float2* __restrict__ partial, f
 
 // spec4[((a·Binner + bb)·P2 + f2/2)·H + f1].{xy|zw} = DFT_P(w_kc or flip180(w_kc))[f1][f2] / P²
 // with (k, c) = loop_is_k ? (a, bb) : (bb, a); the odd last f2 slot is zero.
-__global__ void oaa_spectrum_kernel(const float* __restrict__ w, float4* __restrict__ spec, int K,
-                                    int C, int n, int flip, int loop_is_k) {
+// One CTA per (k, c) pair (grid = K·C): the n×n kernel is staged in fp64, the row DFT
+// R[p1][f2] = Σ_p2 v[p1][p2]·e^{−2πi f2 p2/P} (n terms) goes to shared memory, then each
+// bin pair is Σ_p1 R[p1][f]·e^{−2πi f1 p1/P} (n terms) -- the separable 2-D DFT, fp64
+// throughout, rounded to fp32 once.
+__global__ void __launch_bounds__(128) oaa_spectrum_kernel(const float* __restrict__ w, float4* __restrict__ spec,
+                                                           int K, int C, int n, int flip, int loop_is_k) {
   const int P = 2 * n - 1, H = n, P2 = (P + 1) / 2;
   __shared__ double tc[16], ts[16];  // cos / sin (2π m / P), fp64
-  if (threadIdx.x < P) sincospi(2.0 * (double)threadIdx.x / (double)P, &ts[threadIdx.x], &tc[threadIdx.x]);
+  __shared__ double v[64];           // the kernel (flipped for bwd_data)
+  __shared__ double Rr[8 * 15], Ri[8 * 15];
+  const int tid = threadIdx.x;
+  const int kc = blockIdx.x;  // = k·C + c
+  const int k = kc / C, c = kc - (kc / C) * C;
+  const float* wk = w + (size_t)kc * n * n;
+  if (tid < P) sincospi(2.0 * (double)tid / (double)P, &ts[tid], &tc[tid]);
+  if (tid < n * n) {
+    const int p1 = tid / n, p2 = tid - (tid / n) * n;
+    v[tid] = (double)(flip ? wk[(n - 1 - p1) * n + (n - 1 - p2)] : wk[tid]);
+  }
   __syncthreads();
-  const long total = (long)K * C * P2 * H;
-  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total;
-       t += (long)gridDim.x * blockDim.x) {
-    const int f1 = (int)(t % H);
-    const int q = (int)((t / H) % P2);
-    const long ab = t / ((long)H * P2);
-    int k, c;
-    if (loop_is_k) { k = (int)(ab / C); c = (int)(ab % C); }
-    else { c = (int)(ab / K); k = (int)(ab % K); }
-    const float* wk = w + ((size_t)k * C + c) * n * n;
-    // both bins f2 = 2q, 2q+1 of the pair in one pass (two independent fp64 chains), the
-    // twiddle index (f1·p1 + f2·p2) mod P kept incrementally (no integer division); the
-    // terms are summed in the same (p1, p2) order as the plain double loop
-    const int fa = 2 * q, fb = 2 * q + 1 < P ? 2 * q + 1 : 0;
-    double sra = 0.0, sia = 0.0, srb = 0.0, sib = 0.0;
-    int m1 = 0;
-    for (int p1 = 0; p1 < n; ++p1) {
-      int ma = m1, mb = m1;
-      for (int p2 = 0; p2 < n; ++p2) {
-        const float v = flip ? wk[(n - 1 - p1) * n + (n - 1 - p2)] : wk[p1 * n + p2];
-        sra += (double)v * tc[ma];
-        sia -= (double)v * ts[ma];
-        srb += (double)v * tc[mb];
-        sib -= (double)v * ts[mb];
-        ma += fa;
-        if (ma >= P) ma -= P;
-        mb += fb;
-        if (mb >= P) mb -= P;
-      }
-      m1 += f1;
-      if (m1 >= P) m1 -= P;
+  if (tid < n * P) {
+    const int p1 = tid / P, f2 = tid - (tid / P) * P;
+    double sr = 0.0, si = 0.0;
+    int m = 0;  // f2·p2 mod P
+    for (int p2 = 0; p2 < n; ++p2) {
+      const double x = v[p1 * n + p2];
+      sr += x * tc[m];
+      si -= x * ts[m];
+      m += f2;
+      if (m >= P) m -= P;
     }
-    const double inv = 1.0 / ((double)P * (double)P);
-    const bool hb = 2 * q + 1 < P;
-    spec[t] = make_float4((float)(sra * inv), (float)(sia * inv), hb ? (float)(srb * inv) : 0.f,
-                          hb ? (float)(sib * inv) : 0.f);
+    Rr[tid] = sr;
+    Ri[tid] = si;
+  }
+  __syncthreads();
+  const double inv = 1.0 / ((double)P * (double)P);
+  const int a = loop_is_k ? k : c, bb = loop_is_k ? c : k, Binner = loop_is_k ? C : K;
+  float4* dst = spec + (size_t)(a * Binner + bb) * P2 * H;
+  for (int t = tid; t < P2 * H; t += blockDim.x) {
+    const int q = t / H, f1 = t - (t / H) * H;
+    const int fa = 2 * q, fb = 2 * q + 1;
+    const bool hb = fb < P;
+    double sra = 0.0, sia = 0.0, srb = 0.0, sib = 0.0;
+    int m = 0;  // f1·p1 mod P
+    for (int p1 = 0; p1 < n; ++p1) {
+      const double c0 = tc[m], s0 = ts[m];
+      // (R · e^{−iθ}) = (Rr c + Ri s) + i (Ri c − Rr s)
+      const double ar = Rr[p1 * P + fa], ai = Ri[p1 * P + fa];
+      sra += ar * c0 + ai * s0;
+      sia += ai * c0 - ar * s0;
+      if (hb) {
+        const double br = Rr[p1 * P + fb], bi = Ri[p1 * P + fb];
+        srb += br * c0 + bi * s0;
+        sib += bi * c0 - br * s0;
+      }
+      m += f1;
+      if (m >= P) m -= P;
+    }
+    dst[t] = make_float4((float)(sra * inv), (float)(sia * inv), hb ? (float)(srb * inv) : 0.f,
+                         hb ? (float)(sib * inv) : 0.f);
   }
 }
 #endif  // OAA_DEFINE_AUX_KERNELS

@@ -243,7 +243,8 @@ cudaError_t launch_bwdd_n(const oaa::BwdDParams& p, int cr, size_t smem, cudaStr
   if (err != cudaSuccess) return err;
   {
     KTimer kt(KID_BWDD, s);
-    k<<<p.B * p.Td, 32 * (p.NCW == 7 ? 8 : p.NCW), smem, s>>>(p);
+    const int ncwt = p.RPC * p.NCW;
+    k<<<(p.B * p.Td + p.RPC - 1) / p.RPC, 32 * (ncwt == 7 ? 8 : ncwt), smem, s>>>(p);
   }
   g_launches++;
   return cudaGetLastError();
@@ -298,7 +299,7 @@ cudaError_t launch_bwd_fused_n(const oaa::XSpecParams& xp, const oaa::BwdDParams
   if (err != cudaSuccess) return err;
   {
     KTimer kt(KID_BWD_FUSED, s);
-    k<<<nf + pd.B * pd.Td, 256, smem, s>>>(pd, pf, nf, pf.G);
+    k<<<nf + (pd.B * pd.Td + pd.RPC - 1) / pd.RPC, 256, smem, s>>>(pd, pf, nf, pf.G);
   }
   g_launches++;
   return cudaGetLastError();

@@ -394,6 +394,26 @@ def test_fused_backward(B, C, K, N, n, crop):
     assert torch.equal(dx2, dx) and torch.equal(dw2, dw)  # deterministic
 
 
+@pytest.mark.parametrize("B,N,n,crop", [(85, 60, 8, "valid"), (75, 64, 8, "same"), (40, 120, 8, "valid"),
+                                        (97, 45, 5, "full")])
+def test_bwd_data_several_pairs_per_cta(B, N, n, crop):
+    """Narrow images: bwd_data puts several (image, tile row) pairs in one CTA (8 compute
+    warps sharing one kernel-spectrum ring); B·T′ is chosen so that the pairs
+    per CTA is 2-4 and the last CTA is ragged.  dx of every element against the oracle, and
+    the fused backward's dx bitwise equal to it."""
+    C, K = 3, 64
+    d = make_inputs(B, C, K, N, n, crop, seed=B + N + n)
+    w = torch.from_numpy(d["w"]).cuda()
+    dy = torch.from_numpy(d["dy"]).cuda()
+    x = torch.from_numpy(d["x"]).cuda()
+    dx = oaa.conv_bwd_data(dy, w, N, crop)
+    dxf, dwf = oaa.conv_bwd(x, dy, w, crop)
+    torch.cuda.synchronize()
+    check(dx.cpu().numpy(), oracle.conv_bwd_data(d["dy"], d["w"], N, crop), "bwd_data")
+    assert torch.equal(dx, dxf)
+    check(dwf.cpu().numpy(), oracle.conv_bwd_filter(d["x"], d["dy"], n, crop), "fused dw")
+
+
 def test_cuda_graph_capture_replays_bitwise():
     """The library only enqueues kernels, memsets and attribute calls on the caller's
     stream (no allocation, no synchronisation; include/oaa.h), so a whole step can be
