@@ -1,5 +1,7 @@
 // oaa_abi.cu -- host side of liboaa.so: argument validation, planning, workspace layout
 // and kernel launches behind the C ABI declared in include/oaa.h.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -25,6 +27,43 @@ using namespace oaa_host;
 constexpr size_t kAlign = 256;
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+// ------------------------------------------------------------------ TMA tensor maps
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link); the
+// lookup runs once (thread-safe static initialisation).
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+// The x-block / x-window tiler of oaa_xspec_kernel: x viewed as [B·Cin][R][R] (dim 0 =
+// columns), box {SW, rows, Cin} at (org, t1·n + org, b·Cin), out-of-bounds elements
+// zero-filled -- the zero padding of PAPER.md:18 done by the TMA unit.  TMA needs 16-byte
+// global strides (R a multiple of 4), box dimensions ≤ 256 and a non-negative box origin
+// (measured: a window origin o − (n−1) < 0, i.e. Full / Same x-windows, faults with an
+// illegal instruction); otherwise the kernel stages the rows with per-element cp.async
+// zero fill (tma = 0).
+void set_xspec_tma(oaa::XSpecParams& xp, int B, int rows) {
+  xp.tma = 0;
+  const PFN_cuTensorMapEncodeTiled_v12000 enc = tmap_encoder();
+  if (!enc || B < 1 || xp.org != 0 || xp.R % 4 != 0 || xp.SW % 4 != 0 || xp.SW > 256 || rows > 256 || xp.Cin > 256 ||
+      (reinterpret_cast<uintptr_t>(xp.in) & 15) != 0)
+    return;
+  const cuuint64_t dims[3] = {(cuuint64_t)xp.R, (cuuint64_t)xp.R, (cuuint64_t)B * xp.Cin};
+  const cuuint64_t strides[2] = {(cuuint64_t)xp.R * 4, (cuuint64_t)xp.R * xp.R * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)xp.SW, (cuuint32_t)rows, (cuuint32_t)xp.Cin};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = enc(&xp.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(xp.in), dims, strides, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  xp.tma = r == CUDA_SUCCESS ? 1 : 0;
+}
 
 // ------------------------------------------------------------------ profiling
 struct ProfRec {
@@ -795,6 +834,7 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
     xp.NCH = wk.NCH;
     xp.SW = wk.NCH * wk.CW;
     xp.org = 0;
+    set_xspec_tma(xp, B, n);
     oaa::WalkParams wp;
     wp.S = xp.S;
     wp.spec = spec;
@@ -1127,6 +1167,7 @@ oaa_status_t oaa_conv_bwd(const float* x, const float* dy, const float* w, float
     oaa::XSpecParams xp;
     xp.in = x; xp.S = reinterpret_cast<float4*>(base + fp.data_b); xp.Cin = C; xp.R = N; xp.T = bf.Td;
     xp.NCH = bf.NCH; xp.SW = bf.SW; xp.org = g.o - (n - 1);
+    set_xspec_tma(xp, B, 2 * n - 1);
     oaa::BwdFParams pf;
     pf.dy = dy; pf.XS = xp.S; pf.partial = reinterpret_cast<float2*>(base + fp.data_b + bf.xs_b); pf.B = B; pf.K = K;
     pf.C = C; pf.M = g.M; pf.Td = bf.Td; pf.NCH = bf.NCH; pf.G = bf.G; pf.KG = bf.KG;
@@ -1208,6 +1249,7 @@ oaa_status_t oaa_conv_fwd_oas(const float* x, const float* w, float* y, int B, i
   xp.NCH = o.NCH;
   xp.SW = o.SW;
   xp.org = g.o - (n - 1);  // window of output block t: input rows from t·n + o − (n−1)
+  set_xspec_tma(xp, B, 2 * n - 1);
   oaa::WalkParams wp{};
   wp.S = xp.S;
   wp.spec = spec;
@@ -1269,6 +1311,7 @@ oaa_status_t oaa_conv_bwd_filter(const float* x, const float* dy, float* dw, int
     xp.NCH = bf.NCH;
     xp.SW = bf.SW;
     xp.org = g.o - (n - 1);
+    set_xspec_tma(xp, B, 2 * n - 1);
     oaa::BwdFParams fp;
     fp.dy = dy;
     fp.XS = xp.S;

@@ -317,7 +317,46 @@ __global__ void __launch_bounds__(tc_threads<CONV>(), 1) oaa_bin_gemm_kernel(con
           }
         }
       }
-      if (p.mode == 2 && active) {
+      if (p.mode == 2 && active && p.TT % p.TPW == 0 && p.SBL == 5) {
+        // walker layout with walker slot = GEMM column (whole walker chunks per tile row):
+        // a 32-column chunk of the tile is one 32-slot block, i.e. per row one 128-byte run
+        // D[o·plane + blk·2·bf8 + ri·bf8 + f·32 + 0..31].  The warp's 32 rows × 32 columns go
+        // through its XOR-swizzled 4 KB buffer (float4 j of row r at r·8 + (j ^ (r & 7)):
+        // conflict-free both ways), then 8 lanes write each row run with 16-byte stores --
+        // 4 full runs per store instruction.
+        float4* tb4 = reinterpret_cast<float4*>(smem_raw + kTcStages * kTcStageBytes) + (warp - 2) * 256;
+        const int nc = min(128, T.ncols - cb), nr = min(32, T.mrows - 32 * q);
+        const long long bf8 = (long long)p.SB * p.H * p.P;
+        const int sub = lane >> 3, ch = lane & 7;
+        float* dbin = p.D + (long long)T.f * p.SB + 4 * ch;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            tb4[lane * 8 + (j ^ (lane & 7))] =
+                make_float4(acc[32 * c + 4 * j], acc[32 * c + 4 * j + 1], acc[32 * c + 4 * j + 2], acc[32 * c + 4 * j + 3]);
+          __syncwarp();
+          const int col0 = 32 * c + 4 * ch;  // tile column of this lane's 4 values
+          const long long blk = (long long)((T.n0 + cb + 32 * c) >> 5) * 2 * bf8;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = 4 * i + sub;
+            if (r < nr && col0 < nc) {
+              const float4 v = tb4[r * 8 + (ch ^ (r & 7))];
+              const int m = T.m0 + 32 * q + r, ri = m >= p.Cf;
+              float* dst = dbin + (long long)(m - (ri ? p.Cf : 0)) * p.plane + (ri ? bf8 : 0) + blk;
+              if (col0 + 3 < nc) {
+                __stcg(reinterpret_cast<float4*>(dst), v);
+              } else {
+                __stcg(dst, v.x);
+                if (col0 + 1 < nc) __stcg(dst + 1, v.y);
+                if (col0 + 2 < nc) __stcg(dst + 2, v.z);
+              }
+            }
+          }
+        }
+      } else if (p.mode == 2 && active) {
         // walker layout: per bin an SB-float run of slots; transpose 32 columns at a time
         float* tb = reinterpret_cast<float*>(smem_raw + kTcStages * kTcStageBytes) + (warp - 2) * 32 * 33;
         const int nc = min(128, T.ncols - cb);

@@ -25,6 +25,7 @@
 // bulk copies (TMA engine); the last warp to release a slot issues the copy that refills
 // it, so there is no producer warp and no CTA barrier in the steady state.
 #pragma once
+#include <cuda.h>  // CUtensorMap (the tensor map itself is encoded on the host, oaa_abi.cu)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -52,10 +53,16 @@ struct WalkGeo {
 //   WIN = true : the (2n−1)² x-window at (t1·n + org, t2·n + org) correlated with the dy
 //                block in the weight gradient, full DFT.
 struct XSpecParams {
+  // TMA tensor map of `in` viewed as [B·Cin][R][R] (3-D, dim 0 = columns), box
+  // {SW, rows, Cin}, out-of-bounds elements zero-filled: one cp.async.bulk.tensor per CTA
+  // stages the zero-padded rows of all channels (the block tiler/padder of PAPER.md:18);
+  // tma == 0 (R not a multiple of 4, SW > 256): per-element cp.async with zero fill.
+  CUtensorMap tmap;
   const float* in;  // [B][Cin][R][R]
   float4* S;        // chunked spectra
   int Cin, R, T, NCH, SW;  // T tile rows (and columns), SW = staged row width
   int org;                 // window origin offset (WIN only)
+  int tma;
 };
 
 // One CTA per (image, tile row): the rows of every channel are staged (zero padded),
@@ -70,7 +77,7 @@ inline size_t xspec_smem_bytes(int Cin, int rows, int SW, int CH4) {
 }
 
 template <int NN, bool WIN>
-__global__ void __launch_bounds__(256) oaa_xspec_kernel(const XSpecParams p) {
+__global__ void __launch_bounds__(256) oaa_xspec_kernel(const __grid_constant__ XSpecParams p) {
   using G = WalkGeo<NN>;
   constexpr int P = G::P, H = G::H, RS4 = G::RS4;
   constexpr int ROWS = WIN ? P : NN;
@@ -86,7 +93,23 @@ __global__ void __launch_bounds__(256) oaa_xspec_kernel(const XSpecParams p) {
   const int b = item / p.T, t1 = item - (item / p.T) * p.T;
   const float* in_b = p.in + (size_t)b * p.Cin * p.R * p.R;
   const int org = WIN ? p.org : 0;
-  {
+  if (p.tma) {
+    __shared__ uint64_t tbar;
+    if (tid == 0) {
+      mbar_init(&tbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(&tbar, (uint32_t)(p.SW * ROWS * p.Cin * 4));
+      // box origin: column org, row t1·n + org, channel plane b·Cin (negative / past-the-end
+      // coordinates are the zero padding)
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+              smem_u32(rows_s)),
+          "l"(reinterpret_cast<uint64_t>(&p.tmap)), "r"(org), "r"(t1 * NN + org), "r"(b * p.Cin), "r"(smem_u32(&tbar))
+          : "memory");
+    }
+    __syncthreads();  // (the barrier init is visible before anyone waits)
+    mbar_wait(&tbar, 0);
+  } else {
     const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
     for (int sg = warp; sg < p.Cin * ROWS; sg += nw) {
       const int c = sg / ROWS, rr = sg - (sg / ROWS) * ROWS;
@@ -347,7 +370,12 @@ __global__ void __launch_bounds__(256, (LOAD && NN <= 6) ? 2 : 1) oaa_walk_kerne
             if (c < p.Cin) {
 #pragma unroll
               for (int q = 0; q < P2; ++q) {
+#ifdef OAA_EXP_NOXLD  // experiment builds only: X̂ from registers instead of shared memory (timing)
+                const float fs = __int_as_float(0x3f800000 + (seq << 4) + c + q);
+                const float4 x = make_float4(fs, -fs, fs * 0.5f, fs + 1.f);
+#else
                 const float4 x = xs[c * G::CH4 + q];
+#endif
                 const float4 w = Wr[c][q];
                 const int f = 2 * q;
                 if (c == 0) {
