@@ -61,6 +61,11 @@
 #ifdef __cplusplus
 extern "C" {
 #endif
+/* liboaa.so is built with hidden default visibility: exactly the declarations below are
+   exported. */
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
 
 typedef enum { OAA_CROP_FULL = 0, OAA_CROP_VALID = 1, OAA_CROP_SAME = 2 } oaa_crop_t;
 
@@ -189,6 +194,10 @@ int oaa_profile_collect(double* ms, int* count);
 int oaa_profile_kernel_count(void);
 const char* oaa_profile_kernel_name(int id);
 int oaa_profile_collect_kernels(double* ms, int* count, int n);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
 
 #ifdef __cplusplus
 }
