@@ -65,6 +65,27 @@ void set_xspec_tma(oaa::XSpecParams& xp, int B, int rows) {
   xp.tma = r == CUDA_SUCCESS ? 1 : 0;
 }
 
+// Ŷ of the tensor-core path (bin GEMM mode 2, walker slot = GEMM column): D viewed as the 5-D
+// tensor [o][blk][ri][f][32 slots], box {32, 1, 1, 1, 32} (one drain warp's 32 rows × 32 slots),
+// 128-byte swizzle (the drain buffer's XOR layout).  Needs whole 32-row groups per ri (Cf a
+// multiple of 32); otherwise the drain warps store with st.global (dtma = 0).
+void set_gemm_dmap(oaa::BinGemmParams& gp, long long nblk) {
+  gp.dtma = 0;
+  const PFN_cuTensorMapEncodeTiled_v12000 enc = tmap_encoder();
+  if (!enc || gp.mode != 2 || gp.SBL != 5 || gp.TT % gp.TPW != 0 || gp.Cf % 32 != 0 || nblk < 1 ||
+      (reinterpret_cast<uintptr_t>(gp.D) & 15) != 0)
+    return;
+  const long long bf8 = (long long)gp.SB * gp.H * gp.P;
+  const cuuint64_t dims[5] = {32, (cuuint64_t)gp.H * gp.P, 2, (cuuint64_t)nblk, (cuuint64_t)gp.Cf};
+  const cuuint64_t strides[4] = {32 * 4, (cuuint64_t)bf8 * 4, (cuuint64_t)bf8 * 8, (cuuint64_t)gp.plane * 4};
+  const cuuint32_t box[5] = {32, 1, 1, 1, 32};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  const CUresult r = enc(&gp.dmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, gp.D, dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  gp.dtma = r == CUDA_SUCCESS ? 1 : 0;
+}
+
 // ------------------------------------------------------------------ profiling
 struct ProfRec {
   int op;
@@ -726,6 +747,7 @@ oaa_status_t tc_data_chunk(TcData& d, int b0, int bc, cudaStream_t s) {
   gp.ldd = (int)btc;
   gp.strideD = (long long)gp.M * btc;
   gp.plane = ((long long)bc * T * gp.NT4 * gp.TPW + gp.SB - 1) / gp.SB * 2 * d.F * gp.SB;
+  set_gemm_dmap(gp, ((long long)bc * T * gp.NT4 * gp.TPW + gp.SB - 1) / gp.SB);
   if (launch_bin_gemm(gp, s) != cudaSuccess) return OAA_ERR_CUDA;
   d.wp.B = bc;
   d.wp.b0 = b0;

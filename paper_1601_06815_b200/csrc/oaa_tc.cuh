@@ -25,6 +25,7 @@
 //     .kind::tf32 (M=128, N=256, K=8) and commits them to the stage's "empty" mbarrier;
 //   * all 4 warps: epilogue, tcgen05.ld of the 128 × 256 fp32 accumulator (thread = row).
 #pragma once
+#include <cuda.h>  // CUtensorMap (encoded on the host, oaa_abi.cu)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -44,6 +45,11 @@ constexpr size_t kTcStageBytes = (size_t)(2 * kTcM + 2 * kTcN) * kTcK * sizeof(f
 constexpr size_t kTcSmem = kTcStages * kTcStageBytes + 8 * 32 * 33 * sizeof(float);  // + epilogue transpose buffers
 
 struct BinGemmParams {
+  // mode 2 with dtma: TMA tensor map of D as the 5-D tensor [o][blk][ri][f][32 slots]
+  // (dims {32, F, 2, blocks, Cf}); the drain warps store each 32-row × 32-slot sub-tile with
+  // one cp.async.bulk.tensor from their 128-byte-swizzled shared buffer
+  CUtensorMap dmap;
+  int dtma;
   const float* A;  // blocked [F][Kc][2][RTA][4096]
   const float* B;  // blocked [F][Kc][2][RTB][4096]  (RTB even)
   float* D;        // [F][M][ldd] (row m, column n)
@@ -114,7 +120,7 @@ template <bool CONV> constexpr int tc_threads() { return CONV ? 384 : 320; }
 // Two TMEM accumulators of 256 columns alternate per group of kTcDrain K chunks, so the
 // MMAs of group g+1 run while the epilogue warps drain group g.
 template <bool CONV>
-__global__ void __launch_bounds__(tc_threads<CONV>(), 1) oaa_bin_gemm_kernel(const BinGemmParams p) {
+__global__ void __launch_bounds__(tc_threads<CONV>(), 1) oaa_bin_gemm_kernel(const __grid_constant__ BinGemmParams p) {
   // Persistent: CTA b takes output tiles b, b + gridDim.x, ...  (tile order: M tiles of one
   // (bin, N tile) first, so their shared B operand is re-read from L2).  The smem stage ring
   // and the two TMEM accumulators carry on across tiles: the drain warps write tile t while
@@ -212,9 +218,11 @@ __global__ void __launch_bounds__(tc_threads<CONV>(), 1) oaa_bin_gemm_kernel(con
             const uint64_t dal = umma_desc_kmajor(a_lo + koff, 128, 1024);
             const uint64_t dbh = umma_desc_kmajor(b_hi + koff, 128, 1024);
             const uint64_t dbl = umma_desc_kmajor(b_lo + koff, 128, 1024);
+#ifndef OAA_EXP_TC_NOMMA  // experiment builds only (timing): no MMAs
             umma_tf32(acc_t, dal, dbh, idesc, (first && ks == 0) ? 0u : 1u);
             umma_tf32(acc_t, dah, dbl, idesc, 1u);
             umma_tf32(acc_t, dah, dbh, idesc, 1u);
+#endif
           }
           umma_commit(&empty[s]);
           if ((ch % kTcDrain) == kTcDrain - 1 || ch == T.nk - 1) umma_commit(&accf[buf]);
@@ -247,7 +255,11 @@ __global__ void __launch_bounds__(tc_threads<CONV>(), 1) oaa_bin_gemm_kernel(con
           h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
           l = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
         };
+#ifdef OAA_EXP_TC_NOCONV  // experiment builds only (timing): converters skip the split
+        if (false) {
+#else
         if (!p.a_split) {
+#endif
 #pragma unroll 4
           for (int e = ct; e < 1024; e += 64) {
             float4 h, l;
@@ -256,8 +268,12 @@ __global__ void __launch_bounds__(tc_threads<CONV>(), 1) oaa_bin_gemm_kernel(con
             al[e] = l;
           }
         }
+#ifdef OAA_EXP_TC_NOCONV
+        for (int e = ct; e < 0; e += 64) {
+#else
 #pragma unroll 4
         for (int e = ct; e < nb4; e += 64) {
+#endif
           float4 h, l;
           split4(h, l, bh[e]);
           bh[e] = h;
@@ -329,16 +345,38 @@ __global__ void __launch_bounds__(tc_threads<CONV>(), 1) oaa_bin_gemm_kernel(con
         const long long bf8 = (long long)p.SB * p.H * p.P;
         const int sub = lane >> 3, ch = lane & 7;
         float* dbin = p.D + (long long)T.f * p.SB + 4 * ch;
+        // rows 32q.. of the tile: one ri, o0.. (Cf a multiple of 32 for the TMA store)
+        const int mg = T.m0 + 32 * q, rig = mg >= p.Cf, o0 = mg - (rig ? p.Cf : 0);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
+          if (p.dtma) {
+            // the previous store of this buffer has read it
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
           __syncwarp();
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             tb4[lane * 8 + (j ^ (lane & 7))] =
                 make_float4(acc[32 * c + 4 * j], acc[32 * c + 4 * j + 1], acc[32 * c + 4 * j + 2], acc[32 * c + 4 * j + 3]);
-          __syncwarp();
           const int col0 = 32 * c + 4 * ch;  // tile column of this lane's 4 values
-          const long long blk = (long long)((T.n0 + cb + 32 * c) >> 5) * 2 * bf8;
+          const int blkn = (T.n0 + cb + 32 * c) >> 5;
+          if (p.dtma) {
+            // 128-byte swizzle of the tensor map = this buffer's XOR layout; rows past M and
+            // slots past the allocation are clipped by the TMA unit
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0 && 32 * c < nc && nr > 0) {
+              asm volatile(
+                  "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+                      reinterpret_cast<uint64_t>(&p.dmap)),
+                  "r"(0), "r"(T.f), "r"(rig), "r"(blkn), "r"(o0), "r"(smem_u32(tb4))
+                  : "memory");
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            continue;
+          }
+          __syncwarp();
+          const long long blk = (long long)blkn * 2 * bf8;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int r = 4 * i + sub;
@@ -356,6 +394,7 @@ __global__ void __launch_bounds__(tc_threads<CONV>(), 1) oaa_bin_gemm_kernel(con
             }
           }
         }
+        if (p.dtma && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       } else if (p.mode == 2 && active) {
         // walker layout: per bin an SB-float run of slots; transpose 32 columns at a time
         float* tb = reinterpret_cast<float*>(smem_raw + kTcStages * kTcStageBytes) + (warp - 2) * 32 * 33;
