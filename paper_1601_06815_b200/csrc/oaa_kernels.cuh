@@ -1252,7 +1252,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) oaa_bwd_filter_kernel(const Fi
 #ifdef OAA_DEFINE_AUX_KERNELS  // defined in exactly one translation unit (oaa_abi.cu)
 // partial[G][K][C][P][H] → dw[K][C][n][n].  One CTA of 512 threads per (k, c): thread
 // (j, t) sums the partial spectra g ≡ j (mod 4) of bin t in fp64 (four interleaved chains,
-// so 16 L2 loads per bin are in flight), the four sums are combined in a fixed order --
+// up to 64 loads per bin in flight), the four sums are combined in a fixed order --
 // bitwise reproducible -- then the inverse DFT and lag read-out.
 __global__ void __launch_bounds__(512) oaa_filter_finalize_kernel(const float2* __restrict__ partial,
                                                                   float* __restrict__ dw, int G, int K, int C,
@@ -1270,6 +1270,14 @@ __global__ void __launch_bounds__(512) oaa_filter_finalize_kernel(const float2* 
       const float2* src = partial + (size_t)kc * bins + t;
       double sr[4] = {0.0, 0.0, 0.0, 0.0}, si[4] = {0.0, 0.0, 0.0, 0.0};
       int g = j;
+      // 16 loads in flight per thread (the sum is latency-bound, not bandwidth-bound)
+      for (; g + 60 < G; g += 64) {
+        float2 v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = __ldg(src + (size_t)(g + 4 * u) * gstride);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) { sr[u & 3] += (double)v[u].x; si[u & 3] += (double)v[u].y; }
+      }
       for (; g + 12 < G; g += 16) {
         float2 v[4];
 #pragma unroll
