@@ -975,13 +975,18 @@ oaa_status_t tc_filt_chunk(TcFilt& f, int ci, int b0, int bc, bool g_done, cudaS
   f.gp.accumulate = ci > 0;
   return launch_bin_gemm(f.gp, s) == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
 }
+// fp64 finalize of the weight gradient: many partial spectra (the SIMT kernels' G ≈ 148
+// slices) → one 512-thread CTA per (k, c) with the sum spread over 4 × bins threads; few
+// (the tensor-core splits) → one warp per (k, c), 8 per CTA.
+void launch_finalize(const float2* partial, float* dw, int G, int K, int C, int n, cudaStream_t s) {
+  KTimer kt(KID_FINALIZE, s);
+  if (G >= 32)
+    oaa::oaa_filter_finalize_kernel<<<K * C, 512, sizeof(double2) * (2 * n - 1) * n, s>>>(partial, dw, G, K, C, n);
+  else
+    oaa::oaa_filter_finalize_small_kernel<<<(K * C + 7) / 8, 256, 0, s>>>(partial, dw, G, K, C, n);
+}
 oaa_status_t tc_filt_finalize(TcFilt& f, float* dw, int K, int C, cudaStream_t s) {
-  const int n = f.n, bins = (2 * n - 1) * n;
-  {
-    KTimer kt(KID_FINALIZE, s);
-    oaa::oaa_filter_finalize_kernel<<<K * C, 512, sizeof(double2) * bins, s>>>(
-        reinterpret_cast<const float2*>(f.part), dw, f.t.G, K, C, n);
-  }
+  launch_finalize(reinterpret_cast<const float2*>(f.part), dw, f.t.G, K, C, f.n, s);
   g_launches++;
   return cudaGetLastError() == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
 }
@@ -1194,10 +1199,7 @@ oaa_status_t oaa_conv_bwd(const float* x, const float* dy, const float* w, float
     pf.dy = dy; pf.XS = xp.S; pf.partial = reinterpret_cast<float2*>(base + fp.data_b + bf.xs_b); pf.B = B; pf.K = K;
     pf.C = C; pf.M = g.M; pf.Td = bf.Td; pf.NCH = bf.NCH; pf.G = bf.G; pf.KG = bf.KG;
     if (launch_bwd_fused(n, xp, dp, pf, bf.xspec_smem, fp.smem, bf.G * bf.nkg, s) != cudaSuccess) return OAA_ERR_CUDA;
-    {
-      KTimer kt(KID_FINALIZE, s);
-      oaa::oaa_filter_finalize_kernel<<<K * C, 512, sizeof(double2) * g.P * g.H, s>>>(pf.partial, dw, bf.G, K, C, n);
-    }
+    launch_finalize(pf.partial, dw, bf.G, K, C, n, s);
     g_launches++;
     return cudaGetLastError() == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
   }
@@ -1351,10 +1353,7 @@ oaa_status_t oaa_conv_bwd_filter(const float* x, const float* dy, float* dw, int
     cudaError_t err = launch_bwdf(n, xp, fp, BwdfLaunch{bf.xspec_smem, bf.smem, bf.nkg, bf.tm}, s);
     prof.stop();
     if (err != cudaSuccess) return OAA_ERR_CUDA;
-    {
-      KTimer kt(KID_FINALIZE, s);
-      oaa::oaa_filter_finalize_kernel<<<K * C, 512, sizeof(double2) * g.P * g.H, s>>>(fp.partial, dw, bf.G, K, C, n);
-    }
+    launch_finalize(fp.partial, dw, bf.G, K, C, n, s);
     g_launches++;
     return cudaGetLastError() == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
   }
@@ -1387,12 +1386,7 @@ oaa_status_t oaa_conv_bwd_filter(const float* x, const float* dy, float* dw, int
   cudaError_t err = launch_filter(n, p, f, s);
   prof.stop();
   if (err != cudaSuccess) return OAA_ERR_CUDA;
-  const int bins = g.P * g.H;
-  {
-    KTimer kt(KID_FINALIZE, s);
-    oaa::oaa_filter_finalize_kernel<<<K * C, 512, sizeof(double2) * bins, s>>>(
-        static_cast<const float2*>(ws), dw, f.G, K, C, n);
-  }
+  launch_finalize(static_cast<const float2*>(ws), dw, f.G, K, C, n, s);
   g_launches++;
   if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
   return OAA_OK;

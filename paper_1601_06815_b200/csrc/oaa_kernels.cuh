@@ -1322,6 +1322,56 @@ __global__ void __launch_bounds__(512) oaa_filter_finalize_kernel(const float2* 
   }
 }
 
+// The same for few partial spectra (G < 32, e.g. the tensor-core weight gradient's splits):
+// one warp per (k, c), 8 per CTA -- the many (k, c) pairs of a wide layer (AlexNet-like:
+// 24 576) then take 3 072 CTAs instead of 24 576.  Fixed summation order (g ascending).
+__global__ void __launch_bounds__(256) oaa_filter_finalize_small_kernel(const float2* __restrict__ partial,
+                                                                        float* __restrict__ dw, int G, int K, int C,
+                                                                        int n) {
+  const int P = 2 * n - 1, H = n, bins = P * H;
+  __shared__ double tc[16], ts[16];
+  __shared__ double2 S[8][120];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kc = blockIdx.x * 8 + warp;
+  if (threadIdx.x < P) sincospi(2.0 * (double)threadIdx.x / (double)P, &ts[threadIdx.x], &tc[threadIdx.x]);
+  __syncthreads();
+  if (kc >= K * C) return;
+  const size_t gstride = (size_t)K * C * bins;
+  for (int t = lane; t < bins; t += 32) {
+    const float2* src = partial + (size_t)kc * bins + t;
+    double sr = 0.0, si = 0.0;
+    for (int g = 0; g < G; ++g) {
+      const float2 v = __ldg(src + (size_t)g * gstride);
+      sr += (double)v.x;
+      si += (double)v.y;
+    }
+    S[warp][t] = make_double2(sr, si);
+  }
+  __syncwarp();
+  const double inv = 1.0 / ((double)P * (double)P);
+  for (int t = lane; t < n * n; t += 32) {
+    const int u = t / n, v = t - (t / n) * n;
+    const int l1 = n - 1 - u, l2 = n - 1 - v;
+    double acc = 0.0;
+    int m1 = 0;
+    for (int f1 = 0; f1 < H; ++f1) {
+      const double wgt = (f1 == 0) ? 1.0 : 2.0;
+      double a = 0.0;
+      int m = m1;
+      for (int f2 = 0; f2 < P; ++f2) {
+        const double2 z = S[warp][f2 * H + f1];
+        a += z.x * tc[m] - z.y * ts[m];
+        m += l2;
+        if (m >= P) m -= P;
+      }
+      acc += wgt * a;
+      m1 += l1;
+      if (m1 >= P) m1 -= P;
+    }
+    dw[(size_t)kc * n * n + t] = (float)(acc * inv);
+  }
+}
+
 // spec4[((a·Binner + bb)·P2 + f2/2)·H + f1].{xy|zw} = DFT_P(w_kc or flip180(w_kc))[f1][f2] / P²
 // with (k, c) = loop_is_k ? (a, bb) : (bb, a); the odd last f2 slot is zero.
 // One CTA per (k, c) pair (grid = K·C): the n×n kernel is staged in fp64, the row DFT
