@@ -89,12 +89,15 @@ def test_channel_regimes(B, C, K, crop):
 @pytest.mark.parametrize("crop", CROPS)
 @pytest.mark.parametrize("B,C,K,N,n", [(2, 16, 20, 17, 3), (1, 17, 33, 29, 5), (3, 24, 16, 20, 8),
                                        (2, 16, 16, 9, 1), (1, 20, 18, 40, 7), (2, 33, 17, 23, 2),
-                                       (1, 16, 130, 12, 3), (1, 200, 16, 10, 5)])
+                                       (1, 16, 130, 12, 3), (1, 200, 16, 10, 5), (2, 32, 32, 32, 8),
+                                       (2, 48, 96, 32, 8)])
 def test_tensor_core_path(B, C, K, N, n, crop):
     """C ≥ 16 and K ≥ 16: fwd and bwd_data run tile spectra → tcgen05 bin GEMM (3×TF32)
     → walker (load mode); ragged 2C (K padding), ragged GEMM tiles, ragged spatial tails.
     2·Cout > 256 (K = 130 fwd, C = 200 bwd_data) takes the pre-split block-spectra GEMM
-    (≥ 3 M tiles); the other cases split in the GEMM's converter warps."""
+    (≥ 3 M tiles); the other cases split in the GEMM's converter warps.  (2, 32, 32, 32, 8) and
+    (2, 48, 96, 32, 8) have whole walker chunks per tile row and 32-row output-channel groups,
+    so their GEMM drains store Ŷ with TMA tensor stores (the other cases with st.global)."""
     if crop == "valid" and n > N:
         pytest.skip("Valid needs n <= N")
     d = make_inputs(B, C, K, N, n, crop, seed=B * 131 + C * 17 + K * 3 + n)

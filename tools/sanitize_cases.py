@@ -10,6 +10,7 @@ CASES = [(2, 3, 8, 40, 8, "valid"),    # walker / bwd_data / bwd_filter SIMT ker
          (2, 2, 5, 23, 5, "full"),     # n ∤ 32, full crop
          (1, 6, 7, 19, 4, "same"),     # first-generation engine (C > 4, small K)
          (2, 16, 20, 17, 3, "same"),   # tensor-core path (tile spectra, bin GEMM, walker load)
+         (2, 32, 32, 32, 8, "valid"),  # tensor-core path with TMA tensor stores of Y-hat
          (1, 2, 3, 12, 1, "valid")]    # n = 1
 for (B, C, K, N, n, crop) in CASES:
     d = make_inputs(B, C, K, N, n, crop, seed=3)
