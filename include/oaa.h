@@ -103,8 +103,10 @@ oaa_status_t oaa_conv_fwd(const float* x, const float* w, float* y, int B, int C
  * of the kernel with the (2n−1)² input window starting at t·n + o − (n−1) (zero outside
  * x): those outputs have no wrap-around, so they equal the linear convolution and every
  * output is written once, with no overlap-add.  Workspace: op OAA_OP_FWD_OAS.  Supported
- * for C ≤ 4 (the SIMT walker family); larger C returns OAA_ERR_UNSUPPORTED.  Other
- * arguments, layouts, limits and errors as oaa_conv_fwd. */
+ * for C ≤ 4 (the SIMT walker family: window spectra, then the walker in overlap-and-save mode)
+ * and for C, K ≥ 16 (the tensor-core path: window spectra of the output tiles, tcgen05 bin
+ * GEMM, walker in load + overlap-and-save mode); other channel counts return
+ * OAA_ERR_UNSUPPORTED.  Other arguments, layouts, limits and errors as oaa_conv_fwd. */
 oaa_status_t oaa_conv_fwd_oas(const float* x, const float* w, float* y, int B, int C, int K, int N,
                               int n, oaa_crop_t crop, void* ws, size_t ws_bytes, void* stream);
 

@@ -198,7 +198,7 @@ def conv_fwd_oas(x: torch.Tensor, w: torch.Tensor, crop="valid", out: Optional[t
                  stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
     """The same y as conv_fwd, by overlap-and-save (include/oaa.h): each
     n×n output block is the alias-free part of a (2n−1)-point circular convolution of its
-    input window.  C ≤ 4."""
+    input window.  C ≤ 4 (SIMT walker) or C, K ≥ 16 (tensor-core path)."""
     _check(x, "x"); _check(w, "w")
     B, C, N, N2 = x.shape
     K, C2, n, n2 = w.shape

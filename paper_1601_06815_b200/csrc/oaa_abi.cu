@@ -1076,6 +1076,54 @@ bool plan_bwd_fused(int B, int C, int K, int N, int n, oaa_crop_t crop, const Ge
   return true;
 }
 
+// Overlap-and-save forward on the tensor-core path (C, K ≥ 16; NEXT-2): per
+// batch chunk the spectra of the (2n−1)² x-windows of the OUTPUT tiles (tile spectra, window
+// mode), the bin GEMM, and the walker in load + overlap-and-save mode (the blocks' last n rows
+// and columns, no overlap-add).  Workspace: the tensor-core engine's layout over ⌈M/n⌉² tiles.
+struct OasTc {
+  bool use;
+  TcPlan tc;
+  EnginePlan e;
+  EngineWs L;
+};
+OasTc plan_oas_tc(int B, int C, int K, int N, int n, const Geo& g) {
+  OasTc o{};
+  o.tc = plan_tc(B, C, K, g.M, n);  // tiles: ⌈M/n⌉² output tiles
+  o.use = o.tc.use && B > 0;
+  if (!o.use) return o;
+  o.e = EnginePlan{};
+  o.e.R = N;  // the windows read x
+  o.e.Ro = g.M;
+  o.e.off = 0;
+  o.e.T = cdiv(g.M, n);
+  o.e.Cin = C;
+  o.e.Cout = K;
+  o.e.BW = cdiv(o.e.T * n + n - 1, 4) * 4;
+  o.L = engine_ws(B, C, K, o.e.T, g, o.tc);
+  return o;
+}
+oaa_status_t run_oas_tc(const float* x, const float* w, float* y, int B, int C, int K, int n, const Geo& g,
+                        const OasTc& o, char* base, cudaStream_t s) {
+  float* Ag = reinterpret_cast<float*>(base + o.L.spec_off);
+  float* Xg = reinterpret_cast<float*>(base + o.L.xg_off);
+  float* D = reinterpret_cast<float*>(base + o.L.d_off);
+  TcData d;
+  oaa_status_t st = tc_data_setup(d, true, x, w, y, K, C, n, g, o.e, o.tc, Ag, Xg, D, s, nullptr);
+  if (st != OAA_OK) return st;
+  const int P = 2 * n - 1;
+  d.tp.win = 1;
+  d.tp.org = g.o - (n - 1);
+  d.tp.CSTR = P * d.tp.BW + 4;
+  d.t1_smem = sizeof(float) * 4 * (size_t)d.tp.CSTR;
+  d.wp.oas = 1;
+  ProfScope prof(OAA_OP_FWD, s);
+  prof.start();
+  for (int b0 = 0; b0 < B; b0 += o.tc.bc)
+    if ((st = tc_data_chunk(d, b0, std::min(o.tc.bc, B - b0), s)) != OAA_OK) return st;
+  prof.stop();
+  return OAA_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1110,7 +1158,9 @@ size_t oaa_conv_workspace_bytes(oaa_op_t op, int B, int C, int K, int N, int n, 
   }
   if (op == OAA_OP_FWD_OAS) {
     const OasPlan o = plan_oas(B, C, K, N, n, g);
-    return o.use ? o.spec_b + o.xs_b : 0;
+    if (o.use) return o.spec_b + o.xs_b;
+    const OasTc ot = plan_oas_tc(B, C, K, N, n, g);
+    return ot.use ? ot.L.total : 0;
   }
   if (op == OAA_OP_BWD_FILTER) {
     const TcFiltPlan t = plan_tc_filter(B, C, K, N, g.M, n);
@@ -1247,7 +1297,16 @@ oaa_status_t oaa_conv_fwd_oas(const float* x, const float* w, float* y, int B, i
   if (B > 0 && (overlaps(x, x_bytes, y, y_bytes) || overlaps(w, w_bytes, y, y_bytes))) return OAA_ERR_INVALID_VALUE;
   if (std::max(cdiv(N, n) * n, g.M) > oaa::kMaxThreads) return OAA_ERR_UNSUPPORTED;
   const OasPlan o = plan_oas(B, C, K, N, n, g);
-  if (!o.use) return OAA_ERR_UNSUPPORTED;
+  if (!o.use) {
+    const OasTc ot = plan_oas_tc(B, C, K, N, n, g);
+    if (B == 0 && plan_tc(1, C, K, g.M, n).use) return OAA_OK;
+    if (!ot.use) return OAA_ERR_UNSUPPORTED;
+    if (!ws || ws_bytes < ot.L.total || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0) return OAA_ERR_WORKSPACE;
+    if (overlaps(ws, ot.L.total, y, y_bytes) || overlaps(ws, ot.L.total, x, x_bytes) ||
+        overlaps(ws, ot.L.total, w, w_bytes))
+      return OAA_ERR_INVALID_VALUE;
+    return run_oas_tc(x, w, y, B, C, K, n, g, ot, static_cast<char*>(ws), static_cast<cudaStream_t>(stream));
+  }
   if (B == 0) return OAA_OK;
   const size_t need = o.spec_b + o.xs_b;
   if (!ws || ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0) return OAA_ERR_WORKSPACE;

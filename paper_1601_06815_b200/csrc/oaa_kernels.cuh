@@ -1482,15 +1482,21 @@ struct TileSpecParams {
   // convolutions.  Ga == nullptr: plain tile spectra.
   float* Ga;
   int KcG, RTG;
+  // overlap-and-save forward (NEXT-2), win = 1: row bt is an OUTPUT tile and its
+  // spectrum is that of the (2n−1)² x-window at (t1·n + org, t2·n + org), org = o − (n−1), zero
+  // outside x
+  int win, org;
 };
 
 // One CTA per (image, tile row) of the chunk.  A task is (f1, tile t2, quad of 4
 // channels): its spectra go out as float4 (4 consecutive columns of one row), and the 8
 // lanes of consecutive tiles of a warp fill whole 128-byte lines of the blocked layout.
-template <int NN>
+// WIN (overlap-and-save): the tiles are output tiles and the spectra those of their
+// (2n−1)² x-windows (full 2n−1 rows staged, 4 channels per CTA for the larger band).
+template <int NN, bool WIN = false>
 __global__ void __launch_bounds__(128) oaa_tile_spectra_kernel(const TileSpecParams p) {
-  constexpr int P = 2 * NN - 1, CG = 16;
-  extern __shared__ __align__(16) float band[];  // [CG][NN][BW] (channel stride CSTR)
+  constexpr int P = 2 * NN - 1, CG = WIN ? 4 : 16, QGL = WIN ? 0 : 2, ROWS = WIN ? P : NN;
+  extern __shared__ __align__(16) float band[];  // [CG][ROWS][BW] (channel stride CSTR)
   __shared__ float2 tw[16];
   const int tid = threadIdx.x, nthr = blockDim.x;
   if (tid < P) {
@@ -1511,28 +1517,32 @@ __global__ void __launch_bounds__(128) oaa_tile_spectra_kernel(const TileSpecPar
     const int c0 = blockIdx.y * CG;
     const int ncg = min(CG, p.Cin - c0);
     const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
-    for (int sgm = warp; sgm < ncg * NN; sgm += nwarps) {
-      const int ch = sgm / NN, rr = sgm - (sgm / NN) * NN;
-      const int r = t1 * NN + rr;
-      const bool rok = r < p.R;
+    const int org = WIN ? p.org : 0;
+    for (int sgm = warp; sgm < ncg * ROWS; sgm += nwarps) {
+      const int ch = sgm / ROWS, rr = sgm - (sgm / ROWS) * ROWS;
+      const int r = t1 * NN + org + rr;
+      const bool rok = r >= 0 && r < p.R;
       const int roff = ((c0 + ch) * p.R + (rok ? r : 0)) * p.R;  // within the image (32-bit)
       float* d = band + ch * p.CSTR + rr * p.BW;
       for (int q = lane; q < p.BW; q += 32) {
-        const bool ok = rok && q < p.R;
-        cp_async4(d + q, in_b + (ok ? roff + q : 0), ok);
+        const int col = q + org;
+        const bool ok = rok && col >= 0 && col < p.R;
+        cp_async4(d + q, in_b + (ok ? roff + col : 0), ok);
       }
     }
     cp_async_commit();
     cp_async_wait_all();
     __syncthreads();
-    const int ntask = NN * TH8 * 32;
+    // task u: 8 consecutive tiles (u & 7) × the CTA's channel quads × (f1, tile octet)
+    const int ntask = (NN * TH8 * 8) << QGL;
     for (int u = tid; u < ntask; u += nthr) {
-      const int t2 = ((u >> 5) % TH8) * 8 + (u & 7), cq = (u >> 3) & 3, f1 = (u >> 5) / TH8;
+      const int rest = u >> (3 + QGL);
+      const int t2 = (rest % TH8) * 8 + (u & 7), cq = (u >> 3) & ((1 << QGL) - 1), f1 = rest / TH8;
       const int cb = c0 + 4 * cq;
       if (t2 >= p.T || cb >= Cinp) continue;
-      float cf[NN], sf[NN];
+      float cf[ROWS], sf[ROWS];
 #pragma unroll
-      for (int p1 = 0; p1 < NN; ++p1) {
+      for (int p1 = 0; p1 < ROWS; ++p1) {
         const float2 t = tw[(f1 * p1) % P];
         cf[p1] = t.x;
         sf[p1] = t.y;
@@ -1541,7 +1551,25 @@ __global__ void __launch_bounds__(128) oaa_tile_spectra_kernel(const TileSpecPar
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         if (cb + i < p.Cin) {
-          block_row_spectrum_smem<NN>(band + (cb + i - c0) * p.CSTR, p.BW, t2 * NN, cf, sf, xr[i], xi[i]);
+          if constexpr (WIN) {
+            // window: column DFT over all 2n−1 rows at this f1, then the full row DFT
+            const float* blk = band + (cb + i - c0) * p.CSTR + t2 * NN;
+            float rr[P], ri[P];
+#pragma unroll
+            for (int p2 = 0; p2 < P; ++p2) { rr[p2] = blk[p2]; ri[p2] = 0.f; }
+#pragma unroll
+            for (int p1 = 1; p1 < P; ++p1) {
+#pragma unroll
+              for (int p2 = 0; p2 < P; ++p2) {
+                const float v = blk[p1 * p.BW + p2];
+                rr[p2] = fmaf(v, cf[p1], rr[p2]);
+                ri[p2] = fmaf(-v, sf[p1], ri[p2]);
+              }
+            }
+            dft<P, -1>(rr, ri, xr[i], xi[i]);
+          } else {
+            block_row_spectrum_smem<NN>(band + (cb + i - c0) * p.CSTR, p.BW, t2 * NN, cf, sf, xr[i], xi[i]);
+          }
         } else {
 #pragma unroll
           for (int f2 = 0; f2 < P; ++f2) { xr[i][f2] = 0.f; xi[i][f2] = 0.f; }

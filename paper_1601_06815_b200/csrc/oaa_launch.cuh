@@ -149,12 +149,14 @@ cudaError_t launch_filter_n(const oaa::FilterParams& p, const FilterPlan& f, cud
 
 template <int NN>
 cudaError_t launch_tile_spectra_n(const oaa::TileSpecParams& p, size_t smem, cudaStream_t s) {
-  auto k = oaa::oaa_tile_spectra_kernel<NN>;
+  const bool win = p.win != 0;
+  auto k = win ? oaa::oaa_tile_spectra_kernel<NN, true> : oaa::oaa_tile_spectra_kernel<NN, false>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   {
     KTimer kt(KID_TILE_SPECTRA, s);
-    k<<<dim3(p.bc * p.T, (((p.Cin + 3) & ~3) + 15) / 16), 128, smem, s>>>(p);
+    const int cg = win ? 4 : 16;
+    k<<<dim3(p.bc * p.T, (((p.Cin + 3) & ~3) + cg - 1) / cg), 128, smem, s>>>(p);
   }
   g_launches++;
   return cudaGetLastError();
@@ -307,7 +309,8 @@ cudaError_t launch_bwd_fused_n(const oaa::XSpecParams& xp, const oaa::BwdDParams
 
 template <int NN>
 cudaError_t launch_walk_load_n(const oaa::WalkParams& wp, size_t smem, int nimg, cudaStream_t s) {
-  auto k = oaa::oaa_walk_kernel<NN, 1, true>;
+  // (oas: overlap-and-save stage B -- the blocks' last n rows / columns, no overlap-add)
+  auto k = wp.oas ? oaa::oaa_walk_kernel<NN, 1, true, true> : oaa::oaa_walk_kernel<NN, 1, true>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   {

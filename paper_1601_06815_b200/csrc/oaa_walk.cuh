@@ -231,6 +231,7 @@ struct WalkParams {
   const float* D;
   int BTc, b0;
   int SBL;  // log2 of the slots per Ŷ block (oaa_tc.cuh mode 2)
+  int oas;  // LOAD: the launcher picks the overlap-and-save instantiation
 };
 
 constexpr int kWalkRing = 4;  // spectrum chunk slots per CTA

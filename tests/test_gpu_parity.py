@@ -341,6 +341,21 @@ def test_oas_forward_small_grid(N, n, crop):
         check(y.cpu().numpy(), oracle.conv_fwd(d["x"], d["w"], crop), f"oas N={N} n={n} {crop} BCK={B,C,K}")
 
 
+@pytest.mark.parametrize("crop", CROPS)
+@pytest.mark.parametrize("B,C,K,N,n", [(2, 16, 20, 17, 3), (1, 17, 33, 29, 5), (3, 24, 16, 20, 8),
+                                       (2, 32, 32, 32, 8), (1, 20, 18, 40, 7), (2, 16, 16, 9, 1)])
+def test_oas_tensor_core_path(B, C, K, N, n, crop):
+    """Overlap-and-save for C, K ≥ 16: x-window spectra of the output tiles →
+    tcgen05 bin GEMM → walker in load + overlap-and-save mode; every element vs the oracle."""
+    if crop == "valid" and n > N:
+        pytest.skip("Valid needs n <= N")
+    d = make_inputs(B, C, K, N, n, crop, seed=B * 31 + C + K * 7 + N + n)
+    x = torch.from_numpy(d["x"]).cuda(); w = torch.from_numpy(d["w"]).cuda()
+    y = oaa.conv_fwd_oas(x, w, crop)
+    torch.cuda.synchronize()
+    check(y.cpu().numpy(), oracle.conv_fwd(d["x"], d["w"], crop), f"oas tc {B,C,K,N,n,crop}")
+
+
 def test_oas_matches_oaa_and_rejects_large_C():
     d = make_inputs(2, 3, 64, 60, 8, "valid", seed=5)
     x = torch.from_numpy(d["x"]).cuda(); w = torch.from_numpy(d["w"]).cuda()
