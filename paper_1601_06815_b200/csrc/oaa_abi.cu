@@ -713,7 +713,7 @@ oaa_status_t tc_data_setup(TcData& d, bool is_fwd, const float* in, const float*
   gp.TT = T;
   gp.TPW = 32 / n;
   gp.NT4 = cdiv(T, gp.TPW);
-  gp.SBL = 5;
+  gp.SBL = oaa::kYSBL;  // (the walker's load mode reads Ŷ with this block size fixed at compile time)
   gp.SB = 1 << gp.SBL;
   gp.NB = tc.NB;
   gp.Kuse = tc.Kc;

@@ -230,11 +230,13 @@ struct WalkParams {
   // floats [re/im][f1·P + f2][tile in chunk]; BTc = tiles of the batch chunk (images × T²)
   const float* D;
   int BTc, b0;
-  int SBL;  // log2 of the slots per Ŷ block (oaa_tc.cuh mode 2)
+  int SBL;  // log2 of the slots per Ŷ block (oaa_tc.cuh mode 2); must equal kYSBL
   int oas;  // LOAD: the launcher picks the overlap-and-save instantiation
 };
 
 constexpr int kWalkRing = 4;  // spectrum chunk slots per CTA
+constexpr int kYSBL = 5;      // Ŷ slot blocks of 32 (compile-time: the 30 loads of a chunk's Ŷ row
+                              // then use immediate offsets, no per-load address arithmetic)
 
 // grid = B·ngrp CTAs (image-major: the groups of one image run side by side and share
 // its spectra through L2), KG warps each.
@@ -311,7 +313,7 @@ __global__ void __launch_bounds__(256, (LOAD && NN <= 6) ? 2 : 1) oaa_walk_kerne
   float ynr[LOAD ? P : 1], yni[LOAD ? P : 1];
   // Ŷ in the layout of oaa_bin_gemm_kernel mode 2: blocks of 8 walker slots, per bin one
   // 32-byte run; the chunk's TPW slots lie in one or two blocks
-  const int SB = 1 << p.SBL, BF8 = SB * H * P;
+  constexpr int SB = 1 << kYSBL, BF8 = SB * H * P;
   const int NT4 = (p.T + TPW - 1) / TPW;
   const size_t dplane = LOAD ? ((size_t)(p.BTc / p.T) * NT4 * TPW + SB - 1) / SB * 2 * BF8 : 0;
   const float* dlane = LOAD ? p.D + (size_t)(active ? co : 0) * dplane + f1 * P * SB : nullptr;
@@ -320,7 +322,7 @@ __global__ void __launch_bounds__(256, (LOAD && NN <= 6) ? 2 : 1) oaa_walk_kerne
       const int t2 = i * TPW + tt;
       const bool ok = active && laneA && t1 < p.T && t2 < p.T;
       const size_t sl = ((size_t)(bl * p.T + t1) * NT4 + i) * TPW + tt;
-      const float* d = dlane + (ok ? (sl >> p.SBL) * 2 * BF8 + (sl & (SB - 1)) : 0);
+      const float* d = dlane + (ok ? (sl >> kYSBL) * 2 * BF8 + (sl & (SB - 1)) : 0);
 #pragma unroll
       for (int f2 = 0; f2 < P; ++f2) {
         ynr[f2] = ok ? __ldg(d + f2 * SB) : 0.f;
