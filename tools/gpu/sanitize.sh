@@ -1,4 +1,5 @@
 #!/bin/bash
+# GPU suite, headline kernel breakdown, compute-sanitizer memcheck / racecheck / synccheck (tools/sanitize_cases.py) and the toy-library check (tools/sanity_lib.py).
 out=gpurun_out/${1:-tma}; mkdir -p $out
 timeout 1200 python -m pytest tests -m gpu -x -q > $out/pytest.log 2>&1; echo "pytest rc=$?" >> $out/pytest.log
 timeout 300 python tools/kernel_breakdown.py 128,3,64,224,8 valid 5 > $out/bd.json 2>&1
