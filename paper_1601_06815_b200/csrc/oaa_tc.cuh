@@ -474,8 +474,11 @@ __global__ void oaa_realified_spectrum_kernel(const float* __restrict__ w, float
   const double inv = 1.0 / ((double)P * (double)P);
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(t % Ci);
-    const int o = (int)((t / Ci) % Co);
+    // consecutive threads take consecutive c (the fastest index of w): i for fwd (i = c),
+    // o for bwd_data (o = c) -- the weight reads of a warp then stay within a few lines
+    const long long kc = t % ((long long)Ci * Co);
+    const int i = flip_bwd ? (int)(kc / Co) : (int)(kc % Ci);
+    const int o = flip_bwd ? (int)(kc % Co) : (int)(kc / Ci);
     const int f = (int)(t / ((long long)Ci * Co));
     const int f1 = f / P, f2 = f - (f / P) * P;
     const int k = flip_bwd ? i : o, c = flip_bwd ? o : i;
