@@ -944,8 +944,8 @@ void tc_filt_setup(TcFilt& f, const float* x, const float* dy, int C, int K, int
   f.xs = oaa::FiltSpecParams{};
   f.xs.src = x; f.xs.Op = f.Xb; f.xs.nch = C; f.xs.R = N; f.xs.Td = t.Td; f.xs.org = g.o - (n - 1); f.xs.Kc = t.Kc;
   f.xs.RT = t.RTB; f.xs.SW = t.SWx;
-  f.smem_g = sizeof(float) * oaa::kFsCG * n * (size_t)t.SWg;
-  f.smem_x = sizeof(float) * oaa::kFsCG * (2 * n - 1) * (size_t)t.SWx;
+  f.smem_g = 2 * sizeof(float) * oaa::kFsCG * n * (size_t)t.SWg;  // double-buffered bands
+  f.smem_x = 2 * sizeof(float) * oaa::kFsCG * (2 * n - 1) * (size_t)t.SWx;
   oaa::BinGemmParams& gp = f.gp;
   gp = oaa::BinGemmParams{};
   gp.A = f.Ga; gp.B = f.Xb; gp.D = nullptr; gp.F = t.F; gp.M = K; gp.N = 2 * C; gp.Kc = t.Kc; gp.RTA = t.RTA;

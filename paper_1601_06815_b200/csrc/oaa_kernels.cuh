@@ -1641,6 +1641,7 @@ struct FiltSpecParams {
   const float* src;  // dy [B][K][M][M] (G) or x [B][C][N][N] (X)
   float* Op;         // blocked [F][Kc][2][RT][4096]
   int nch, R, Td, org, b0, Kc, RT, SW;
+  int nitems;        // (image, tile row) items of the chunk
 };
 
 constexpr int kFsCG = 4;  // channels per CTA of oaa_filter_spectra_kernel (32·kFsCG threads)
@@ -1649,14 +1650,13 @@ constexpr int kFsCG = 4;  // channels per CTA of oaa_filter_spectra_kernel (32·
 template <int NN, bool XWIN>
 __global__ void __launch_bounds__(32 * kFsCG, NN <= 5 ? 6 : 1) oaa_filter_spectra_kernel(const FiltSpecParams p) {
   constexpr int P = 2 * NN - 1, H = NN, ROWS = XWIN ? P : NN, CG = kFsCG;
-  extern __shared__ __align__(16) float band[];  // [CG][ROWS][SW]
+  // [2][CG][ROWS][SW]: the CTA walks items blockIdx.x, blockIdx.x + gridDim.x, ... with the
+  // next item's band staged (cp.async) while the current one is transformed -- small images
+  // have little work per item, so the staging latency would otherwise dominate
+  extern __shared__ __align__(16) float band[];
   const int tid = threadIdx.x;
   const int kl = tid % CG, grp = tid / CG;       // channel within group, lane group
   const int f1 = grp % H, tsub = grp / H, nsub = 32 / H;
-  const int item = blockIdx.x;
-  const int bl = item / p.Td, t1 = item - (item / p.Td) * p.Td;
-  const int b = p.b0 + bl;
-  const int bt0 = (bl * p.Td + t1) * p.Td;
   float tcx[ROWS], tsx[ROWS];  // e^{−2πi f1 p1 / P} for the column stage
 #pragma unroll
   for (int p1 = 0; p1 < ROWS; ++p1) {
@@ -1666,91 +1666,103 @@ __global__ void __launch_bounds__(32 * kFsCG, NN <= 5 ? 6 : 1) oaa_filter_spectr
     tsx[p1] = sn;
   }
   const int plane = p.R * p.R;
-  const int r0 = t1 * NN + p.org;
-  const int q_lo = bt0 >> 1, q_hi = (bt0 + p.Td - 1) >> 1;
-  // one channel group of CG per CTA (blockIdx.y): items × groups CTAs keep every SM busy
-  {
-    const int c0 = blockIdx.y * CG;
-    if (c0 >= p.nch) return;
-    const int ncg = min(CG, p.nch - c0);
-    {
+  // one channel group of CG per CTA (blockIdx.y)
+  const int c0 = blockIdx.y * CG;
+  if (c0 >= p.nch) return;
+  const int ncg = min(CG, p.nch - c0);
+  const int bandf = CG * ROWS * p.SW;  // floats per band buffer
+  auto stage = [&](int item, int buf) {
+    if (item < p.nitems) {
+      const int bl = item / p.Td, t1 = item - (item / p.Td) * p.Td;
+      const int r0 = t1 * NN + p.org;
       const int lane = tid & 31, warp = tid >> 5;
-      const float* base = p.src + ((size_t)b * p.nch + c0) * plane;  // 32-bit offsets below
+      const float* base = p.src + ((size_t)(p.b0 + bl) * p.nch + c0) * plane;  // 32-bit offsets below
       for (int sg = warp; sg < ncg * ROWS; sg += CG) {
         const int ch = sg / ROWS, rr = sg - (sg / ROWS) * ROWS;
         const int r = r0 + rr;
         const bool rok = r >= 0 && r < p.R;
         const int roff = ch * plane + (rok ? r : 0) * p.R + p.org;
-        float* d = band + (ch * ROWS + rr) * p.SW;
+        float* d = band + buf * bandf + (ch * ROWS + rr) * p.SW;
         for (int q = lane; q < p.SW; q += 32) {
           const int col = q + p.org;
           const bool ok = rok && col >= 0 && col < p.R;
           cp_async4(d + q, base + (ok ? roff + q : 0), ok);
         }
       }
-      cp_async_commit();
-      cp_async_wait_all();
-      __syncthreads();
     }
-    if (kl >= ncg || tsub >= nsub) return;
-    const float* bsrc = band + kl * ROWS * p.SW;
-    const int ch = c0 + kl;
-    for (int q = q_lo + tsub; q <= q_hi; q += nsub) {
-      float sr[2][P], si[2][P];
-      bool have[2];
+    cp_async_commit();
+  };
+  stage(blockIdx.x, 0);
+  int buf = 0;
+  for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, buf ^= 1) {
+    stage(item + gridDim.x, buf ^ 1);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // this item's band has landed
+    __syncthreads();
+    const int bl = item / p.Td, t1 = item - (item / p.Td) * p.Td;
+    const int bt0 = (bl * p.Td + t1) * p.Td;
+    const int q_lo = bt0 >> 1, q_hi = (bt0 + p.Td - 1) >> 1;
+    if (kl < ncg && tsub < nsub) {
+      const float* bsrc = band + buf * bandf + kl * ROWS * p.SW;
+      const int ch = c0 + kl;
+      for (int q = q_lo + tsub; q <= q_hi; q += nsub) {
+        float sr[2][P], si[2][P];
+        bool have[2];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int bt = 2 * q + h;
-        have[h] = bt >= bt0 && bt < bt0 + p.Td;
-        const int t2 = have[h] ? bt - bt0 : 0;
-        if constexpr (!XWIN) {
-          float cf[NN], sf[NN];
+        for (int h = 0; h < 2; ++h) {
+          const int bt = 2 * q + h;
+          have[h] = bt >= bt0 && bt < bt0 + p.Td;
+          const int t2 = have[h] ? bt - bt0 : 0;
+          if constexpr (!XWIN) {
+            float cf[NN], sf[NN];
 #pragma unroll
-          for (int p1 = 0; p1 < NN; ++p1) { cf[p1] = tcx[p1]; sf[p1] = tsx[p1]; }
-          block_row_spectrum_smem<NN>(bsrc, p.SW, t2 * NN, cf, sf, sr[h], si[h]);
-        } else {
-          const float* w = bsrc + t2 * NN;
-          float rr[P], ri[P];
-#pragma unroll
-          for (int p2 = 0; p2 < P; ++p2) {
-            float a = w[p2], bb = 0.f;
-#pragma unroll
-            for (int p1 = 1; p1 < P; ++p1) {
-              const float v = w[p1 * p.SW + p2];
-              a = fmaf(v, tcx[p1], a);
-              bb = fmaf(-v, tsx[p1], bb);
-            }
-            rr[p2] = a;
-            ri[p2] = bb;
-          }
-          dft<P, -1>(rr, ri, sr[h], si[h]);
-        }
-      }
-#pragma unroll
-      for (int f2 = 0; f2 < P; ++f2) {
-        const int f = f1 * P + f2;
-        // row ch: (re, im) pairs; X mode also row nch + ch: (im, −re)
-#pragma unroll
-        for (int rowk = 0; rowk < (XWIN ? 2 : 1); ++rowk) {
-          float v[4];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            v[2 * h] = rowk == 0 ? sr[h][f2] : si[h][f2];
-            v[2 * h + 1] = rowk == 0 ? si[h][f2] : -sr[h][f2];
-          }
-          const int row = ch + rowk * p.nch;
-          float* dh = p.Op + tc_idx(f, p.Kc, p.RT, row, 4 * q);
-          if (have[0] && have[1]) {
-            *reinterpret_cast<float4*>(dh) = make_float4(v[0], v[1], v[2], v[3]);
-          } else if (have[0]) {
-            *reinterpret_cast<float2*>(dh) = make_float2(v[0], v[1]);
+            for (int p1 = 0; p1 < NN; ++p1) { cf[p1] = tcx[p1]; sf[p1] = tsx[p1]; }
+            block_row_spectrum_smem<NN>(bsrc, p.SW, t2 * NN, cf, sf, sr[h], si[h]);
           } else {
-            *reinterpret_cast<float2*>(dh + 2) = make_float2(v[2], v[3]);
+            const float* w = bsrc + t2 * NN;
+            float rr[P], ri[P];
+#pragma unroll
+            for (int p2 = 0; p2 < P; ++p2) {
+              float a = w[p2], bb = 0.f;
+#pragma unroll
+              for (int p1 = 1; p1 < P; ++p1) {
+                const float v = w[p1 * p.SW + p2];
+                a = fmaf(v, tcx[p1], a);
+                bb = fmaf(-v, tsx[p1], bb);
+              }
+              rr[p2] = a;
+              ri[p2] = bb;
+            }
+            dft<P, -1>(rr, ri, sr[h], si[h]);
+          }
+        }
+#pragma unroll
+        for (int f2 = 0; f2 < P; ++f2) {
+          const int f = f1 * P + f2;
+          // row ch: (re, im) pairs; X mode also row nch + ch: (im, −re)
+#pragma unroll
+          for (int rowk = 0; rowk < (XWIN ? 2 : 1); ++rowk) {
+            float v[4];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              v[2 * h] = rowk == 0 ? sr[h][f2] : si[h][f2];
+              v[2 * h + 1] = rowk == 0 ? si[h][f2] : -sr[h][f2];
+            }
+            const int row = ch + rowk * p.nch;
+            float* dh = p.Op + tc_idx(f, p.Kc, p.RT, row, 4 * q);
+            if (have[0] && have[1]) {
+              *reinterpret_cast<float4*>(dh) = make_float4(v[0], v[1], v[2], v[3]);
+            } else if (have[0]) {
+              *reinterpret_cast<float2*>(dh) = make_float2(v[0], v[1]);
+            } else {
+              *reinterpret_cast<float2*>(dh + 2) = make_float2(v[2], v[3]);
+            }
           }
         }
       }
     }
+    __syncthreads();  // every thread is done with this band before it is restaged
   }
+  cp_async_wait_all();
 }
 
 #ifdef OAA_DEFINE_AUX_KERNELS

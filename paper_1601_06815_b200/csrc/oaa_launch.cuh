@@ -167,9 +167,19 @@ cudaError_t launch_filter_spectra_n(const oaa::FiltSpecParams& p, bool xwin, int
   auto k = xwin ? oaa::oaa_filter_spectra_kernel<NN, true> : oaa::oaa_filter_spectra_kernel<NN, false>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
+  // persistent over items: about two waves of resident CTAs, each walking items with its next
+  // band prefetched
+  const int groups = (p.nch + oaa::kFsCG - 1) / oaa::kFsCG;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * oaa::kFsCG, smem);
+  const int gx = std::max(1, std::min(items, 2 * std::max(1, per_sm) * sms / groups));
+  oaa::FiltSpecParams q = p;
+  q.nitems = items;
   {
     KTimer kt(KID_FILTER_SPECTRA, s);
-    k<<<dim3(items, (p.nch + oaa::kFsCG - 1) / oaa::kFsCG), 32 * oaa::kFsCG, smem, s>>>(p);
+    k<<<dim3(gx, groups), 32 * oaa::kFsCG, smem, s>>>(q);
   }
   g_launches++;
   return cudaGetLastError();
