@@ -127,7 +127,11 @@ def test_new_op_workspace_sizes():
         assert oaa.workspace_bytes(op, 128, 3, 64, 224, 8, "valid") % 256 == 0
     # the fused backward needs at least what the two separate ops need on the SIMT path
     assert oaa.workspace_bytes(oaa.OP_BWD, 256, 96, 256, 27, 5, "valid") > 0
-    assert oaa.workspace_bytes(oaa.OP_FWD_OAS, 2, 5, 3, 16, 3, "valid") == 0   # OaS: C ≤ 4 only
+    assert oaa.workspace_bytes(oaa.OP_FWD_OAS, 2, 5, 3, 16, 3, "valid") == 0   # OaS: C ≤ 4 or C, K ≥ 16
+    # OaS on the tensor-core path (C, K ≥ 16): the engine layout over the ⌈M/n⌉² output tiles
+    tc = oaa.workspace_bytes(oaa.OP_FWD_OAS, 4, 32, 32, 32, 8, "valid")
+    assert tc > 0 and tc % 256 == 0
+    assert oaa.workspace_bytes(oaa.OP_FWD_OAS, 4, 32, 32, 32, 8, "full") >= tc  # more output tiles
     L = oaa.lib()
     for op in (oaa.OP_FWD, oaa.OP_BWD_DATA):
         assert L.oaa_weight_spectra_bytes(op, 3, 64, 224, 8, 1) % 256 == 0
