@@ -461,3 +461,48 @@ def test_cuda_graph_capture_replays_bitwise():
             g.replay()
         torch.cuda.synchronize()
         assert torch.equal(y, y0) and torch.equal(dx, dx0) and torch.equal(dw, dw0)
+
+
+def _random_shapes(count, seed):
+    """Seeded random layer shapes across the three kernel families (C ≤ 4 SIMT kernels,
+    5 ≤ C ≤ 15 first-generation engine, C, K ≥ 16 tensor-core path), all n and crops."""
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        fam = len(out) % 3
+        n = int(rng.integers(1, 9))
+        N = int(rng.integers(max(1, n), 48))
+        crop = CROPS[int(rng.integers(0, 3))]
+        B = int(rng.integers(1, 4))
+        if fam == 0:
+            C, K = int(rng.integers(1, 5)), int(rng.integers(1, 40))
+        elif fam == 1:
+            C, K = int(rng.integers(5, 16)), int(rng.integers(1, 12))
+        else:
+            C, K = int(rng.integers(16, 48)), int(rng.integers(16, 48))
+        out.append((B, C, K, N, n, crop))
+    return out
+
+
+@pytest.mark.parametrize("B,C,K,N,n,crop", _random_shapes(60, 2026))
+def test_random_shapes_all_ops(B, C, K, N, n, crop):
+    """Seeded random shapes (every family, n, crop, ragged sizes): fwd, bwd_data, bwd_filter,
+    the fused backward (dx bitwise equal to bwd_data) and, where supported, overlap-and-save —
+    every element against the oracle."""
+    d = make_inputs(B, C, K, N, n, crop, seed=B * 7 + C * 11 + K * 13 + N * 17 + n)
+    y, dx, dw = run_all(d, N, n, crop)
+    check(y, oracle.conv_fwd(d["x"], d["w"], crop), f"fwd {B,C,K,N,n,crop}")
+    ref_dx = oracle.conv_bwd_data(d["dy"], d["w"], N, crop)
+    ref_dw = oracle.conv_bwd_filter(d["x"], d["dy"], n, crop)
+    check(dx, ref_dx, f"bwd_data {B,C,K,N,n,crop}")
+    check(dw, ref_dw, f"bwd_filter {B,C,K,N,n,crop}")
+    x = torch.from_numpy(d["x"]).cuda(); w = torch.from_numpy(d["w"]).cuda()
+    dy = torch.from_numpy(d["dy"]).cuda()
+    dxf, dwf = oaa.conv_bwd(x, dy, w, crop)
+    torch.cuda.synchronize()
+    check(dxf.cpu().numpy(), ref_dx, "fused dx")
+    check(dwf.cpu().numpy(), ref_dw, "fused dw")
+    if C <= 4 or (C >= 16 and K >= 16):
+        yo = oaa.conv_fwd_oas(x, w, crop)
+        torch.cuda.synchronize()
+        check(yo.cpu().numpy(), oracle.conv_fwd(d["x"], d["w"], crop), "oas")
