@@ -506,3 +506,31 @@ def test_random_shapes_all_ops(B, C, K, N, n, crop):
         yo = oaa.conv_fwd_oas(x, w, crop)
         torch.cuda.synchronize()
         check(yo.cpu().numpy(), oracle.conv_fwd(d["x"], d["w"], crop), "oas")
+
+
+def _random_large_shapes(count, seed):
+    """Seeded random large images (N up to the 256-column limit): many tile rows, up to 8
+    chunk warps, both SIMT and tensor-core families."""
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        n = int(rng.integers(2, 9))
+        N = int(rng.integers(100, 251))
+        crop = CROPS[int(rng.integers(0, 3))]
+        if max(-(-N // n) * n, N + n - 1 if crop == "full" else N) > 256:
+            continue
+        if len(out) % 2 == 0:
+            B, C, K = int(rng.integers(1, 3)), int(rng.integers(1, 5)), int(rng.integers(1, 12))
+        else:
+            B, C, K = 1, int(rng.integers(16, 24)), int(rng.integers(16, 24))
+        out.append((B, C, K, N, n, crop))
+    return out
+
+
+@pytest.mark.parametrize("B,C,K,N,n,crop", _random_large_shapes(30, 77))
+def test_random_large_shapes(B, C, K, N, n, crop):
+    d = make_inputs(B, C, K, N, n, crop, seed=B + C * 3 + K * 5 + N + n)
+    y, dx, dw = run_all(d, N, n, crop)
+    check(y, oracle.conv_fwd(d["x"], d["w"], crop), f"fwd {B,C,K,N,n,crop}")
+    check(dx, oracle.conv_bwd_data(d["dy"], d["w"], N, crop), f"bwd_data {B,C,K,N,n,crop}")
+    check(dw, oracle.conv_bwd_filter(d["x"], d["dy"], n, crop), f"bwd_filter {B,C,K,N,n,crop}")
