@@ -19,7 +19,7 @@ for (B, C, K, N, n, crop) in CASES:
     oaa.conv_bwd_data(dy, w, N, crop)
     oaa.conv_bwd_filter(x, dy, n, crop)
     oaa.conv_bwd(x, dy, w, crop)
-    if C <= 4:
+    if C <= 4 or (C >= 16 and K >= 16):
         oaa.conv_fwd_oas(x, w, crop)
     oaa.PreparedWeights(w, N, "fwd", crop).fwd(x)
     torch.cuda.synchronize()
