@@ -67,12 +67,12 @@ struct BinGemmParams {
   // mode 2 (fwd / bwd_data, read by oaa_walk_kernel in load mode): column bt = (b·TT + t1)·TT
   // + t2 is walker slot s = ((b·TT + t1)·NT4 + t2 / TPW)·TPW + t2 % TPW (tile rows padded to
   // whole walker chunks of TPW tiles); row m = ri·Cf + o of bin f = f1·P + f2 goes to
-  //   D[o·plane + (s / 8)·16·F + ri·8·F + f·8 + s % 8],   F = H·P bins,
-  // i.e. blocks of 8 slots: every bin's run is one aligned 32-byte sector, and a walker chunk
+  //   D[o·plane + (s / SB)·2·SB·F + ri·SB·F + f·SB + s % SB],   F = H·P bins, SB = 32 slots,
+  // i.e. blocks of 32 slots: every bin's run is one aligned 128-byte line, and a walker chunk
   // spans one or two blocks
   int a_split;  // A arrives pre-split ([F][Kc][hi|lo][RTA][4096])
   int b_split;  // B arrives pre-split likewise (else the converter warps split it)
-  int TT, TPW, NT4, SB, SBL;  // SB = 1 << SBL slots per block (8 in the text below)
+  int TT, TPW, NT4, SB, SBL;  // SB = 1 << SBL slots per block (32, oaa_walk.cuh kYSBL)
   long long plane;
 };
 

@@ -311,8 +311,8 @@ __global__ void __launch_bounds__(256, (LOAD && NN <= 6) ? 2 : 1) oaa_walk_kerne
   }
   // LOAD: this lane's Ŷ row (bins f1·P + f2) for chunk (t1, i), prefetched one chunk ahead
   float ynr[LOAD ? P : 1], yni[LOAD ? P : 1];
-  // Ŷ in the layout of oaa_bin_gemm_kernel mode 2: blocks of 8 walker slots, per bin one
-  // 32-byte run; the chunk's TPW slots lie in one or two blocks
+  // Ŷ in the layout of oaa_bin_gemm_kernel mode 2: blocks of 32 walker slots, per bin one
+  // 128-byte run; the chunk's TPW slots lie in one or two blocks
   constexpr int SB = 1 << kYSBL, BF8 = SB * H * P;
   const int NT4 = (p.T + TPW - 1) / TPW;
   const size_t dplane = LOAD ? ((size_t)(p.BTc / p.T) * NT4 * TPW + SB - 1) / SB * 2 * BF8 : 0;
