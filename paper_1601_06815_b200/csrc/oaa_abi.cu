@@ -410,22 +410,29 @@ TcPlan plan_tc(int B, int Cin, int Cout, int R, int n) {
 constexpr int kWalkMaxCin = 4;
 struct WalkHostGeo {
   bool use;
-  int TPW, CW, RS4, CH4, NCH, KG, ngrp;
+  int BB, P, H, T, TPW, CW, RS4, CH4, NCH, KG, ngrp;  // BB = block size b, T = ⌈R / b⌉ tiles per side
   size_t spec_b, xs_b;
 };
-WalkHostGeo plan_walk(bool is_fwd, int B, int Cin, int Cout, int T, int Ro, int off, int n, const TcPlan& tc) {
+WalkHostGeo plan_walk(bool is_fwd, int B, int Cin, int Cout, int R, int Ro, int off, int n, const TcPlan& tc) {
   WalkHostGeo w{};
   w.use = is_fwd && !tc.use && Cin <= kWalkMaxCin;
-  const int H = n;
-  w.TPW = 32 / H;
-  w.CW = w.TPW * n;
-  w.RS4 = n | 1;
-  w.CH4 = w.TPW * H * w.RS4;
+  // block size: for 3 ≤ n ≤ 7 the blocks grow to
+  // b = 16 − n, so every block uses the P = 15 grid of n = 8 (PFA 3×5 codelets, 8 spectrum rows,
+  // 4 blocks per warp) and yields b² instead of n² outputs -- once the image holds ≥ 3 of them
+  const int big = walk_block_big(n);
+  w.BB = (big != n && R >= 3 * big) ? big : n;
+  w.P = w.BB + n - 1;
+  w.H = (w.P + 1) / 2;
+  w.T = cdiv(R, w.BB);
+  w.TPW = 32 / w.H;
+  w.CW = w.TPW * w.BB;
+  w.RS4 = w.H | 1;
+  w.CH4 = w.TPW * w.H * w.RS4;
   w.NCH = cdiv(off + Ro, w.CW);
   w.KG = std::min(8, Cout);
   w.ngrp = cdiv(Cout, w.KG);
-  w.spec_b = align_up(sizeof(float4) * (size_t)Cin * Cout * n * H);
-  w.xs_b = align_up(sizeof(float4) * (size_t)B * T * w.NCH * Cin * w.CH4);
+  w.spec_b = align_up(sizeof(float4) * (size_t)Cin * Cout * w.H * w.H);
+  w.xs_b = align_up(sizeof(float4) * (size_t)B * w.T * w.NCH * Cin * w.CH4);
   return w;
 }
 
@@ -796,7 +803,7 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
   EnginePlan e;
   if (!plan_engine(R, Ro, off, n, Cin, Cout, &e, tc.use)) return OAA_ERR_UNSUPPORTED;
   if (B == 0) return OAA_OK;
-  const WalkHostGeo wk = plan_walk(is_fwd, B, Cin, Cout, e.T, Ro, off, n, tc);
+  const WalkHostGeo wk = plan_walk(is_fwd, B, Cin, Cout, R, Ro, off, n, tc);
   const BwddPlan bd = plan_bwdd(is_fwd, B, Cout, R, n, tc);
   EngineWs L = engine_ws(B, C, K, e.T, g, tc, &wk, &bd);
   if (!ws || ws_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0)
@@ -818,7 +825,7 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
     if (cudaMemsetAsync(out, 0, out_bytes, s) != cudaSuccess) return OAA_ERR_CUDA;
     if (!prepared) {
       KTimer kt(KID_SPECTRUM, s);
-      oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, spec, K, C, n, 1, 1);
+      oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, spec, K, C, n, 2 * n - 1, 1, 1);
       g_launches++;
       if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
     }
@@ -843,7 +850,7 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
   if (wk.use) {
     if (!prepared) {
       KTimer kt(KID_SPECTRUM, s);
-      oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, spec, K, C, n, 0, 1);
+      oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, spec, K, C, n, wk.P, 0, 1);
       g_launches++;
       if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
     }
@@ -852,11 +859,11 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
     xp.S = reinterpret_cast<float4*>(base + L.xg_off);
     xp.Cin = Cin;
     xp.R = R;
-    xp.T = e.T;
+    xp.T = wk.T;
     xp.NCH = wk.NCH;
     xp.SW = wk.NCH * wk.CW;
     xp.org = 0;
-    set_xspec_tma(xp, B, n);
+    set_xspec_tma(xp, B, wk.BB);
     oaa::WalkParams wp;
     wp.S = xp.S;
     wp.spec = spec;
@@ -864,7 +871,7 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
     wp.B = B;
     wp.Cin = Cin;
     wp.Cout = Cout;
-    wp.T = e.T;
+    wp.T = wk.T;
     wp.Ro = Ro;
     wp.off = off;
     wp.NCH = wk.NCH;
@@ -875,8 +882,9 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
     wpl.ngrp = wk.ngrp;
     wpl.NCH = wk.NCH;
     wpl.SW = xp.SW;
-    wpl.xspec_smem = oaa::xspec_smem_bytes(Cin, n, xp.SW, wk.CH4);
-    const int QSZ = ((2 * wk.TPW + 1) * n * g.P + 1) & ~1;
+    wpl.BB = wk.BB;
+    wpl.xspec_smem = oaa::xspec_smem_bytes(Cin, wk.BB, xp.SW, wk.CH4);
+    const int QSZ = ((2 * wk.TPW + 1) * wk.H * wk.P + 1) & ~1;
     wpl.walk_smem = sizeof(float4) * (size_t)oaa::kWalkRing * Cin * wk.CH4 + sizeof(float2) * (size_t)wk.KG * QSZ +
                     sizeof(float) * (size_t)wk.KG * oaa::walk_trp(n) * wk.NCH * wk.CW;
     if (wpl.walk_smem > 220 * 1024 || wpl.xspec_smem > 220 * 1024) return OAA_ERR_UNSUPPORTED;
@@ -890,7 +898,7 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
   const int loop_is_k = (is_fwd == e.S1) ? 1 : 0;  // fwd S1 / bwd_data S2 loop over k
   if (!prepared) {
     KTimer kt(KID_SPECTRUM, s);
-    oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, spec, K, C, n, is_fwd ? 0 : 1, loop_is_k);
+    oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, spec, K, C, n, 2 * n - 1, is_fwd ? 0 : 1, loop_is_k);
     g_launches++;
     if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
   }
@@ -1147,7 +1155,7 @@ size_t oaa_conv_workspace_bytes(oaa_op_t op, int B, int C, int K, int N, int n, 
     const int R = fwd ? N : g.M;
     const TcPlan tc = plan_tc(B, fwd ? C : K, fwd ? K : C, R, n);
     const int Ro = fwd ? g.M : N, off = fwd ? g.o : (n - 1 - g.o);
-    const WalkHostGeo wk = plan_walk(fwd, B, fwd ? C : K, fwd ? K : C, cdiv(R, n), Ro, off, n, tc);
+    const WalkHostGeo wk = plan_walk(fwd, B, fwd ? C : K, fwd ? K : C, R, Ro, off, n, tc);
     const BwddPlan bd = plan_bwdd(fwd, B, fwd ? K : C, R, n, tc);
     return engine_ws(B, C, K, cdiv(R, n), g, tc, &wk, &bd).total;
   }
@@ -1189,14 +1197,14 @@ SpecPlan spec_plan(bool is_fwd, int C, int K, int N, int n, const Geo& g) {
   const TcPlan tc = plan_tc(1, Cin, Cout, R, n);
   EnginePlan e;
   if (!plan_engine(R, Ro, off, n, Cin, Cout, &e, tc.use)) return sp;
-  const WalkHostGeo wk = plan_walk(is_fwd, 1, Cin, Cout, e.T, Ro, off, n, tc);
+  const WalkHostGeo wk = plan_walk(is_fwd, 1, Cin, Cout, R, Ro, off, n, tc);
   const BwddPlan bd = plan_bwdd(is_fwd, 1, Cout, R, n, tc);
-  (void)wk;
   (void)bd;
   sp.ok = true;
   // the TC path's real-ified, pre-split UMMA-blocked weights, else the float4 bin-pair
-  // spectra [.][.][n][n] of the walker / bwd_data / engine kernels (same size, own order)
-  sp.bytes = tc.use ? align_up(tc.ag_b) : align_up(sizeof(float4) * (size_t)K * C * n * n);
+  // spectra [.][.][n][n] of the bwd_data / engine kernels ([.][.][H][H] for the walker,
+  // whose blocks may be larger than n)
+  sp.bytes = tc.use ? align_up(tc.ag_b) : wk.use ? wk.spec_b : align_up(sizeof(float4) * (size_t)K * C * n * n);
   return sp;
 }
 
@@ -1233,7 +1241,7 @@ oaa_status_t oaa_conv_bwd(const float* x, const float* dy, const float* w, float
     if (cudaMemsetAsync(dx, 0, x_bytes, s) != cudaSuccess) return OAA_ERR_CUDA;
     {
       KTimer kt(KID_SPECTRUM, s);
-      oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, spec, K, C, n, 1, 1);
+      oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, spec, K, C, n, 2 * n - 1, 1, 1);
       g_launches++;
       if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
     }
@@ -1319,7 +1327,7 @@ oaa_status_t oaa_conv_fwd_oas(const float* x, const float* w, float* y, int B, i
   prof.start();
   {
     KTimer kt(KID_SPECTRUM, s);
-    oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, spec, K, C, n, 0, 1);
+    oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, spec, K, C, n, 2 * n - 1, 0, 1);
     g_launches++;
     if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
   }
@@ -1488,10 +1496,10 @@ oaa_status_t oaa_weight_spectra(oaa_op_t op, const float* w, void* spec, size_t 
   } else {
     EnginePlan e;
     plan_engine(R, Ro, off, n, Cin, Cout, &e, false);
-    const WalkHostGeo wk = plan_walk(is_fwd, 1, Cin, Cout, e.T, Ro, off, n, tc);
+    const WalkHostGeo wk = plan_walk(is_fwd, 1, Cin, Cout, R, Ro, off, n, tc);
     const BwddPlan bd = plan_bwdd(is_fwd, 1, Cout, R, n, tc);
     const int loop_is_k = (wk.use || bd.use) ? 1 : ((is_fwd == e.S1) ? 1 : 0);
-    oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, static_cast<float4*>(spec), K, C, n, is_fwd ? 0 : 1,
+    oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, static_cast<float4*>(spec), K, C, n, wk.use ? wk.P : 2 * n - 1, is_fwd ? 0 : 1,
                                                     loop_is_k);
   }
   g_launches++;

@@ -248,11 +248,9 @@ __device__ __forceinline__ void block_row_spectrum(const float (&z)[NN][NN], con
 
 // Same as block_row_spectrum, reading the block row by row from staged shared memory
 // (row stride ld, block column origin c) so the n×n block is never held in registers.
-template <int NN>
+template <int NN, int P = 2 * NN - 1>
 __device__ __forceinline__ void block_row_spectrum_smem(const float* src, int ld, int c, const float (&cf)[NN],
-                                                        const float (&sf)[NN], float (&xr)[2 * NN - 1],
-                                                        float (&xi)[2 * NN - 1]) {
-  constexpr int P = 2 * NN - 1;
+                                                        const float (&sf)[NN], float (&xr)[P], float (&xi)[P]) {
   float rr[P], ri[P];
 #pragma unroll
   for (int p1 = 0; p1 < NN; ++p1) {
@@ -1378,9 +1376,11 @@ __global__ void __launch_bounds__(256) oaa_filter_finalize_small_kernel(const fl
 // R[p1][f2] = Σ_p2 v[p1][p2]·e^{−2πi f2 p2/P} (n terms) goes to shared memory, then each
 // bin pair is Σ_p1 R[p1][f]·e^{−2πi f1 p1/P} (n terms) -- the separable 2-D DFT, fp64
 // throughout, rounded to fp32 once.
+// P: the transform size, 2n−1 for blocks of the kernel's size, b + n − 1 for the walker's
+// larger blocks b (oaa_walk.cuh; P odd, H = P2 = (P + 1) / 2 half-spectrum rows / bin pairs).
 __global__ void __launch_bounds__(128) oaa_spectrum_kernel(const float* __restrict__ w, float4* __restrict__ spec,
-                                                           int K, int C, int n, int flip, int loop_is_k) {
-  const int P = 2 * n - 1, H = n, P2 = (P + 1) / 2;
+                                                           int K, int C, int n, int P, int flip, int loop_is_k) {
+  const int H = (P + 1) / 2, P2 = (P + 1) / 2;
   __shared__ double tc[16], ts[16];  // cos / sin (2π m / P), fp64
   __shared__ double v[64];           // the kernel (flipped for bwd_data)
   __shared__ double Rr[8 * 15], Ri[8 * 15];

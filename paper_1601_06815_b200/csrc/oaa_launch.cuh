@@ -188,14 +188,17 @@ cudaError_t launch_filter_spectra_n(const oaa::FiltSpecParams& p, bool xwin, int
 // Walker forward (small Cin): block spectra X̂ of the input, then the walker.
 struct WalkPlan {
   int KG, ngrp, NCH, SW;
+  int BB;  // block size b: n, or walk_block_big(n) (oaa_walk.cuh WalkGeo)
   size_t xspec_smem, walk_smem;
 };
+// the walker's larger block for 3 ≤ n ≤ 7: b = 16 − n, i.e. P = b + n − 1 = 15 (the n = 8 grid)
+constexpr int walk_block_big(int n) { return (n >= 3 && n <= 7) ? 16 - n : n; }
 
-template <int NN>
-cudaError_t launch_walk_n(const oaa::XSpecParams& xp, const oaa::WalkParams& wp, const WalkPlan& w, int cr,
-                          cudaStream_t s) {
+template <int NN, int BB>
+cudaError_t launch_walk_nb(const oaa::XSpecParams& xp, const oaa::WalkParams& wp, const WalkPlan& w, int cr,
+                           cudaStream_t s) {
   {
-    auto k = oaa::oaa_xspec_kernel<NN, false>;
+    auto k = oaa::oaa_xspec_kernel<NN, false, BB>;
     cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w.xspec_smem);
     if (err != cudaSuccess) return err;
     {
@@ -205,8 +208,8 @@ cudaError_t launch_walk_n(const oaa::XSpecParams& xp, const oaa::WalkParams& wp,
     g_launches++;
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
   }
-  auto k = cr <= 1 ? oaa::oaa_walk_kernel<NN, 1> : cr == 2 ? oaa::oaa_walk_kernel<NN, 2>
-         : cr == 3 ? oaa::oaa_walk_kernel<NN, 3> : oaa::oaa_walk_kernel<NN, 4>;
+  auto k = cr <= 1 ? oaa::oaa_walk_kernel<NN, 1, false, false, BB> : cr == 2 ? oaa::oaa_walk_kernel<NN, 2, false, false, BB>
+         : cr == 3 ? oaa::oaa_walk_kernel<NN, 3, false, false, BB> : oaa::oaa_walk_kernel<NN, 4, false, false, BB>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w.walk_smem);
   if (err != cudaSuccess) return err;
   {
@@ -215,6 +218,13 @@ cudaError_t launch_walk_n(const oaa::XSpecParams& xp, const oaa::WalkParams& wp,
   }
   g_launches++;
   return cudaGetLastError();
+}
+template <int NN>
+cudaError_t launch_walk_n(const oaa::XSpecParams& xp, const oaa::WalkParams& wp, const WalkPlan& w, int cr,
+                          cudaStream_t s) {
+  if constexpr (walk_block_big(NN) != NN)
+    if (w.BB != NN) return launch_walk_nb<NN, walk_block_big(NN)>(xp, wp, w, cr, s);
+  return launch_walk_nb<NN, NN>(xp, wp, w, cr, s);
 }
 
 // Overlap-and-save forward (NEXT-2): (2n−1)² input-window spectra, then the walker in OAS mode.

@@ -34,11 +34,15 @@
 
 namespace oaa {
 
-template <int NN>
+// NN = kernel size n, BB = block size b (the paper's OaA has b = n; the walker
+// also runs b = 16 − n for 3 ≤ n ≤ 7, SURVEY.md §8(f) NEXT-4 "block size b ≠ n"): P = b + n − 1
+// is the smallest exact transform size (linear convolution of a b×b block with an n×n
+// kernel), odd in both cases, so H = P2 = (P + 1) / 2 half-spectrum rows / f2 pairs.
+template <int NN, int BB = NN>
 struct WalkGeo {
-  static constexpr int P = 2 * NN - 1, H = NN, P2 = NN;  // f2 pairs (the last one half zero)
+  static constexpr int P = BB + NN - 1, H = (P + 1) / 2, P2 = (P + 1) / 2;  // f2 pairs (the last one half zero)
   static constexpr int TPW = 32 / H;                     // tiles per chunk
-  static constexpr int CW = TPW * NN;                    // output columns per chunk
+  static constexpr int CW = TPW * BB;                    // output columns per chunk (stage B: ⌈CW/32⌉ rounds)
   static constexpr int RS4 = P2 | 1;                     // float4 per spectrum row (odd: LDS.128 conflict free)
   static constexpr int CH4 = TPW * H * RS4;              // float4 per channel in a chunk
   static constexpr int QT = H * P;                       // float2 per tile in Q
@@ -76,11 +80,13 @@ inline size_t xspec_smem_bytes(int Cin, int rows, int SW, int CH4) {
   return sizeof(float) * xspec_rows_floats(Cin, rows, SW) + 8 * 16 * (size_t)CH4;
 }
 
-template <int NN, bool WIN>
+// BB: block size of the forward blocks (WIN = false); the x-windows (WIN) keep b = n.
+template <int NN, bool WIN, int BB = NN>
 __global__ void __launch_bounds__(256) oaa_xspec_kernel(const __grid_constant__ XSpecParams p) {
-  using G = WalkGeo<NN>;
+  static_assert(!WIN || BB == NN, "x-windows are for blocks of the kernel's size");
+  using G = WalkGeo<NN, BB>;
   constexpr int P = G::P, H = G::H, RS4 = G::RS4;
-  constexpr int ROWS = WIN ? P : NN;
+  constexpr int ROWS = WIN ? P : BB;
   extern __shared__ __align__(128) float rows_s[];  // [Cin][ROWS][SW] | per-warp output tile
   __shared__ float2 tw_s[16];                        // (cos, sin)(2π m / P), m < P
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -104,7 +110,7 @@ __global__ void __launch_bounds__(256) oaa_xspec_kernel(const __grid_constant__ 
       asm volatile(
           "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
               smem_u32(rows_s)),
-          "l"(reinterpret_cast<uint64_t>(&p.tmap)), "r"(org), "r"(t1 * NN + org), "r"(b * p.Cin), "r"(smem_u32(&tbar))
+          "l"(reinterpret_cast<uint64_t>(&p.tmap)), "r"(org), "r"(t1 * BB + org), "r"(b * p.Cin), "r"(smem_u32(&tbar))
           : "memory");
     }
     __syncthreads();  // (the barrier init is visible before anyone waits)
@@ -113,7 +119,7 @@ __global__ void __launch_bounds__(256) oaa_xspec_kernel(const __grid_constant__ 
     const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
     for (int sg = warp; sg < p.Cin * ROWS; sg += nw) {
       const int c = sg / ROWS, rr = sg - (sg / ROWS) * ROWS;
-      const int r = t1 * NN + org + rr;
+      const int r = t1 * BB + org + rr;
       const bool rok = r >= 0 && r < p.R;
       const float* src = in_b + ((size_t)c * p.R + (rok ? r : 0)) * p.R;
       float* d = rows_s + (c * ROWS + rr) * p.SW;
@@ -151,19 +157,19 @@ __global__ void __launch_bounds__(256) oaa_xspec_kernel(const __grid_constant__ 
     const int i = ic / p.Cin, c = ic - (ic / p.Cin) * p.Cin;
     float xr[P], xi[P];
     const float* blk = rows_s + c * ROWS * p.SW;
-    const int c0 = (i * G::TPW + tt) * NN;
+    const int c0 = (i * G::TPW + tt) * BB;
     if constexpr (!WIN) {
       // (pruned blocks: per-task sincospif measured faster than the hoisted table values,
       // 0.143 vs 0.165 ms at the headline -- more registers live across the task loop)
-      float cf[NN], sf[NN];
+      float cf[BB], sf[BB];
 #pragma unroll
-      for (int p1 = 0; p1 < NN; ++p1) {
+      for (int p1 = 0; p1 < BB; ++p1) {
         float s, co;
         sincospif(2.0f * (float)((f1 * p1) % P) / (float)P, &s, &co);
         cf[p1] = co;
         sf[p1] = s;
       }
-      block_row_spectrum_smem<NN>(blk, p.SW, c0, cf, sf, xr, xi);
+      block_row_spectrum_smem<BB, P>(blk, p.SW, c0, cf, sf, xr, xi);
     } else {
       // column DFT of the window rows (row p1 = 0 has twiddle 1), rows read as float4
       // when the staged width keeps them 16-byte aligned (c0 = t2·n)
@@ -254,9 +260,10 @@ __host__ __device__ constexpr int walk_trp(int n) { return ((n - 1) + 3) & ~3; }
 // 4 warps run 3 per SM -- the load walker is latency bound on its Ŷ reads; measured
 // AlexNet-like fwd 0.323 → 0.304 ms, bwd_data 0.117 → 0.107 ms.  For n ≥ 7 the cap cost
 // more than the occupancy gained: sharded-config fwd 4.53 → 5.29 ms per chunk.)
-template <int NN, int CR, bool LOAD = false, bool OAS = false>
+template <int NN, int CR, bool LOAD = false, bool OAS = false, int BB = NN>
 __global__ void __launch_bounds__(256, (LOAD && NN <= 6) ? 2 : 1) oaa_walk_kernel(const WalkParams p) {
-  using G = WalkGeo<NN>;
+  static_assert(BB == NN || (!LOAD && !OAS), "blocks b != n: forward walker only");
+  using G = WalkGeo<NN, BB>;
   constexpr int P = G::P, H = G::H, P2 = G::P2, TPW = G::TPW, CW = G::CW, RS4 = G::RS4, QT = G::QT;
   constexpr int TR = NN - 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -331,8 +338,10 @@ __global__ void __launch_bounds__(256, (LOAD && NN <= 6) ? 2 : 1) oaa_walk_kerne
     }
   };
   if (LOAD) load_y(0, 0);
-  // stage-B geometry: lane = column J = i·CW + lane, tile J/n = i·TPW + lq at p2 = pA
-  const int lq = lane / NN, pA = lane - (lane / NN) * NN;
+  // stage-B geometry: lane = column J = i·CW + lane (+ 32 per further round when CW > 32),
+  // tile J/b = i·TPW + lq at p2 = pA
+  constexpr int NRB = (CW + 31) / 32;
+  const int lq = lane / BB, pA = lane - (lane / BB) * BB;
   const bool laneB = lane < CW;
   const bool hasB = pA <= NN - 2;
   const size_t plane = (size_t)p.Ro * p.Ro;
@@ -340,12 +349,12 @@ __global__ void __launch_bounds__(256, (LOAD && NN <= 6) ? 2 : 1) oaa_walk_kerne
 
   int seq = 0;
   for (int t1 = 0; t1 < p.T; ++t1) {
-    const int r0 = t1 * NN - p.off;  // output row of block row 0
-    unsigned rowmask = 0;            // rows p1 < n of this tile row inside [0, Ro)
+    const int r0 = t1 * BB - p.off;  // output row of block row 0
+    unsigned rowmask = 0;            // rows p1 < b of this tile row inside [0, Ro)
 #pragma unroll
-    for (int p1 = 0; p1 < NN; ++p1)
+    for (int p1 = 0; p1 < BB; ++p1)
       if (r0 + p1 >= 0 && r0 + p1 < p.Ro) rowmask |= 1u << p1;
-    const bool rows_full = rowmask == (1u << NN) - 1u;
+    const bool rows_full = rowmask == (1u << BB) - 1u;
     for (int i = 0; i < p.NCH; ++i, ++seq) {
       const int s = seq % kWalkRing;
       if (!LOAD) mbar_wait(&full[s], (seq / kWalkRing) & 1);
@@ -450,67 +459,73 @@ __global__ void __launch_bounds__(256, (LOAD && NN <= 6) ? 2 : 1) oaa_walk_kerne
         }
       }
       // ---- stage B: horizontal overlap-add, c2r along f1, vertical carry, stores
-      if (!OAS && active && laneB) {
-        const int tA = i * TPW + lq;
-        const int offA = (half * TPW + lq) * QT + pA;
-        int offB = G::QS * QT;  // zero tile
-        if (hasB && tA >= 1) offB = (lq > 0 ? (half * TPW + lq - 1) : ((half ^ 1) * TPW + TPW - 1)) * QT + pA + NN;
-        float zr[H], zi[H];
 #pragma unroll
-        for (int k = 0; k < H; ++k) {
-          const float2 a = Q[offA + k * P], bb = Q[offB + k * P];
-          zr[k] = a.x + bb.x;
-          zi[k] = a.y + bb.y;
-        }
-        float y[P];
-        c2r_half<P>(zr, zi, y);
-        const int J = i * CW + lane;
-        const int j = J - p.off;
-        float4* cr = reinterpret_cast<float4*>(carry) + J;
-        float cv[TQ > 0 ? 4 * TQ : 4];
+      for (int rb = 0; rb < NRB; ++rb) {
+        const int jb = lane + 32 * rb;  // column of the chunk
+        const int lqr = NRB == 1 ? lq : jb / BB, pAr = NRB == 1 ? pA : jb - (jb / BB) * BB;
+        const bool hasBr = NRB == 1 ? hasB : pAr <= NN - 2;
+        if (!OAS && active && (NRB == 1 ? laneB : jb < CW)) {
+          const int tA = i * TPW + lqr;
+          const int offA = (half * TPW + lqr) * QT + pAr;
+          int offB = G::QS * QT;  // zero tile
+          if (hasBr && tA >= 1) offB = (lqr > 0 ? (half * TPW + lqr - 1) : ((half ^ 1) * TPW + TPW - 1)) * QT + pAr + BB;
+          float zr[H], zi[H];
 #pragma unroll
-        for (int q = 0; q < TQ; ++q) {
-          const float4 t = cr[q * CWT];
-          cv[4 * q] = t.x; cv[4 * q + 1] = t.y; cv[4 * q + 2] = t.z; cv[4 * q + 3] = t.w;
-        }
-        const bool colok = j >= 0 && j < p.Ro;
-        if (rows_full) {
-          if (colok) {
-            char* op = reinterpret_cast<char*>(outp + ((ptrdiff_t)r0 * p.Ro + j));
-            const ptrdiff_t rb = (ptrdiff_t)p.Ro * (ptrdiff_t)sizeof(float);
+          for (int k = 0; k < H; ++k) {
+            const float2 a = Q[offA + k * P], bb = Q[offB + k * P];
+            zr[k] = a.x + bb.x;
+            zi[k] = a.y + bb.y;
+          }
+          float y[P];
+          c2r_half<P>(zr, zi, y);
+          const int J = i * CW + jb;
+          const int j = J - p.off;
+          float4* cr = reinterpret_cast<float4*>(carry) + J;
+          float cv[TQ > 0 ? 4 * TQ : 4];
 #pragma unroll
-            for (int p1 = 0; p1 < NN; ++p1) {
+          for (int q = 0; q < TQ; ++q) {
+            const float4 t = cr[q * CWT];
+            cv[4 * q] = t.x; cv[4 * q + 1] = t.y; cv[4 * q + 2] = t.z; cv[4 * q + 3] = t.w;
+          }
+          const bool colok = j >= 0 && j < p.Ro;
+          if (rows_full) {
+            if (colok) {
+              char* op = reinterpret_cast<char*>(outp + ((ptrdiff_t)r0 * p.Ro + j));
+              const ptrdiff_t rbytes = (ptrdiff_t)p.Ro * (ptrdiff_t)sizeof(float);
+#pragma unroll
+              for (int p1 = 0; p1 < BB; ++p1) {
+                float v = y[p1];
+                if (p1 < TR) v += cv[p1];
+                __stcs(reinterpret_cast<float*>(op), v);
+                op += rbytes;
+              }
+            }
+          } else {
+            float* op = outp + (ptrdiff_t)r0 * p.Ro + j;
+#pragma unroll
+            for (int p1 = 0; p1 < BB; ++p1) {
               float v = y[p1];
               if (p1 < TR) v += cv[p1];
-              __stcs(reinterpret_cast<float*>(op), v);
-              op += rb;
+              if (colok && ((rowmask >> p1) & 1u)) __stcs(op + (ptrdiff_t)p1 * p.Ro, v);
             }
           }
-        } else {
-          float* op = outp + (ptrdiff_t)r0 * p.Ro + j;
 #pragma unroll
-          for (int p1 = 0; p1 < NN; ++p1) {
-            float v = y[p1];
-            if (p1 < TR) v += cv[p1];
-            if (colok && ((rowmask >> p1) & 1u)) __stcs(op + (ptrdiff_t)p1 * p.Ro, v);
+          for (int q = 0; q < TQ; ++q) {
+            float t[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) t[r] = (4 * q + r < TR) ? y[BB + 4 * q + r] : 0.f;
+            cr[q * CWT] = make_float4(t[0], t[1], t[2], t[3]);
           }
-        }
-#pragma unroll
-        for (int q = 0; q < TQ; ++q) {
-          float t[4];
-#pragma unroll
-          for (int r = 0; r < 4; ++r) t[r] = (4 * q + r < TR) ? y[NN + 4 * q + r] : 0.f;
-          cr[q * CWT] = make_float4(t[0], t[1], t[2], t[3]);
         }
       }
       __syncwarp();
     }
   }
   // flush: the carry holds the last tile row's bottom rows (final)
-  if (!OAS && active && laneB) {
-    const int r0 = p.T * NN - p.off;
-    for (int i = 0; i < p.NCH; ++i) {
-      const int J = i * CW + lane, j = J - p.off;
+  if (!OAS && active) {
+    const int r0 = p.T * BB - p.off;
+    for (int J = lane; J < p.NCH * CW; J += 32) {
+      const int j = J - p.off;
       if (j < 0 || j >= p.Ro) continue;
 #pragma unroll
       for (int p1 = 0; p1 < TR; ++p1) {

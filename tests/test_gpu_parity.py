@@ -120,6 +120,35 @@ def test_largest_images(n, crop):
     check(dw, oracle.conv_bwd_filter(d["x"], d["dy"], n, crop), f"bwd_filter N=250 n={n} {crop}")
 
 
+def _big_block_cases():
+    # forward walker with blocks b = 16 − n (P = 15) for 3 <= n <= 7 once N >= 3b: N at the
+    # threshold, one past it, ragged (the last block mostly padding) and several chunks per
+    # tile row (stage B in two 32-column rounds when 4b > 32); C = 1..4 register channels
+    out = []
+    for n in range(3, 8):
+        b = 16 - n
+        for i, N in enumerate(sorted({3 * b, 3 * b + 1, 4 * b - 1, 7 * b + 2, 100})):
+            out.append((1 + i % 2, 1 + (n + i) % 4, 3 + 2 * i, N, n))
+    return out
+
+
+@pytest.mark.parametrize("crop", CROPS)
+@pytest.mark.parametrize("B,C,K,N,n", _big_block_cases())
+def test_walker_block_size_b_ne_n(B, C, K, N, n, crop):
+    """SURVEY.md §8(f) NEXT-4 "block sizes b != n": the forward walker tiles the
+    input into b×b blocks, b = 16 − n, transformed on the (b + n − 1)² = 15² grid; the
+    result is the same linear convolution (every element vs the direct oracle), and
+    prepared spectra (their own P) give it bitwise."""
+    d = make_inputs(B, C, K, N, n, crop, seed=N * 7 + n * 3 + C)
+    x = torch.from_numpy(d["x"]).cuda()
+    w = torch.from_numpy(d["w"]).cuda()
+    y = oaa.conv_fwd(x, w, crop)
+    yp = oaa.PreparedWeights(w, N, "fwd", crop).fwd(x)
+    torch.cuda.synchronize()
+    assert torch.equal(y, yp)
+    check(y.cpu().numpy(), oracle.conv_fwd(d["x"], d["w"], crop), f"fwd b=16-n N={N} n={n} C={C} {crop}")
+
+
 @pytest.mark.parametrize("crop", CROPS)
 def test_config1_parity(crop):
     """BASELINE config 1: N=32, n=3, C=K=B=1, forward, vs CPU float64 direct."""
