@@ -481,24 +481,33 @@ cudaError_t launch_walk_oas(int n, const oaa::XSpecParams& xp, const oaa::WalkPa
 // bwd_data for few output channels (oaa_bwdd.cuh) ------------------------------------
 struct BwddPlan {
   bool use;
+  int BB, P, H, Td;  // dy block size b (as the forward walker's, plan_walk), grid, tiles per side
   int NCW, BW, RPC, WSL;
-  size_t spec_b, smem;
+  size_t smem;
 };
-BwddPlan plan_bwdd(bool is_fwd, int B, int Cout, int R, int n, const TcPlan& tc) {
+// allow_big = false: blocks of the kernel's size (the fused SIMT backward shares its dy tiling
+// with the weight-gradient body)
+BwddPlan plan_bwdd(bool is_fwd, int B, int Cout, int R, int n, const TcPlan& tc, bool allow_big = true) {
   BwddPlan d{};
   d.use = !is_fwd && !tc.use && Cout <= kWalkMaxCin;
-  const int H = n, P = 2 * n - 1, TPW = 32 / H, CW = TPW * n;
-  const int Td = cdiv(R, n);
-  d.NCW = cdiv(Td, TPW);
+  // (the larger blocks from 3 per side for n ≤ 4, from R ≥ 96 for n ≥ 5: measured at R = 58-60,
+  // n = 5 / 7, the fewer, larger blocks leave too few warps per CTA, 0.155 → 0.185 ms at n = 5)
+  const int big = walk_block_big(n);
+  d.BB = (allow_big && big != n && R >= 3 * big && (n <= 4 || R >= 96)) ? big : n;
+  d.P = d.BB + n - 1;
+  d.H = (d.P + 1) / 2;
+  const int TPW = 32 / d.H, CW = TPW * d.BB;
+  d.Td = cdiv(R, d.BB);
+  d.NCW = cdiv(d.Td, TPW);
   if (d.NCW > 8) d.use = false;  // ≤ 8 warps (256 threads)
   d.BW = d.NCW * CW;
   // narrow images: several (image, tile row) pairs per CTA so that it has 8 compute warps
   // sharing one Ŵ ring (a half-depth ring keeps two such CTAs per SM); the headline's 7
   // chunk warps keep one pair and the 16-deep ring
   // while keeping ≥ 2 CTAs per SM of work
-  d.RPC = (d.NCW >= 1 && d.NCW <= 4) ? std::max(1, std::min(8 / d.NCW, B * Td / 296)) : 1;
+  d.RPC = (d.NCW >= 1 && d.NCW <= 4) ? std::max(1, std::min(8 / d.NCW, B * d.Td / 296)) : 1;
   d.WSL = d.RPC > 1 ? 3 : 4;
-  d.smem = oaa::bwdd_smem_bytes(n, Cout, d.NCW, d.RPC, d.WSL);
+  d.smem = oaa::bwdd_smem_bytes(n, d.BB, Cout, d.NCW, d.RPC, d.WSL);
   if (d.smem > 220 * 1024) d.use = false;
   return d;
 }
@@ -546,7 +555,7 @@ EngineWs engine_ws(int B, int C, int K, int Tr, const Geo& g, const TcPlan& tc, 
   w.spec_off = 0;
   if (bd && bd->use) {
     w.flags_off = w.counter_off = w.d_off = w.xg_off = 0;
-    w.total = align_up(sizeof(float4) * (size_t)K * C * g.n * g.H);
+    w.total = align_up(sizeof(float4) * (size_t)K * C * bd->H * bd->H);
     return w;
   }
   if (wk && wk->use) {
@@ -825,7 +834,7 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
     if (cudaMemsetAsync(out, 0, out_bytes, s) != cudaSuccess) return OAA_ERR_CUDA;
     if (!prepared) {
       KTimer kt(KID_SPECTRUM, s);
-      oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, spec, K, C, n, 2 * n - 1, 1, 1);
+      oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, spec, K, C, n, bd.P, 1, 1);
       g_launches++;
       if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
     }
@@ -838,11 +847,12 @@ oaa_status_t run_engine(bool is_fwd, const float* in, const float* w, float* out
     dp.C = C;
     dp.M = R;
     dp.N = Ro;
-    dp.Td = e.T;
+    dp.Td = bd.Td;
     dp.off = off;
     dp.NCW = bd.NCW;
     dp.RPC = bd.RPC;
     dp.WSL = bd.WSL;
+    dp.BB = bd.BB;
     cudaError_t err = launch_bwdd(n, dp, C, bd.smem, s);
     prof.stop();
     return err == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
@@ -1064,9 +1074,9 @@ bool plan_bwd_fused(int B, int C, int K, int N, int n, oaa_crop_t crop, const Ge
     // SIMT family: both bodies fit 128 registers, ≤ 110 KB of shared memory and 256 TMEM
     // columns, and the weight-gradient CTA has the full 8 warps
     const TcPlan none{};
-    p->bd = plan_bwdd(false, B, C, g.M, n, none);
+    p->bd = plan_bwdd(false, B, C, g.M, n, none, false);
     p->bf = plan_bwdf(B, C, K, g.M, n);
-    const size_t bsm = oaa::bwdd_smem_bytes(n, C, p->bd.NCW, p->bd.RPC, p->bd.WSL);
+    const size_t bsm = oaa::bwdd_smem_bytes(n, n, C, p->bd.NCW, p->bd.RPC, p->bd.WSL);
     p->simt = B > 0 && p->bd.use && p->bf.use && p->bf.tm && p->bf.nwb == oaa::kBwdfWarps && bsm <= 110 * 1024 &&
               p->bf.smem <= 110 * 1024;
     if (p->simt) {
@@ -1199,12 +1209,14 @@ SpecPlan spec_plan(bool is_fwd, int C, int K, int N, int n, const Geo& g) {
   if (!plan_engine(R, Ro, off, n, Cin, Cout, &e, tc.use)) return sp;
   const WalkHostGeo wk = plan_walk(is_fwd, 1, Cin, Cout, R, Ro, off, n, tc);
   const BwddPlan bd = plan_bwdd(is_fwd, 1, Cout, R, n, tc);
-  (void)bd;
   sp.ok = true;
   // the TC path's real-ified, pre-split UMMA-blocked weights, else the float4 bin-pair
-  // spectra [.][.][n][n] of the bwd_data / engine kernels ([.][.][H][H] for the walker,
+  // spectra [.][.][n][n] of the engine kernels ([.][.][H][H] for the walker and bwd_data,
   // whose blocks may be larger than n)
-  sp.bytes = tc.use ? align_up(tc.ag_b) : wk.use ? wk.spec_b : align_up(sizeof(float4) * (size_t)K * C * n * n);
+  sp.bytes = tc.use   ? align_up(tc.ag_b)
+             : wk.use ? wk.spec_b
+             : bd.use ? align_up(sizeof(float4) * (size_t)K * C * bd.H * bd.H)
+                      : align_up(sizeof(float4) * (size_t)K * C * n * n);
   return sp;
 }
 
@@ -1248,7 +1260,7 @@ oaa_status_t oaa_conv_bwd(const float* x, const float* dy, const float* w, float
     oaa::BwdDParams dp;
     dp.dy = dy; dp.spec = spec; dp.dx = dx; dp.B = B; dp.K = K; dp.C = C; dp.M = g.M; dp.N = N;
     dp.Td = cdiv(g.M, n); dp.off = n - 1 - g.o; dp.NCW = fp.bd.NCW;
-    dp.RPC = fp.bd.RPC; dp.WSL = fp.bd.WSL;
+    dp.RPC = fp.bd.RPC; dp.WSL = fp.bd.WSL; dp.BB = n;
     oaa::XSpecParams xp;
     xp.in = x; xp.S = reinterpret_cast<float4*>(base + fp.data_b); xp.Cin = C; xp.R = N; xp.T = bf.Td;
     xp.NCH = bf.NCH; xp.SW = bf.SW; xp.org = g.o - (n - 1);
@@ -1499,7 +1511,7 @@ oaa_status_t oaa_weight_spectra(oaa_op_t op, const float* w, void* spec, size_t 
     const WalkHostGeo wk = plan_walk(is_fwd, 1, Cin, Cout, R, Ro, off, n, tc);
     const BwddPlan bd = plan_bwdd(is_fwd, 1, Cout, R, n, tc);
     const int loop_is_k = (wk.use || bd.use) ? 1 : ((is_fwd == e.S1) ? 1 : 0);
-    oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, static_cast<float4*>(spec), K, C, n, wk.use ? wk.P : 2 * n - 1, is_fwd ? 0 : 1,
+    oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, static_cast<float4*>(spec), K, C, n, wk.use ? wk.P : bd.use ? bd.P : 2 * n - 1, is_fwd ? 0 : 1,
                                                     loop_is_k);
   }
   g_launches++;

@@ -36,24 +36,31 @@ struct BwdDParams {
   int NCW;                     // chunk warps per tile row
   int RPC;                     // (image, tile row) pairs per CTA: RPC·NCW ≤ 8 compute warps
   int WSL;                     // log2 of the Ŵ ring depth (≤ kBwddWStages)
+  int BB;                      // dy block size b (n, or 16 − n: the launcher picks the instantiation)
 };
 
 constexpr int kBwddStages = 8;    // per-warp dy ring depth (covers HBM latency)
 constexpr int kBwddWStages = 16;  // max shared Ŵ ring depth: how far the fastest warp may run ahead
-
-__host__ __device__ constexpr size_t bwdd_dy_bytes(int n, int NCW, int RPC) {
-  return (size_t)RPC * NCW * kBwddStages * n * ((32 / n) * n) * 4;
+// dy ring depth for blocks b: 8 slices of n = b rows, 4 of the larger b = 16 − n (more
+// bytes per slice; the ring then still holds more bytes in flight than at n = 8)
+__host__ __device__ constexpr int bwdd_stages(int n, int bb) { return bb > n ? 4 : kBwddStages; }
+// geometry of WalkGeo<n, bb>: H = (b + n) / 2 spectrum rows, TPW = 32 / H blocks per warp
+__host__ __device__ constexpr int bwdd_h(int n, int bb) { return (bb + n) / 2; }
+__host__ __device__ constexpr size_t bwdd_dy_bytes(int n, int bb, int NCW, int RPC) {
+  return (size_t)RPC * NCW * bwdd_stages(n, bb) * bb * ((32 / bwdd_h(n, bb)) * bb) * 4;
 }
-__host__ __device__ constexpr size_t bwdd_q_bytes(int n, int NCW, int RPC) {
-  return (size_t)RPC * (NCW * (32 / n) + 1) * n * (2 * n - 1) * 8;
+__host__ __device__ constexpr size_t bwdd_q_bytes(int n, int bb, int NCW, int RPC) {
+  return (size_t)RPC * (NCW * (32 / bwdd_h(n, bb)) + 1) * bwdd_h(n, bb) * (bb + n - 1) * 8;
 }
-// bytes of one Ŵ ring stage ([C][n][n] float4, padded to 128 B)
-__host__ __device__ constexpr int bwdd_w_bytes(int n, int C) { return (C * n * n * 16 + 127) & ~127; }
+// bytes of one Ŵ ring stage ([C][H][H] float4, padded to 128 B)
+__host__ __device__ constexpr int bwdd_w_bytes(int n, int bb, int C) {
+  return (C * bwdd_h(n, bb) * bwdd_h(n, bb) * 16 + 127) & ~127;
+}
 // Ŵ ring | dy ring (the epilogue's Q buffer reuses the dy ring: the k loop is over by then)
-__host__ __device__ constexpr size_t bwdd_smem_bytes(int n, int C, int NCW, int RPC, int WSL) {
-  return ((size_t)1 << WSL) * bwdd_w_bytes(n, C) +
-         (bwdd_dy_bytes(n, NCW, RPC) > bwdd_q_bytes(n, NCW, RPC) ? bwdd_dy_bytes(n, NCW, RPC)
-                                                                  : bwdd_q_bytes(n, NCW, RPC));
+__host__ __device__ constexpr size_t bwdd_smem_bytes(int n, int bb, int C, int NCW, int RPC, int WSL) {
+  return ((size_t)1 << WSL) * bwdd_w_bytes(n, bb, C) +
+         (bwdd_dy_bytes(n, bb, NCW, RPC) > bwdd_q_bytes(n, bb, NCW, RPC) ? bwdd_dy_bytes(n, bb, NCW, RPC)
+                                                                          : bwdd_q_bytes(n, bb, NCW, RPC));
 }
 
 __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
@@ -69,12 +76,13 @@ __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
 // compute warp w works on pair w / NCW, chunk w mod NCW.
 // TM = true: the C output spectra are accumulated in tensor memory (96 columns per warp)
 // instead of registers, so the kernel fits 128 registers and two CTAs share an SM.
-template <int NN, int CR, bool TM = false>
+// BB: dy block size b (WalkGeo; b = n is the paper's OaA, b = 16 − n the P = 15 grid)
+template <int NN, int CR, bool TM = false, int BB = NN>
 __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
-  using G = WalkGeo<NN>;
+  using G = WalkGeo<NN, BB>;
   constexpr int P = G::P, H = G::H, P2 = G::P2, TPW = G::TPW, QT = G::QT, CW = G::CW;
-  constexpr int S = kBwddStages;
-  constexpr int DYS = NN * CW;                // floats per warp stage
+  constexpr int S = bwdd_stages(NN, BB);
+  constexpr int DYS = BB * CW;                // floats per warp stage
   const int SW = 1 << p.WSL, SWM = SW - 1;    // Ŵ ring depth (power of two)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t wfull[kBwddWStages];
@@ -88,7 +96,7 @@ __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
   const bool pair_ok = pair < npairs;
   const int b = pair_ok ? pair / p.Td : 0, t1 = pair_ok ? pair - (pair / p.Td) * p.Td : 0;
   const int w4 = p.C * P2 * H;                // float4 of kernel spectra per dy channel
-  const int wst = bwdd_w_bytes(NN, p.C);      // bytes per Ŵ stage
+  const int wst = bwdd_w_bytes(NN, BB, p.C);  // bytes per Ŵ stage
   unsigned char* Wring = smem_raw;
   float* dyring = reinterpret_cast<float*>(smem_raw + (size_t)SW * wst);
   const uint32_t wbytes = (uint32_t)w4 * 16u;
@@ -145,32 +153,38 @@ __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
   // compute warp w: TMEM lanes 32·(w mod 4).., columns 128·(w / 4) + 32·c
   const uint32_t tacc = TM ? s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * 128u : 0u;
 
-  // ---------------- compute warps: each stages its own columns of the n dy rows
+  // ---------------- compute warps: each stages its own columns of the b dy rows
+  // (CW > 32 for the larger blocks: a lane stages columns lane, lane + 32)
+  constexpr int NCR = (CW + 31) / 32;
   const size_t planeM = (size_t)p.M * p.M;
-  const int col = wchunk * CW + lane;                   // staged column (lane < CW)
-  const bool cok = pair_ok && lane < CW && col < p.M;
-  int nrow = p.M - t1 * NN;                             // dy rows of this tile row inside dy
-  nrow = nrow < NN ? nrow : NN;
-  const float* src0 = p.dy + (size_t)b * p.K * planeM + (size_t)(t1 * NN) * p.M + (cok ? col : 0);
+  int nrow = p.M - t1 * BB;                             // dy rows of this tile row inside dy
+  nrow = nrow < BB ? nrow : BB;
+  const float* srcb = p.dy + (size_t)b * p.K * planeM + (size_t)(t1 * BB) * p.M;
   float* mydy = dyring + (size_t)warp * S * DYS;
   auto stage_dy = [&](int k) {
-    if (k < p.K && lane < CW) {
-      const float* src = src0 + (size_t)k * planeM;
-      float* d = mydy + (k % S) * DYS + lane;
-      if (cok && nrow == NN) {
 #pragma unroll
-        for (int rr = 0; rr < NN; ++rr) {
-          cp_async4(d, src, true);
-          src += p.M;
-          d += CW;
-        }
-      } else {
+    for (int cr = 0; cr < NCR; ++cr) {
+      const int cl = lane + 32 * cr;                    // column of the chunk
+      const int col = wchunk * CW + cl;
+      const bool cok = pair_ok && cl < CW && col < p.M;
+      if (k < p.K && cl < CW) {
+        const float* src = srcb + (cok ? col : 0) + (size_t)k * planeM;
+        float* d = mydy + (k % S) * DYS + cl;
+        if (cok && nrow == BB) {
 #pragma unroll
-        for (int rr = 0; rr < NN; ++rr) {
-          const bool ok = cok && rr < nrow;
-          cp_async4(d, ok ? src : p.dy, ok);
-          src += p.M;
-          d += CW;
+          for (int rr = 0; rr < BB; ++rr) {
+            cp_async4(d, src, true);
+            src += p.M;
+            d += CW;
+          }
+        } else {
+#pragma unroll
+          for (int rr = 0; rr < BB; ++rr) {
+            const bool ok = cok && rr < nrow;
+            cp_async4(d, ok ? src : p.dy, ok);
+            src += p.M;
+            d += CW;
+          }
         }
       }
     }
@@ -182,9 +196,9 @@ __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
   const int tt = lane / H, f1 = lane - (lane / H) * H;
   const bool laneA = tt < TPW;
   const int t2 = wchunk * TPW + tt;
-  float cf[NN], sf[NN];
+  float cf[BB], sf[BB];
 #pragma unroll
-  for (int p1 = 0; p1 < NN; ++p1) {
+  for (int p1 = 0; p1 < BB; ++p1) {
     float s, c;
     sincospif(2.0f * (float)((f1 * p1) % P) / (float)P, &s, &c);
     cf[p1] = c;
@@ -269,7 +283,7 @@ __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
       __syncwarp();
       w_wait(k);
       float gr[P], gi[P];
-      block_row_spectrum_smem<NN>(mydy + s0 * DYS, CW, (laneA ? tt : 0) * NN, cf, sf, gr, gi);
+      block_row_spectrum_smem<BB, P>(mydy + s0 * DYS, CW, (laneA ? tt : 0) * BB, cf, sf, gr, gi);
       accum_tm(k, gr, gi);
       __syncwarp();
       w_release(k);
@@ -285,8 +299,8 @@ __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
     w_wait(k + 1);
     if (laneA) {
       float g0r[P], g0i[P], g1r[P], g1i[P];
-      block_row_spectrum_smem<NN>(mydy + s0 * DYS, CW, tt * NN, cf, sf, g0r, g0i);
-      block_row_spectrum_smem<NN>(mydy + s1 * DYS, CW, tt * NN, cf, sf, g1r, g1i);
+      block_row_spectrum_smem<BB, P>(mydy + s0 * DYS, CW, tt * BB, cf, sf, g0r, g0i);
+      block_row_spectrum_smem<BB, P>(mydy + s1 * DYS, CW, tt * BB, cf, sf, g1r, g1i);
       accum(k, g0r, g0i);
       accum(k + 1, g1r, g1i);
     }
@@ -301,7 +315,7 @@ __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
     w_wait(k);
     if (laneA) {
       float gr[P], gi[P];
-      block_row_spectrum_smem<NN>(mydy + s0 * DYS, CW, tt * NN, cf, sf, gr, gi);
+      block_row_spectrum_smem<BB, P>(mydy + s0 * DYS, CW, tt * BB, cf, sf, gr, gi);
       accum(k, gr, gi);
     }
     __syncwarp();
@@ -318,7 +332,7 @@ __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
     const int r = e / QT;
     Q[r * QP + ntile_q * QT + (e - r * QT)] = make_float2(0.f, 0.f);
   }
-  const int FW = p.Td * NN + NN - 1;  // full-frame width
+  const int FW = p.Td * BB + NN - 1;  // full-frame width
   const size_t planeN = (size_t)p.N * p.N;
 #pragma unroll
   for (int c = 0; c < CR; ++c) {
@@ -353,10 +367,10 @@ __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
       if (pr >= npairs || j < 0 || j >= p.N) continue;
       const int pb = pr / p.Td, pt1 = pr - (pr / p.Td) * p.Td;
       float* dxc = p.dx + ((size_t)pb * p.C + c) * planeN;
-      const int I0 = pt1 * NN - p.off;  // dx row of block row 0
-      const int tA = J / NN, pA = J - (J / NN) * NN;
+      const int I0 = pt1 * BB - p.off;  // dx row of block row 0
+      const int tA = J / BB, pA = J - (J / BB) * BB;
       const int offA = r * QP + (tA < p.Td ? tA : ntile_q) * QT + pA;
-      const int offB = r * QP + ((pA <= NN - 2 && tA >= 1) ? (tA - 1) * QT + pA + NN : ntile_q * QT);
+      const int offB = r * QP + ((pA <= NN - 2 && tA >= 1) ? (tA - 1) * QT + pA + BB : ntile_q * QT);
       float zr[H], zi[H];
 #pragma unroll
       for (int f = 0; f < H; ++f) {
@@ -383,9 +397,9 @@ __device__ __forceinline__ void bwdd_body(const BwdDParams& p, const int item) {
   }
 }
 
-template <int NN, int CR, bool TM = false>
+template <int NN, int CR, bool TM = false, int BB = NN>
 __global__ void __launch_bounds__(256, TM ? 2 : 1) oaa_bwdd_kernel(const BwdDParams p) {
-  bwdd_body<NN, CR, TM>(p, blockIdx.x);
+  bwdd_body<NN, CR, TM, BB>(p, blockIdx.x);
 }
 
 }  // namespace oaa

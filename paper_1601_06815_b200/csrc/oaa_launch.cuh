@@ -254,13 +254,13 @@ cudaError_t launch_walk_oas_n(const oaa::XSpecParams& xp, const oaa::WalkParams&
   return cudaGetLastError();
 }
 
-template <int NN>
-cudaError_t launch_bwdd_n(const oaa::BwdDParams& p, int cr, size_t smem, cudaStream_t s) {
+template <int NN, int BB>
+cudaError_t launch_bwdd_nb(const oaa::BwdDParams& p, int cr, size_t smem, cudaStream_t s) {
   const bool tm = smem <= 110 * 1024;  // TMEM accumulators whenever 2 CTAs fit an SM
-  auto k = tm ? (cr <= 1 ? oaa::oaa_bwdd_kernel<NN, 1, true> : cr == 2 ? oaa::oaa_bwdd_kernel<NN, 2, true>
-                 : cr == 3 ? oaa::oaa_bwdd_kernel<NN, 3, true> : oaa::oaa_bwdd_kernel<NN, 4, true>)
-              : (cr <= 1 ? oaa::oaa_bwdd_kernel<NN, 1, false> : cr == 2 ? oaa::oaa_bwdd_kernel<NN, 2, false>
-                 : cr == 3 ? oaa::oaa_bwdd_kernel<NN, 3, false> : oaa::oaa_bwdd_kernel<NN, 4, false>);
+  auto k = tm ? (cr <= 1 ? oaa::oaa_bwdd_kernel<NN, 1, true, BB> : cr == 2 ? oaa::oaa_bwdd_kernel<NN, 2, true, BB>
+                 : cr == 3 ? oaa::oaa_bwdd_kernel<NN, 3, true, BB> : oaa::oaa_bwdd_kernel<NN, 4, true, BB>)
+              : (cr <= 1 ? oaa::oaa_bwdd_kernel<NN, 1, false, BB> : cr == 2 ? oaa::oaa_bwdd_kernel<NN, 2, false, BB>
+                 : cr == 3 ? oaa::oaa_bwdd_kernel<NN, 3, false, BB> : oaa::oaa_bwdd_kernel<NN, 4, false, BB>);
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   {
@@ -270,6 +270,12 @@ cudaError_t launch_bwdd_n(const oaa::BwdDParams& p, int cr, size_t smem, cudaStr
   }
   g_launches++;
   return cudaGetLastError();
+}
+template <int NN>
+cudaError_t launch_bwdd_n(const oaa::BwdDParams& p, int cr, size_t smem, cudaStream_t s) {
+  if constexpr (walk_block_big(NN) != NN)
+    if (p.BB != NN) return launch_bwdd_nb<NN, walk_block_big(NN)>(p, cr, smem, s);
+  return launch_bwdd_nb<NN, NN>(p, cr, smem, s);
 }
 
 template <int NN>

@@ -136,17 +136,22 @@ def _big_block_cases():
 @pytest.mark.parametrize("B,C,K,N,n", _big_block_cases())
 def test_walker_block_size_b_ne_n(B, C, K, N, n, crop):
     """SURVEY.md §8(f) NEXT-4 "block sizes b != n": the forward walker tiles the
-    input into b×b blocks, b = 16 − n, transformed on the (b + n − 1)² = 15² grid; the
-    result is the same linear convolution (every element vs the direct oracle), and
-    prepared spectra (their own P) give it bitwise."""
+    input, and bwd_data (C <= 4 output channels) tiles dy, into b×b blocks, b = 16 − n,
+    transformed on the (b + n − 1)² = 15² grid; the results are the same linear convolutions
+    (every element vs the direct oracle), and prepared spectra (their own P) give them
+    bitwise."""
     d = make_inputs(B, C, K, N, n, crop, seed=N * 7 + n * 3 + C)
     x = torch.from_numpy(d["x"]).cuda()
     w = torch.from_numpy(d["w"]).cuda()
+    dy = torch.from_numpy(d["dy"]).cuda()
     y = oaa.conv_fwd(x, w, crop)
     yp = oaa.PreparedWeights(w, N, "fwd", crop).fwd(x)
+    dx = oaa.conv_bwd_data(dy, w, N, crop)
+    dxp = oaa.PreparedWeights(w, N, "bwd_data", crop).bwd_data(dy)
     torch.cuda.synchronize()
-    assert torch.equal(y, yp)
+    assert torch.equal(y, yp) and torch.equal(dx, dxp)
     check(y.cpu().numpy(), oracle.conv_fwd(d["x"], d["w"], crop), f"fwd b=16-n N={N} n={n} C={C} {crop}")
+    check(dx.cpu().numpy(), oracle.conv_bwd_data(d["dy"], d["w"], N, crop), f"bwd_data b=16-n N={N} n={n} C={C} {crop}")
 
 
 @pytest.mark.parametrize("crop", CROPS)
