@@ -533,8 +533,15 @@ BwdfPlan plan_bwdf(int B, int C, int K, int M, int n) {
   // balanced kernel groups: each CTA takes ⌈K / nkg⌉ kernels rounded up to whole warps
   f.nwb = cdiv(cdiv(K, f.nkg), f.KPW);
   f.KG = f.nwb * f.KPW;
-  f.tm = true;  // TMEM accumulators, 2 CTAs / SM (measured faster than registers)
-  int slots = f.tm ? 296 : 148;
+  // TMEM accumulators for n ≥ 6 (C·P complex per lane would not fit 128 registers; measured
+  // faster than registers at 1 CTA / SM); registers for n ≤ 5, where the per-block
+  // TMEM ld + st of 32 columns per channel outweighs the C·P·4 FMAs it serves
+#ifdef OAA_EXP_BWDF_TM_ALL  // experiment builds only: tensor-memory accumulators for every n
+  f.tm = true;
+#else
+  f.tm = n >= 6;
+#endif
+  int slots = 296;
   f.G = std::max(1, std::min(B * f.Td, slots / f.nkg));
   f.SW = cdiv(f.NCH * f.CW + n - 1, 4) * 4;
   f.xs_b = align_up(sizeof(float4) * (size_t)B * f.Td * f.NCH * C * f.CH4);
@@ -1077,7 +1084,7 @@ bool plan_bwd_fused(int B, int C, int K, int N, int n, oaa_crop_t crop, const Ge
     p->bd = plan_bwdd(false, B, C, g.M, n, none, false);
     p->bf = plan_bwdf(B, C, K, g.M, n);
     const size_t bsm = oaa::bwdd_smem_bytes(n, n, C, p->bd.NCW, p->bd.RPC, p->bd.WSL);
-    p->simt = B > 0 && p->bd.use && p->bf.use && p->bf.tm && p->bf.nwb == oaa::kBwdfWarps && bsm <= 110 * 1024 &&
+    p->simt = B > 0 && p->bd.use && p->bf.use && p->bf.nwb == oaa::kBwdfWarps && bsm <= 110 * 1024 &&
               p->bf.smem <= 110 * 1024;
     if (p->simt) {
 #ifndef OAA_EXP_FUSED_SLOTS  // experiment builds only: -DOAA_EXP_FUSED_SLOTS=<weight-gradient CTAs>

@@ -36,10 +36,11 @@ struct BwdFParams {
 };
 
 constexpr int kBwdfWarps = 8;
-// TM = false: dŴ accumulators in registers (1 CTA / SM, deeper rings);
-// TM = true : accumulators in tensor memory, ≤ 128 registers, 2 CTAs / SM.
+// TM = false: dŴ accumulators in registers (small n: C·P complex values per lane);
+// TM = true : accumulators in tensor memory (every block: a 32-column ld + st per channel).
+// Both ≤ 128 registers, 2 CTAs / SM.
 template <bool TM> struct BwdfCfg;
-template <> struct BwdfCfg<false> { static constexpr int ring = 4, dy = 3, minb = 1; };
+template <> struct BwdfCfg<false> { static constexpr int ring = 3, dy = 2, minb = 2; };
 template <> struct BwdfCfg<true> { static constexpr int ring = 3, dy = 2, minb = 2; };
 
 template <bool TM>
