@@ -428,7 +428,12 @@ def test_prepared_weight_spectra_bitwise(B, C, K, N, n, crop):
 @pytest.mark.parametrize("B,C,K,N,n,crop", [(2, 3, 8, 40, 8, "valid"), (3, 2, 5, 23, 5, "full"),
                                             (2, 16, 20, 17, 3, "same"), (3, 24, 16, 20, 8, "valid"),
                                             (2, 33, 17, 23, 2, "full"), (1, 200, 16, 10, 5, "same"),
-                                            (5, 17, 33, 29, 5, "valid")])
+                                            (5, 17, 33, 29, 5, "valid"),
+                                            # tensor-core fused backward: ragged bt tails, 1-2
+                                            # weight-gradient M tiles, split-K, several batch chunks
+                                            (2, 16, 32, 17, 3, "same"), (2, 64, 128, 20, 8, "valid"),
+                                            (1, 48, 64, 25, 5, "full"), (3, 32, 96, 14, 4, "valid"),
+                                            (2, 64, 256, 12, 7, "same"), (9, 16, 32, 40, 6, "valid")])
 def test_fused_backward(B, C, K, N, n, crop):
     """NEXT-1: oaa_conv_bwd gives dx bitwise equal to oaa_conv_bwd_data and
     dw within the bar of the oracle (on the tensor-core path it shares the dy spectra

@@ -16,7 +16,8 @@ dy = torch.rand((B, K, M, M), generator=g, device="cuda") * 2 - 1
 y = torch.empty((B, K, M, M), device="cuda"); dx = torch.empty_like(x); dw = torch.empty_like(w)
 ops = {"fwd": lambda: oaa.conv_fwd(x, w, crop, out=y),
        "bwd_data": lambda: oaa.conv_bwd_data(dy, w, N, crop, out=dx),
-       "bwd_filter": lambda: oaa.conv_bwd_filter(x, dy, n, crop, out=dw)}
+       "bwd_filter": lambda: oaa.conv_bwd_filter(x, dy, n, crop, out=dw),
+       "bwd_fused": lambda: oaa.conv_bwd(x, dy, w, crop)}
 res = {}
 for name, f in ops.items():
     for _ in range(3): f()
