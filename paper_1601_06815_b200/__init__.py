@@ -26,7 +26,7 @@ __all__ = [
     "conv_fwd", "conv_bwd_data", "conv_bwd_filter", "out_size", "workspace_bytes", "lib",
     "OaAConv2dFunction", "OaAConv2d", "launch_count", "profile_enable", "profile_collect",
     "profile_collect_kernels",
-    "CROPS", "OP_FWD", "OP_BWD_DATA", "OP_BWD_FILTER", "OP_FWD_OAS", "OP_BWD", "OaAError", "conv_fwd_oas", "PreparedWeights", "conv_bwd",
+    "CROPS", "block_size", "OP_FWD", "OP_BWD_DATA", "OP_BWD_FILTER", "OP_FWD_OAS", "OP_BWD", "OaAError", "conv_fwd_oas", "PreparedWeights", "conv_bwd",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -78,6 +78,8 @@ def lib():
             L.oaa_debug_bin_gemm.restype = I
             L.oaa_status_string.argtypes = [I]
             L.oaa_status_string.restype = ctypes.c_char_p
+            L.oaa_block_size.argtypes = [I, I, I, I, I, I]
+            L.oaa_block_size.restype = I
             L.oaa_version.argtypes = []
             L.oaa_version.restype = ctypes.c_char_p
             L.oaa_launch_count.argtypes = []
@@ -98,6 +100,13 @@ def lib():
 
 def version() -> str:
     return lib().oaa_version().decode()
+
+
+def block_size(op: str, C: int, K: int, N: int, n: int, crop: str = "valid") -> int:
+    """Block size b the fwd / bwd_data call tiles into (host planning only; R18)."""
+    if op not in ("fwd", "bwd_data"):
+        raise ValueError("op must be 'fwd' or 'bwd_data'")
+    return lib().oaa_block_size(OP_FWD if op == "fwd" else OP_BWD_DATA, int(C), int(K), int(N), int(n), _crop_id(crop))
 
 
 def _crop_id(crop) -> int:

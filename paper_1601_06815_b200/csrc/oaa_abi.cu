@@ -1618,6 +1618,20 @@ int oaa_profile_collect_kernels(double* ms, int* count, int n) {
 
 const char* oaa_version(void) { return "oaa-b200 0.1.0 sm_100a"; }
 
+int oaa_block_size(oaa_op_t op, int C, int K, int N, int n, oaa_crop_t crop) {
+  Geo g;
+  if (op != OAA_OP_FWD && op != OAA_OP_BWD_DATA) return -1;
+  if (validate(1, C, K, N, n, crop, &g) != OAA_OK) return -1;
+  const bool fwd = op == OAA_OP_FWD;
+  const int R = fwd ? N : g.M, Ro = fwd ? g.M : N, off = fwd ? g.o : (n - 1 - g.o);
+  const int Cin = fwd ? C : K, Cout = fwd ? K : C;
+  const TcPlan tc = plan_tc(1, Cin, Cout, R, n);
+  const WalkHostGeo wk = plan_walk(fwd, 1, Cin, Cout, R, Ro, off, n, tc);
+  if (wk.use) return wk.BB;
+  const BwddPlan bd = plan_bwdd(fwd, 1, Cout, R, n, tc);
+  return bd.use ? bd.BB : n;
+}
+
 uint64_t oaa_launch_count(void) { return g_launches.load(); }
 
 void oaa_profile_enable(int on) {

@@ -141,3 +141,30 @@ def test_new_op_workspace_sizes():
     P = ctypes.c_void_p
     assert L.oaa_weight_spectra(oaa.OP_FWD, P(0x1000), P(0x7000000000), 16, 3, 64, 224, 8, 1, None) == 3
     assert L.oaa_weight_spectra(oaa.OP_BWD_FILTER, P(0x1000), P(0x7000000000), 1 << 20, 3, 64, 224, 8, 1, None) == 1
+
+
+def test_block_size_planning():
+    """DESIGN.md R18 (SURVEY.md §8(f) NEXT-4 "block size b != n"): the forward walker and bwd_data
+    (C <= 4 output channels) tile into b = 16 - n blocks (P = 15) for 3 <= n <= 7 once the image
+    holds >= 3 of them (bwd_data: n <= 4, or >= 96 pixels per side); everything else keeps the
+    paper's b = n.  Host planning only -- no GPU needed."""
+    bs = oaa.block_size
+    # the BASELINE sweep at N = 224 and 128 (C = 3, K = 64): larger blocks in both ops
+    for N in (224, 128):
+        for n in (3, 5, 7):
+            assert bs("fwd", 3, 64, N, n) == 16 - n
+            assert bs("bwd_data", 3, 64, N, n) == 16 - n
+        assert bs("fwd", 3, 64, N, 8) == 8 and bs("bwd_data", 3, 64, N, 8) == 8
+    # thresholds: fwd from N >= 3b; bwd_data (dy side M) from 3b for n <= 4, from 96 for n >= 5
+    assert bs("fwd", 1, 1, 39, 3) == 13 and bs("fwd", 1, 1, 38, 3) == 3
+    assert bs("fwd", 1, 1, 27, 7, "same") == 9 and bs("fwd", 1, 1, 26, 7, "same") == 7
+    assert bs("bwd_data", 3, 8, 64, 5) == 5          # M = 60 < 96
+    assert bs("bwd_data", 3, 8, 64, 3) == 13         # M = 62 >= 39
+    # n = 1, 2 and the tensor-core path (C, K >= 16) keep b = n; so does any op with C > 4 inputs
+    assert bs("fwd", 3, 8, 224, 2) == 2 and bs("fwd", 3, 8, 224, 1) == 1
+    assert bs("fwd", 64, 128, 224, 5) == 5 and bs("bwd_data", 64, 128, 224, 5) == 5
+    assert bs("fwd", 6, 7, 224, 3) == 3
+    assert oaa.lib().oaa_block_size(2, 3, 64, 224, 3, 1) == -1  # bwd_filter: not a block-size op
+    assert oaa.lib().oaa_block_size(0, 3, 64, 2, 3, 1) == -1    # Valid with n > N
+    with pytest.raises(ValueError):
+        bs("bwd_filter", 3, 64, 224, 3)

@@ -140,6 +140,7 @@ def test_walker_block_size_b_ne_n(B, C, K, N, n, crop):
     transformed on the (b + n − 1)² = 15² grid; the results are the same linear convolutions
     (every element vs the direct oracle), and prepared spectra (their own P) give them
     bitwise."""
+    assert oaa.block_size("fwd", C, K, N, n, crop) == 16 - n  # the larger blocks run
     d = make_inputs(B, C, K, N, n, crop, seed=N * 7 + n * 3 + C)
     x = torch.from_numpy(d["x"]).cuda()
     w = torch.from_numpy(d["w"]).cuda()
