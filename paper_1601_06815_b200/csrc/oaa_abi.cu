@@ -418,9 +418,12 @@ WalkHostGeo plan_walk(bool is_fwd, int B, int Cin, int Cout, int R, int Ro, int 
   w.use = is_fwd && !tc.use && Cin <= kWalkMaxCin;
   // block size: for 3 ≤ n ≤ 7 the blocks grow to
   // b = 16 − n, so every block uses the P = 15 grid of n = 8 (PFA 3×5 codelets, 8 spectrum rows,
-  // 4 blocks per warp) and yields b² instead of n² outputs -- once the image holds ≥ 3 of them
+  // 4 blocks per warp) and yields b² instead of n² outputs -- once the image holds ≥ 3 of them,
+  // or 2 with at most 1.5× the image area in padded blocks (measured at N = 32, B = 128, C = 3,
+  // K = 64: n = 3 / 5 walk 0.080 → 0.055 ms; at N = 20, n = 7, 1.8× area, 0.043 → 0.052)
   const int big = walk_block_big(n);
-  w.BB = (big != n && R >= 3 * big) ? big : n;
+  const long long pad = (long long)cdiv(R, big) * big;
+  w.BB = (big != n && (R >= 3 * big || (R >= 2 * big && 2 * pad * pad <= 3LL * R * R))) ? big : n;
   w.P = w.BB + n - 1;
   w.H = (w.P + 1) / 2;
   w.T = cdiv(R, w.BB);

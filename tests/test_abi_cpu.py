@@ -155,9 +155,12 @@ def test_block_size_planning():
             assert bs("fwd", 3, 64, N, n) == 16 - n
             assert bs("bwd_data", 3, 64, N, n) == 16 - n
         assert bs("fwd", 3, 64, N, 8) == 8 and bs("bwd_data", 3, 64, N, 8) == 8
-    # thresholds: fwd from N >= 3b; bwd_data (dy side M) from 3b for n <= 4, from 96 for n >= 5
-    assert bs("fwd", 1, 1, 39, 3) == 13 and bs("fwd", 1, 1, 38, 3) == 3
-    assert bs("fwd", 1, 1, 27, 7, "same") == 9 and bs("fwd", 1, 1, 26, 7, "same") == 7
+    # thresholds: fwd from N >= 3b, or from 2b with <= 1.5x the area in padded blocks; bwd_data
+    # (dy side M) from 3b for n <= 4, from 96 for n >= 5
+    assert bs("fwd", 1, 1, 39, 3) == 13 and bs("fwd", 1, 1, 38, 3) == 13 and bs("fwd", 1, 1, 32, 3) == 13
+    assert bs("fwd", 1, 1, 27, 3) == 3 and bs("fwd", 1, 1, 25, 3) == 3     # 39²/27² > 1.5; < 2b
+    assert bs("fwd", 1, 1, 27, 7, "same") == 9 and bs("fwd", 1, 1, 20, 7, "same") == 7
+    assert bs("fwd", 3, 64, 32, 5) == 11 and bs("fwd", 3, 64, 16, 5) == 5
     assert bs("bwd_data", 3, 8, 64, 5) == 5          # M = 60 < 96
     assert bs("bwd_data", 3, 8, 64, 3) == 13         # M = 62 >= 39
     # n = 1, 2 and the tensor-core path (C, K >= 16) keep b = n; so does any op with C > 4 inputs

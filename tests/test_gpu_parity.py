@@ -121,13 +121,14 @@ def test_largest_images(n, crop):
 
 
 def _big_block_cases():
-    # forward walker with blocks b = 16 − n (P = 15) for 3 <= n <= 7 once N >= 3b: N at the
-    # threshold, one past it, ragged (the last block mostly padding) and several chunks per
-    # tile row (stage B in two 32-column rounds when 4b > 32); C = 1..4 register channels
+    # forward walker with blocks b = 16 − n (P = 15) for 3 <= n <= 7 once N >= 3b (or 2b with
+    # little padding): N = 2b, the 3b threshold, one past it, ragged (the last block mostly
+    # padding) and several chunks per tile row (stage B in two 32-column rounds when 4b > 32);
+    # C = 1..4 register channels
     out = []
     for n in range(3, 8):
         b = 16 - n
-        for i, N in enumerate(sorted({3 * b, 3 * b + 1, 4 * b - 1, 7 * b + 2, 100})):
+        for i, N in enumerate(sorted({2 * b, 3 * b, 3 * b + 1, 4 * b - 1, 7 * b + 2, 100})):
             out.append((1 + i % 2, 1 + (n + i) % 4, 3 + 2 * i, N, n))
     return out
 
