@@ -1,6 +1,8 @@
 // oaa_bwdd.cuh -- bwd_data for layers with few input channels (C ≤ 4): the first of the
 // two backward convolutions of PAPER.md:89, dx = crop(Σ_k FullConv(dy_k, flip180 w_kc)),
-// evaluated by OaA over the n×n blocks of dy.
+// evaluated by OaA over the n×n blocks of dy -- or, for 3 ≤ n ≤ 7 and
+// large images, over b×b blocks with b = 16 − n on the P = 15 grid (R18); with b ≥ n − 1
+// the vertical overlap still gives each dx element at most two addends (below).
 //
 // One CTA per (image b, dy tile row t1).  Compute warp i owns chunk i of the tile row:
 // lanes (tt, f1) hold block t2 = i·TPW + tt, spectrum row f1.  For every dy channel k in

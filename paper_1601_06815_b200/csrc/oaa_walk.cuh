@@ -16,10 +16,11 @@
 //            the K·C frequency-domain products summed over c; Ŵ lives in registers),
 //            inverse DFT along f2 → Q[f1][p2] in the warp's shared Q ring;
 //   stage B  lane = output column J of the chunk: the two block columns that land on J
-//            (tile J/n at p2 = J mod n, tile J/n − 1 at p2 + n) are summed BEFORE the last
-//            transform (linearity -- the horizontal overlap-add), Hermitian
-//            c2r along f1 gives the column's 2n−1 rows; rows [0, n−1) add the carry, rows
-//            [0, n) are final and stored, rows [n, 2n−1) become the carry.
+//            (tile J/b at p2 = J mod b, tile J/b − 1 at p2 + b; blocks of b = n, or of
+//            b = 16 − n, WalkGeo) are summed BEFORE the last transform (linearity -- the
+//            horizontal overlap-add), Hermitian c2r along f1 gives the column's
+//            P = b + n − 1 rows; rows [0, n−1) add the carry, rows [0, b) are final and
+//            stored, rows [b, b + n − 1) become the carry.
 // The forward spectra X̂ of the input blocks (one per (image, channel, block), computed
 // once by oaa_xspec_kernel) stream through a ring of shared-memory chunk slots filled by
 // bulk copies (TMA engine); the last warp to release a slot issues the copy that refills
