@@ -171,8 +171,9 @@ oaa_status_t oaa_debug_bin_gemm(const float* A, const float* B, float* D, int F,
 /* Block size b the call (op = FWD or BWD_DATA) with these arguments tiles its input into
  * (host-side planning only, no GPU work): n for the paper's OaA (blocks of the
  * kernel's size), 16 − n when the forward walker / bwd_data kernels (C ≤ 4 input / output
- * channels) use larger blocks on the P = b + n − 1 = 15 grid (R18, SURVEY.md §8(f)
- * NEXT-4).  Returns −1 for invalid arguments or another op. */
+ * channels) or the tensor-core path (C, K ≥ 16) use larger blocks on the P = b + n − 1 = 15
+ * grid (R18).  Returns −1 for invalid arguments or another
+ * op. */
 int oaa_block_size(oaa_op_t op, int C, int K, int N, int n, oaa_crop_t crop);
 
 /* Static description of a status code. */

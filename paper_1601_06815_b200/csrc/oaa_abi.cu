@@ -375,17 +375,33 @@ constexpr size_t kTcChunkBytes = size_t(1) << 33;  // Xg + D per chunk (8 GB: la
 
 struct TcPlan {
   bool use;
+  int BB, P, H;  // block size b (n, or 16 − n: DESIGN.md R18), transform size, spectrum rows
   int F, T, Kc, RTA, RTB, NB, bc, nchunks;  // K chunks of 32, row tiles of A and B, B tiles per CTA
   bool b_split;  // B (block spectra) stored pre-split: each B tile is re-read by RTA ≥ 3 M tiles
   size_t ag_b, xg_b, d_b;
 };
-TcPlan plan_tc(int B, int Cin, int Cout, int R, int n) {
+// allow_big = false: blocks of the kernel's size (the fused backward, whose weight-gradient
+// producers share the dy tiling, and overlap-and-save keep b = n)
+TcPlan plan_tc(int B, int Cin, int Cout, int R, int n, bool allow_big = true) {
   TcPlan t{};
   t.use = Cin >= kTcMinChannels && Cout >= kTcMinChannels;
   if (!t.use || B < 1) return t;
-  const int P = 2 * n - 1;
-  t.F = n * P;
-  t.T = cdiv(R, n);
+  // larger blocks as the walker's (plan_walk), P = 15, for n = 6, 7 only, whose own grids P = 11,
+  // 13 are primes (costly pairing codelets in the tile producer and the load walker): measured
+  // B = 128 C = 32 K = 64 N = 64 n = 7 fwd 1.009 → 0.523 ms, bwd_data 0.770 → 0.592.  For n ≤ 5
+  // the tensor cores make the contraction cheap and the P = 15 producer / walker cost more than
+  // the bins they save (N = 56 n = 3 fwd 0.500 → 0.541; configs[3] n = 5 fwd 0.888 → 1.317).
+  const int big = walk_block_big(n);
+  const long long pad = (long long)cdiv(R, big) * big;
+#ifdef OAA_EXP_TC_SMALLB  // experiment builds only: the tensor-core path keeps b = n
+  t.BB = n;
+#else
+  t.BB = (allow_big && n >= 6 && big != n && (R >= 3 * big || (R >= 2 * big && 2 * pad * pad <= 3LL * R * R))) ? big : n;
+#endif
+  t.P = t.BB + n - 1;
+  t.H = (t.P + 1) / 2;
+  t.F = t.H * t.P;
+  t.T = cdiv(R, t.BB);
   t.Kc = cdiv(2 * ((Cin + 3) & ~3), oaa::kTcK);
   t.RTA = cdiv(2 * Cout, oaa::kTcM);
   // measured (AlexNet-like fwd, 4 M tiles): splitting B once in HBM beats re-splitting every
@@ -401,7 +417,7 @@ TcPlan plan_tc(int B, int Cin, int Cout, int R, int n) {
   t.ag_b = sizeof(float) * (size_t)t.F * t.Kc * 2 * t.RTA * 4096;  // pre-split (hi | lo)
   t.xg_b = sizeof(float) * (size_t)t.F * t.Kc * (t.b_split ? 2 : 1) * t.RTB * 4096;
   // Ŷ in the walker layout (oaa_tc.cuh mode 2): tile rows padded to whole walker chunks
-  const int TPW = 32 / n;
+  const int TPW = 32 / t.H;
   t.d_b = sizeof(float) * (size_t)t.F * 2 * Cout * ((size_t)t.bc * t.T * (cdiv(t.T, TPW) * TPW) + 31) / 32 * 32;
   return t;
 }
@@ -689,20 +705,22 @@ struct TcData {
 oaa_status_t tc_data_setup(TcData& d, bool is_fwd, const float* in, const float* w, float* out, int K, int C, int n,
                            const Geo& g, const EnginePlan& e, const TcPlan& tc, float* Ag, float* Xg, float* D,
                            cudaStream_t s, const void* prepared) {
-  const int Cin = e.Cin, Cout = e.Cout, T = e.T;
+  const int Cin = e.Cin, Cout = e.Cout, T = tc.T;  // (tc.T = e.T for blocks of the kernel's size)
   if (!prepared) {
     if (cudaMemsetAsync(Ag, 0, tc.ag_b, s) != cudaSuccess) return OAA_ERR_CUDA;
     const long long total = (long long)tc.F * Cin * Cout;
     const int thr = 256;
     const int blocks = (int)std::min<long long>((total + thr - 1) / thr, 8192);
     KTimer kt(KID_SPECTRUM, s);
-    oaa::oaa_realified_spectrum_kernel<<<blocks, thr, 0, s>>>(w, Ag, K, C, n, is_fwd ? 0 : 1, tc.Kc, tc.RTA);
+    oaa::oaa_realified_spectrum_kernel<<<blocks, thr, 0, s>>>(w, Ag, K, C, n, tc.P, is_fwd ? 0 : 1, tc.Kc, tc.RTA);
     g_launches++;
     if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
   }
   d.n = n;
   d.T = T;
   d.F = tc.F;
+  const int BB = tc.BB, H = tc.H;
+  const int BW = BB == n ? e.BW : cdiv(T * BB, 4) * 4;  // staged row width of the tile producer
   oaa::TileSpecParams& tp = d.tp;
   tp = oaa::TileSpecParams{};
   tp.in = in;
@@ -712,8 +730,9 @@ oaa_status_t tc_data_setup(TcData& d, bool is_fwd, const float* in, const float*
   tp.T = T;
   tp.Kc = tc.Kc;
   tp.RTB = tc.RTB;
-  tp.BW = e.BW;
-  tp.CSTR = n * e.BW + 4;
+  tp.BW = BW;
+  tp.CSTR = BB * BW + 4;
+  tp.BB = BB;
   tp.split = tc.b_split ? 1 : 0;
   tp.Ga = nullptr;
   d.t1_smem = sizeof(float) * 16 * (size_t)tp.CSTR;
@@ -734,17 +753,17 @@ oaa_status_t tc_data_setup(TcData& d, bool is_fwd, const float* in, const float*
   gp.b_split = tc.b_split ? 1 : 0;
   gp.partial = nullptr;
   gp.Cf = Cout;
-  gp.H = n;
-  gp.P = g.P;
+  gp.H = H;
+  gp.P = tc.P;
   gp.TT = T;
-  gp.TPW = 32 / n;
+  gp.TPW = 32 / H;
   gp.NT4 = cdiv(T, gp.TPW);
   gp.SBL = oaa::kYSBL;  // (the walker's load mode reads Ŷ with this block size fixed at compile time)
   gp.SB = 1 << gp.SBL;
   gp.NB = tc.NB;
   gp.Kuse = tc.Kc;
   // walker in LOAD mode: inverse DFT + overlap-add of Ŷ straight from the GEMM output
-  const int TPW = 32 / n, CW = TPW * n;
+  const int TPW = 32 / H, CW = TPW * BB;
   oaa::WalkParams& wp = d.wp;
   wp = oaa::WalkParams{};
   wp.out = out;
@@ -754,10 +773,11 @@ oaa_status_t tc_data_setup(TcData& d, bool is_fwd, const float* in, const float*
   wp.Ro = e.Ro;
   wp.off = e.off;
   wp.NCH = cdiv(e.off + e.Ro, CW);
-  wp.KG = std::min(n <= 6 ? 4 : 8, Cout);  // warps per load-walker CTA (oaa_walk.cuh launch bounds)
+  wp.KG = std::min(tc.P <= 11 ? 4 : 8, Cout);  // warps per load-walker CTA (oaa_walk.cuh launch bounds)
   wp.ngrp = cdiv(Cout, wp.KG);
   wp.D = D;
-  const int QSZ = ((2 * TPW + 1) * n * g.P + 1) & ~1;
+  wp.BB = BB;
+  const int QSZ = ((2 * TPW + 1) * H * tc.P + 1) & ~1;
   d.walk_smem = sizeof(float2) * (size_t)wp.KG * QSZ + sizeof(float) * (size_t)wp.KG * oaa::walk_trp(n) * wp.NCH * CW;
   return OAA_OK;
 }
@@ -1070,7 +1090,7 @@ struct BwdFusedPlan {
 };
 bool plan_bwd_fused(int B, int C, int K, int N, int n, oaa_crop_t crop, const Geo& g, BwdFusedPlan* p) {
   *p = BwdFusedPlan{};
-  p->td = plan_tc(B, K, C, g.M, n);
+  p->td = plan_tc(B, K, C, g.M, n, false);
   TcFiltPlan tf0 = plan_tc_filter(B, C, K, N, g.M, n);
   p->tc = p->td.use && tf0.use && B > 0;
   if (p->tc) {
@@ -1116,7 +1136,7 @@ struct OasTc {
 };
 OasTc plan_oas_tc(int B, int C, int K, int N, int n, const Geo& g) {
   OasTc o{};
-  o.tc = plan_tc(B, C, K, g.M, n);  // tiles: ⌈M/n⌉² output tiles
+  o.tc = plan_tc(B, C, K, g.M, n, false);  // tiles: ⌈M/n⌉² output tiles
   o.use = o.tc.use && B > 0;
   if (!o.use) return o;
   o.e = EnginePlan{};
@@ -1513,7 +1533,7 @@ oaa_status_t oaa_weight_spectra(oaa_op_t op, const float* w, void* spec, size_t 
     if (cudaMemsetAsync(spec, 0, tc.ag_b, s) != cudaSuccess) return OAA_ERR_CUDA;
     const long long total = (long long)tc.F * Cin * Cout;
     const int blocks = (int)std::min<long long>((total + 255) / 256, 8192);
-    oaa::oaa_realified_spectrum_kernel<<<blocks, 256, 0, s>>>(w, static_cast<float*>(spec), K, C, n, is_fwd ? 0 : 1,
+    oaa::oaa_realified_spectrum_kernel<<<blocks, 256, 0, s>>>(w, static_cast<float*>(spec), K, C, n, tc.P, is_fwd ? 0 : 1,
                                                               tc.Kc, tc.RTA);
   } else {
     EnginePlan e;
@@ -1629,6 +1649,7 @@ int oaa_block_size(oaa_op_t op, int C, int K, int N, int n, oaa_crop_t crop) {
   const int R = fwd ? N : g.M, Ro = fwd ? g.M : N, off = fwd ? g.o : (n - 1 - g.o);
   const int Cin = fwd ? C : K, Cout = fwd ? K : C;
   const TcPlan tc = plan_tc(1, Cin, Cout, R, n);
+  if (tc.use) return tc.BB;
   const WalkHostGeo wk = plan_walk(fwd, 1, Cin, Cout, R, Ro, off, n, tc);
   if (wk.use) return wk.BB;
   const BwddPlan bd = plan_bwdd(fwd, 1, Cout, R, n, tc);

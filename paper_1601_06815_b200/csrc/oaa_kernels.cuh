@@ -1486,6 +1486,7 @@ struct TileSpecParams {
   // spectrum is that of the (2n−1)² x-window at (t1·n + org, t2·n + org), org = o − (n−1), zero
   // outside x
   int win, org;
+  int BB;  // block size (launcher: b = n, or 16 − n, R18)
 };
 
 // One CTA per (image, tile row) of the chunk.  A task is (f1, tile t2, quad of 4
@@ -1493,9 +1494,12 @@ struct TileSpecParams {
 // lanes of consecutive tiles of a warp fill whole 128-byte lines of the blocked layout.
 // WIN (overlap-and-save): the tiles are output tiles and the spectra those of their
 // (2n−1)² x-windows (full 2n−1 rows staged, 4 channels per CTA for the larger band).
-template <int NN, bool WIN = false>
+// BB: block size (b = n, or b = 16 − n on the P = 15 grid for 3 ≤ n ≤ 7, R18; windows
+// keep b = n)
+template <int NN, bool WIN = false, int BB = NN>
 __global__ void __launch_bounds__(128) oaa_tile_spectra_kernel(const TileSpecParams p) {
-  constexpr int P = 2 * NN - 1, CG = WIN ? 4 : 16, QGL = WIN ? 0 : 2, ROWS = WIN ? P : NN;
+  static_assert(!WIN || BB == NN, "windows are for blocks of the kernel's size");
+  constexpr int P = BB + NN - 1, H = (P + 1) / 2, CG = WIN ? 4 : 16, QGL = WIN ? 0 : 2, ROWS = WIN ? P : BB;
   extern __shared__ __align__(16) float band[];  // [CG][ROWS][BW] (channel stride CSTR)
   __shared__ float2 tw[16];
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -1520,7 +1524,7 @@ __global__ void __launch_bounds__(128) oaa_tile_spectra_kernel(const TileSpecPar
     const int org = WIN ? p.org : 0;
     for (int sgm = warp; sgm < ncg * ROWS; sgm += nwarps) {
       const int ch = sgm / ROWS, rr = sgm - (sgm / ROWS) * ROWS;
-      const int r = t1 * NN + org + rr;
+      const int r = t1 * BB + org + rr;
       const bool rok = r >= 0 && r < p.R;
       const int roff = ((c0 + ch) * p.R + (rok ? r : 0)) * p.R;  // within the image (32-bit)
       float* d = band + ch * p.CSTR + rr * p.BW;
@@ -1534,7 +1538,7 @@ __global__ void __launch_bounds__(128) oaa_tile_spectra_kernel(const TileSpecPar
     cp_async_wait_all();
     __syncthreads();
     // task u: 8 consecutive tiles (u & 7) × the CTA's channel quads × (f1, tile octet)
-    const int ntask = (NN * TH8 * 8) << QGL;
+    const int ntask = (H * TH8 * 8) << QGL;
     for (int u = tid; u < ntask; u += nthr) {
       const int rest = u >> (3 + QGL);
       const int t2 = (rest % TH8) * 8 + (u & 7), cq = (u >> 3) & ((1 << QGL) - 1), f1 = rest / TH8;
@@ -1568,7 +1572,7 @@ __global__ void __launch_bounds__(128) oaa_tile_spectra_kernel(const TileSpecPar
             }
             dft<P, -1>(rr, ri, xr[i], xi[i]);
           } else {
-            block_row_spectrum_smem<NN>(band + (cb + i - c0) * p.CSTR, p.BW, t2 * NN, cf, sf, xr[i], xi[i]);
+            block_row_spectrum_smem<BB, P>(band + (cb + i - c0) * p.CSTR, p.BW, t2 * BB, cf, sf, xr[i], xi[i]);
           }
         } else {
 #pragma unroll
@@ -1617,7 +1621,7 @@ __global__ void __launch_bounds__(128) oaa_tile_spectra_kernel(const TileSpecPar
   if (blockIdx.y != gridDim.y - 1) return;
   const int padq = (32 * p.Kc - 2 * Cinp) >> 2;
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int e = tid; e < NN * P * p.T * padq; e += nthr) {
+  for (int e = tid; e < H * P * p.T * padq; e += nthr) {
     const int qq = e % padq, rest = e / padq;
     const int t2 = rest % p.T, f = rest / p.T;
     if (!p.split) {

@@ -15,6 +15,8 @@
 #include "oaa_bwdf.cuh"
 
 namespace oaa_host {
+// the walker's larger block for 3 ≤ n ≤ 7: b = 16 − n, i.e. P = b + n − 1 = 15 (the n = 8 grid)
+constexpr int walk_block_big(int n) { return (n >= 3 && n <= 7) ? 16 - n : n; }
 
 extern std::atomic<uint64_t> g_launches;
 
@@ -151,6 +153,8 @@ template <int NN>
 cudaError_t launch_tile_spectra_n(const oaa::TileSpecParams& p, size_t smem, cudaStream_t s) {
   const bool win = p.win != 0;
   auto k = win ? oaa::oaa_tile_spectra_kernel<NN, true> : oaa::oaa_tile_spectra_kernel<NN, false>;
+  if constexpr (walk_block_big(NN) != NN)
+    if (!win && p.BB == walk_block_big(NN)) k = oaa::oaa_tile_spectra_kernel<NN, false, walk_block_big(NN)>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   {
@@ -191,8 +195,6 @@ struct WalkPlan {
   int BB;  // block size b: n, or walk_block_big(n) (oaa_walk.cuh WalkGeo)
   size_t xspec_smem, walk_smem;
 };
-// the walker's larger block for 3 ≤ n ≤ 7: b = 16 − n, i.e. P = b + n − 1 = 15 (the n = 8 grid)
-constexpr int walk_block_big(int n) { return (n >= 3 && n <= 7) ? 16 - n : n; }
 
 template <int NN, int BB>
 cudaError_t launch_walk_nb(const oaa::XSpecParams& xp, const oaa::WalkParams& wp, const WalkPlan& w, int cr,
@@ -337,6 +339,8 @@ template <int NN>
 cudaError_t launch_walk_load_n(const oaa::WalkParams& wp, size_t smem, int nimg, cudaStream_t s) {
   // (oas: overlap-and-save stage B -- the blocks' last n rows / columns, no overlap-add)
   auto k = wp.oas ? oaa::oaa_walk_kernel<NN, 1, true, true> : oaa::oaa_walk_kernel<NN, 1, true>;
+  if constexpr (walk_block_big(NN) != NN)
+    if (!wp.oas && wp.BB == walk_block_big(NN)) k = oaa::oaa_walk_kernel<NN, 1, true, false, walk_block_big(NN)>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   {

@@ -463,9 +463,10 @@ namespace oaa {
 // W_{o,i}[f] = DFT_P(w_{o,i})[f1][f2] / P² (fwd: o = k, i = c) or of flip180(w_{k,c})
 // with o = c, i = k (bwd_data).  All other columns are zeroed by the caller.  One thread
 // per (f, o, i), twiddles from a per-block fp64 table.
+// P: transform size (2n − 1, or b + n − 1 for blocks b ≠ n, R18); H = (P + 1) / 2 rows
 __global__ void oaa_realified_spectrum_kernel(const float* __restrict__ w, float* __restrict__ Ag, int K, int C,
-                                              int n, int flip_bwd, int Kc, int RTA) {
-  const int P = 2 * n - 1, H = n, F = H * P;
+                                              int n, int P, int flip_bwd, int Kc, int RTA) {
+  const int H = (P + 1) / 2, F = H * P;
   const int Co = flip_bwd ? C : K, Ci = flip_bwd ? K : C, Cip = (Ci + 3) & ~3;
   __shared__ double tc[16], ts[16];
   if (threadIdx.x < P) sincospi(2.0 * (double)threadIdx.x / (double)P, &ts[threadIdx.x], &tc[threadIdx.x]);

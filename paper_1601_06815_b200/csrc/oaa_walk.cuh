@@ -239,6 +239,7 @@ struct WalkParams {
   int BTc, b0;
   int SBL;  // log2 of the slots per Ŷ block (oaa_tc.cuh mode 2); must equal kYSBL
   int oas;  // LOAD: the launcher picks the overlap-and-save instantiation
+  int BB;   // LOAD: block size (the launcher picks the instantiation; 0 = n)
 };
 
 constexpr int kWalkRing = 4;  // spectrum chunk slots per CTA
@@ -262,8 +263,8 @@ __host__ __device__ constexpr int walk_trp(int n) { return ((n - 1) + 3) & ~3; }
 // AlexNet-like fwd 0.323 → 0.304 ms, bwd_data 0.117 → 0.107 ms.  For n ≥ 7 the cap cost
 // more than the occupancy gained: sharded-config fwd 4.53 → 5.29 ms per chunk.)
 template <int NN, int CR, bool LOAD = false, bool OAS = false, int BB = NN>
-__global__ void __launch_bounds__(256, (LOAD && NN <= 6) ? 2 : 1) oaa_walk_kernel(const WalkParams p) {
-  static_assert(BB == NN || (!LOAD && !OAS), "blocks b != n: forward walker only");
+__global__ void __launch_bounds__(256, (LOAD && BB + NN - 1 <= 11) ? 2 : 1) oaa_walk_kernel(const WalkParams p) {
+  static_assert(BB == NN || !OAS, "blocks b != n: overlap-and-add only");
   using G = WalkGeo<NN, BB>;
   constexpr int P = G::P, H = G::H, P2 = G::P2, TPW = G::TPW, CW = G::CW, RS4 = G::RS4, QT = G::QT;
   constexpr int TR = NN - 1;

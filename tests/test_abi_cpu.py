@@ -166,6 +166,8 @@ def test_block_size_planning():
     # n = 1, 2 and the tensor-core path (C, K >= 16) keep b = n; so does any op with C > 4 inputs
     assert bs("fwd", 3, 8, 224, 2) == 2 and bs("fwd", 3, 8, 224, 1) == 1
     assert bs("fwd", 64, 128, 224, 5) == 5 and bs("bwd_data", 64, 128, 224, 5) == 5
+    assert bs("fwd", 96, 256, 27, 5) == 5                       # configs[3]: b = n
+    assert bs("fwd", 32, 64, 64, 7) == 9 and bs("bwd_data", 32, 64, 64, 7) == 9  # TC path, prime P = 13
     assert bs("fwd", 6, 7, 224, 3) == 3
     assert oaa.lib().oaa_block_size(2, 3, 64, 224, 3, 1) == -1  # bwd_filter: not a block-size op
     assert oaa.lib().oaa_block_size(0, 3, 64, 2, 3, 1) == -1    # Valid with n > N
