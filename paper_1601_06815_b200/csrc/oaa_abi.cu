@@ -395,6 +395,8 @@ TcPlan plan_tc(int B, int Cin, int Cout, int R, int n, bool allow_big = true) {
   const long long pad = (long long)cdiv(R, big) * big;
 #ifdef OAA_EXP_TC_SMALLB  // experiment builds only: the tensor-core path keeps b = n
   t.BB = n;
+#elif defined(OAA_EXP_TC_BIG_ALL)  // experiment builds only: larger blocks for every 3 ≤ n ≤ 7
+  t.BB = (allow_big && big != n && (R >= 3 * big || (R >= 2 * big && 2 * pad * pad <= 3LL * R * R))) ? big : n;
 #else
   t.BB = (allow_big && n >= 6 && big != n && (R >= 3 * big || (R >= 2 * big && 2 * pad * pad <= 3LL * R * R))) ? big : n;
 #endif
