@@ -624,6 +624,7 @@ cudaError_t launch_tile_spectra(int n, const oaa::TileSpecParams& p, size_t smem
 // split-K bin GEMM writing per-split partial dŴ → the fp64 finalize of the FFMA path.
 struct TcFiltPlan {
   bool use;
+  int BB, P, H;  // dy block size (n, or 16 − n for n = 6, 7 as plan_tc), grid, spectrum rows
   int F, Td, T2, RTA, RTB, NB, bc, nchunks, Kc, S, kps, G, SWg, SWx;
   size_t a_b, b_b, part_b;
 };
@@ -631,9 +632,20 @@ TcFiltPlan plan_tc_filter(int B, int C, int K, int N, int M, int n, int bc_force
   TcFiltPlan t{};
   t.use = C >= kTcMinChannels && K >= kTcMinChannels;
   if (!t.use || B < 1) return t;
-  const int P = 2 * n - 1;
-  t.F = n * P;
-  t.Td = cdiv(M, n);
+  // blocks b = 16 − n on the P = 15 grid for n = 6, 7 (their own P = 11, 13 are primes; as
+  // plan_tc), except in the fused backward (bc_force: Ĝ comes from the data path's b = n tiling)
+  const int big = walk_block_big(n);
+  const long long pad = (long long)cdiv(M, big) * big;
+#ifdef OAA_EXP_TC_SMALLB  // experiment builds only: b = n
+  t.BB = n;
+#else
+  t.BB = (bc_force == 0 && n >= 6 && big != n && (M >= 3 * big || (M >= 2 * big && 2 * pad * pad <= 3LL * M * M)))
+             ? big : n;
+#endif
+  t.P = t.BB + n - 1;
+  t.H = (t.P + 1) / 2;
+  t.F = t.H * t.P;
+  t.Td = cdiv(M, t.BB);
   t.T2 = t.Td * t.Td;
   t.RTA = cdiv(K, oaa::kTcM);
   t.NB = 2 * C > oaa::kTcM ? 2 : 1;
@@ -652,8 +664,8 @@ TcFiltPlan plan_tc_filter(int B, int C, int K, int N, int M, int n, int bc_force
   t.kps = cdiv(t.Kc, t.S);
   t.S = cdiv(t.Kc, t.kps);
   t.G = t.S;  // chunks accumulate into the same per-split slabs, in stream order
-  t.SWg = cdiv(t.Td * n, 4) * 4;
-  t.SWx = cdiv(t.Td * n + n - 1, 4) * 4;
+  t.SWg = cdiv(t.Td * t.BB, 4) * 4;
+  t.SWx = cdiv(t.Td * t.BB + n - 1, 4) * 4;
   t.a_b = align_up(sizeof(float) * (size_t)t.F * t.Kc * t.RTA * 4096);
   t.b_b = align_up(sizeof(float) * (size_t)t.F * t.Kc * t.RTB * 4096);
   t.part_b = align_up(sizeof(float2) * (size_t)t.G * K * C * t.F);
@@ -994,13 +1006,15 @@ void tc_filt_setup(TcFilt& f, const float* x, const float* dy, int C, int K, int
   f.xs = oaa::FiltSpecParams{};
   f.xs.src = x; f.xs.Op = f.Xb; f.xs.nch = C; f.xs.R = N; f.xs.Td = t.Td; f.xs.org = g.o - (n - 1); f.xs.Kc = t.Kc;
   f.xs.RT = t.RTB; f.xs.SW = t.SWx;
-  f.smem_g = 2 * sizeof(float) * oaa::kFsCG * n * (size_t)t.SWg;  // double-buffered bands
-  f.smem_x = 2 * sizeof(float) * oaa::kFsCG * (2 * n - 1) * (size_t)t.SWx;
+  f.gs.BB = t.BB;
+  f.xs.BB = t.BB;
+  f.smem_g = 2 * sizeof(float) * oaa::kFsCG * t.BB * (size_t)t.SWg;  // double-buffered bands
+  f.smem_x = 2 * sizeof(float) * oaa::kFsCG * t.P * (size_t)t.SWx;
   oaa::BinGemmParams& gp = f.gp;
   gp = oaa::BinGemmParams{};
   gp.A = f.Ga; gp.B = f.Xb; gp.D = nullptr; gp.F = t.F; gp.M = K; gp.N = 2 * C; gp.Kc = t.Kc; gp.RTA = t.RTA;
   gp.RTB = t.RTB; gp.ldd = 0; gp.strideD = 0; gp.S = t.S; gp.kps = t.kps; gp.mode = 1; gp.a_split = 0; gp.Cf = C;
-  gp.H = n; gp.P = 2 * n - 1; gp.partial = f.part; gp.NB = t.NB;
+  gp.H = t.H; gp.P = t.P; gp.partial = f.part; gp.NB = t.NB;
 }
 // chunk ci = images [b0, b0 + bc); g_done: Ĝ already written by the fused dy producer
 oaa_status_t tc_filt_chunk(TcFilt& f, int ci, int b0, int bc, bool g_done, cudaStream_t s) {
@@ -1028,15 +1042,17 @@ oaa_status_t tc_filt_chunk(TcFilt& f, int ci, int b0, int bc, bool g_done, cudaS
 // fp64 finalize of the weight gradient: many partial spectra (the SIMT kernels' G ≈ 148
 // slices) → one 512-thread CTA per (k, c) with the sum spread over 4 × bins threads; few
 // (the tensor-core splits) → one warp per (k, c), 8 per CTA.
-void launch_finalize(const float2* partial, float* dw, int G, int K, int C, int n, cudaStream_t s) {
+// P: transform size of the partial spectra (2n − 1, or b + n − 1 for blocks b ≠ n)
+void launch_finalize(const float2* partial, float* dw, int G, int K, int C, int n, cudaStream_t s, int P = 0) {
   KTimer kt(KID_FINALIZE, s);
+  if (P == 0) P = 2 * n - 1;
   if (G >= 32)
-    oaa::oaa_filter_finalize_kernel<<<K * C, 512, sizeof(double2) * (2 * n - 1) * n, s>>>(partial, dw, G, K, C, n);
+    oaa::oaa_filter_finalize_kernel<<<K * C, 512, sizeof(double2) * P * ((P + 1) / 2), s>>>(partial, dw, G, K, C, n, P);
   else
-    oaa::oaa_filter_finalize_small_kernel<<<(K * C + 7) / 8, 256, 0, s>>>(partial, dw, G, K, C, n);
+    oaa::oaa_filter_finalize_small_kernel<<<(K * C + 7) / 8, 256, 0, s>>>(partial, dw, G, K, C, n, P);
 }
 oaa_status_t tc_filt_finalize(TcFilt& f, float* dw, int K, int C, cudaStream_t s) {
-  launch_finalize(reinterpret_cast<const float2*>(f.part), dw, f.t.G, K, C, f.n, s);
+  launch_finalize(reinterpret_cast<const float2*>(f.part), dw, f.t.G, K, C, f.n, s, f.t.P);
   g_launches++;
   return cudaGetLastError() == cudaSuccess ? OAA_OK : OAA_ERR_CUDA;
 }

@@ -1254,8 +1254,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) oaa_bwd_filter_kernel(const Fi
 // bitwise reproducible -- then the inverse DFT and lag read-out.
 __global__ void __launch_bounds__(512) oaa_filter_finalize_kernel(const float2* __restrict__ partial,
                                                                   float* __restrict__ dw, int G, int K, int C,
-                                                                  int n) {
-  const int P = 2 * n - 1, H = n, bins = P * H;
+                                                                  int n, int P) {
+  const int H = (P + 1) / 2, bins = P * H;  // P = 2n − 1, or b + n − 1 for blocks b ≠ n (odd)
   const int kc = blockIdx.x;
   extern __shared__ double2 S[];  // [P][H]
   __shared__ double tc[16], ts[16];  // cos / sin (2π m / P)
@@ -1325,8 +1325,8 @@ __global__ void __launch_bounds__(512) oaa_filter_finalize_kernel(const float2* 
 // 24 576) then take 3 072 CTAs instead of 24 576.  Fixed summation order (g ascending).
 __global__ void __launch_bounds__(256) oaa_filter_finalize_small_kernel(const float2* __restrict__ partial,
                                                                         float* __restrict__ dw, int G, int K, int C,
-                                                                        int n) {
-  const int P = 2 * n - 1, H = n, bins = P * H;
+                                                                        int n, int P) {
+  const int H = (P + 1) / 2, bins = P * H;
   __shared__ double tc[16], ts[16];
   __shared__ double2 S[8][120];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1646,14 +1646,15 @@ struct FiltSpecParams {
   float* Op;         // blocked [F][Kc][2][RT][4096]
   int nch, R, Td, org, b0, Kc, RT, SW;
   int nitems;        // (image, tile row) items of the chunk
+  int BB;            // block size (launcher: 0 / n, or 16 − n -- DESIGN.md R18)
 };
 
 constexpr int kFsCG = 4;  // channels per CTA of oaa_filter_spectra_kernel (32·kFsCG threads)
 // (n ≤ 5: capped at 80 registers for 6 CTAs / SM, AlexNet-like bwd_filter 1.55 → 1.45 ms; n = 8
 // keeps its 165-205 registers: at 80 or 128 the spills cost more than the occupancy gains)
-template <int NN, bool XWIN>
+template <int NN, bool XWIN, int BB = NN>
 __global__ void __launch_bounds__(32 * kFsCG, NN <= 5 ? 6 : 1) oaa_filter_spectra_kernel(const FiltSpecParams p) {
-  constexpr int P = 2 * NN - 1, H = NN, ROWS = XWIN ? P : NN, CG = kFsCG;
+  constexpr int P = BB + NN - 1, H = (P + 1) / 2, ROWS = XWIN ? P : BB, CG = kFsCG;
   // [2][CG][ROWS][SW]: the CTA walks items blockIdx.x, blockIdx.x + gridDim.x, ... with the
   // next item's band staged (cp.async) while the current one is transformed -- small images
   // have little work per item, so the staging latency would otherwise dominate
@@ -1678,7 +1679,7 @@ __global__ void __launch_bounds__(32 * kFsCG, NN <= 5 ? 6 : 1) oaa_filter_spectr
   auto stage = [&](int item, int buf) {
     if (item < p.nitems) {
       const int bl = item / p.Td, t1 = item - (item / p.Td) * p.Td;
-      const int r0 = t1 * NN + p.org;
+      const int r0 = t1 * BB + p.org;
       const int lane = tid & 31, warp = tid >> 5;
       const float* base = p.src + ((size_t)(p.b0 + bl) * p.nch + c0) * plane;  // 32-bit offsets below
       for (int sg = warp; sg < ncg * ROWS; sg += CG) {
@@ -1717,12 +1718,12 @@ __global__ void __launch_bounds__(32 * kFsCG, NN <= 5 ? 6 : 1) oaa_filter_spectr
           have[h] = bt >= bt0 && bt < bt0 + p.Td;
           const int t2 = have[h] ? bt - bt0 : 0;
           if constexpr (!XWIN) {
-            float cf[NN], sf[NN];
+            float cf[BB], sf[BB];
 #pragma unroll
-            for (int p1 = 0; p1 < NN; ++p1) { cf[p1] = tcx[p1]; sf[p1] = tsx[p1]; }
-            block_row_spectrum_smem<NN>(bsrc, p.SW, t2 * NN, cf, sf, sr[h], si[h]);
+            for (int p1 = 0; p1 < BB; ++p1) { cf[p1] = tcx[p1]; sf[p1] = tsx[p1]; }
+            block_row_spectrum_smem<BB, P>(bsrc, p.SW, t2 * BB, cf, sf, sr[h], si[h]);
           } else {
-            const float* w = bsrc + t2 * NN;
+            const float* w = bsrc + t2 * BB;
             float rr[P], ri[P];
 #pragma unroll
             for (int p2 = 0; p2 < P; ++p2) {

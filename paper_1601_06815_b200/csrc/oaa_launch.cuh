@@ -169,6 +169,10 @@ cudaError_t launch_tile_spectra_n(const oaa::TileSpecParams& p, size_t smem, cud
 template <int NN>
 cudaError_t launch_filter_spectra_n(const oaa::FiltSpecParams& p, bool xwin, int items, size_t smem, cudaStream_t s) {
   auto k = xwin ? oaa::oaa_filter_spectra_kernel<NN, true> : oaa::oaa_filter_spectra_kernel<NN, false>;
+  if constexpr (walk_block_big(NN) != NN)
+    if (p.BB == walk_block_big(NN))
+      k = xwin ? oaa::oaa_filter_spectra_kernel<NN, true, walk_block_big(NN)>
+               : oaa::oaa_filter_spectra_kernel<NN, false, walk_block_big(NN)>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   // persistent over items: about two waves of resident CTAs, each walking items with its next
