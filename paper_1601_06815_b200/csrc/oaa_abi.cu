@@ -628,20 +628,21 @@ struct TcFiltPlan {
   int F, Td, T2, RTA, RTB, NB, bc, nchunks, Kc, S, kps, G, SWg, SWx;
   size_t a_b, b_b, part_b;
 };
-TcFiltPlan plan_tc_filter(int B, int C, int K, int N, int M, int n, int bc_force = 0) {
+// bc_force / bb_force (fused backward): the data path's batch chunk and dy block size
+TcFiltPlan plan_tc_filter(int B, int C, int K, int N, int M, int n, int bc_force = 0, int bb_force = 0) {
   TcFiltPlan t{};
   t.use = C >= kTcMinChannels && K >= kTcMinChannels;
   if (!t.use || B < 1) return t;
   // blocks b = 16 − n on the P = 15 grid for n = 6, 7 (their own P = 11, 13 are primes; as
-  // plan_tc), except in the fused backward (bc_force: Ĝ comes from the data path's b = n tiling)
+  // plan_tc); the fused backward passes its data path's block size (bb_force), whose Ĝ it reads
   const int big = walk_block_big(n);
   const long long pad = (long long)cdiv(M, big) * big;
 #ifdef OAA_EXP_TC_SMALLB  // experiment builds only: b = n
   t.BB = n;
 #else
-  t.BB = (bc_force == 0 && n >= 6 && big != n && (M >= 3 * big || (M >= 2 * big && 2 * pad * pad <= 3LL * M * M)))
-             ? big : n;
+  t.BB = (n >= 6 && big != n && (M >= 3 * big || (M >= 2 * big && 2 * pad * pad <= 3LL * M * M))) ? big : n;
 #endif
+  if (bb_force > 0) t.BB = bb_force;
   t.P = t.BB + n - 1;
   t.H = (t.P + 1) / 2;
   t.F = t.H * t.P;
@@ -1108,12 +1109,12 @@ struct BwdFusedPlan {
 };
 bool plan_bwd_fused(int B, int C, int K, int N, int n, oaa_crop_t crop, const Geo& g, BwdFusedPlan* p) {
   *p = BwdFusedPlan{};
-  p->td = plan_tc(B, K, C, g.M, n, false);
+  p->td = plan_tc(B, K, C, g.M, n);
   TcFiltPlan tf0 = plan_tc_filter(B, C, K, N, g.M, n);
   p->tc = p->td.use && tf0.use && B > 0;
   if (p->tc) {
     if (!plan_engine(g.M, N, n - 1 - g.o, n, K, C, &p->e, true)) return false;
-    p->tf = plan_tc_filter(B, C, K, N, g.M, n, p->td.bc);
+    p->tf = plan_tc_filter(B, C, K, N, g.M, n, p->td.bc, p->td.BB);
     p->data_b = align_up(engine_ws(B, C, K, p->e.T, g, p->td).total);
     p->filt_b = align_up(p->tf.a_b + p->tf.b_b + p->tf.part_b);
   } else {
