@@ -22,7 +22,9 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Shares nothing with the CUDA
     7. crop to Full / Valid / Same (reading R5).
 
   The DFT is the plain definition written as a matrix (``dft_matrix``), valid for any
-  P; ``use_numpy_fft=True`` swaps in numpy's FFT library primitive instead.
+  P; ``use_numpy_fft=True`` swaps in numpy's FFT library primitive instead.  An optional
+  block size ``b`` (default n, the paper's) partitions into b×b blocks, overlap-added at
+  stride b, at P = b + n − 1 -- the product's b ≠ n blocks (reading R18).
 
 * ``oaa_conv_bwd_data`` / ``oaa_conv_bwd_filter`` -- the same OaA machinery applied to
   the two backward convolutions of PAPER.md:89 (reading R7): bwd_data is OaA of dy with
@@ -140,16 +142,19 @@ def _crop(full: np.ndarray, N_r: int, N_c: int, n_r: int, n_c: int, crop) -> np.
 
 # --------------------------------------------------------------------- OaA forward
 def _oaa_full(x: np.ndarray, w: np.ndarray, P1: int, P2: int, use_numpy_fft: bool,
-              return_imag: bool = False):
+              return_imag: bool = False, b=None):
     """Steps 1-6: the Full (N+n−1) linear convolution by overlap-and-add.
-    x[B,C,R,Cc], w[K,C,nr,nc] -> Full[B,K,R+nr−1,Cc+nc−1]."""
+    x[B,C,R,Cc], w[K,C,nr,nc] -> Full[B,K,R+nr−1,Cc+nc−1].
+    b: block size (default the kernel's, as in the paper); any b gives the same
+    linear convolution when P ≥ b + n − 1 (reading R18, the product's b ≠ n blocks)."""
     B, C, R, Cc = x.shape
     K, C2, nr, nc = w.shape
     assert C == C2
-    if P1 < 2 * nr - 1 or P2 < 2 * nc - 1:
-        # Not an error for the reference: it lets tests show aliasing when P < 2n−1.
+    br, bc = (nr, nc) if b is None else ((b, b) if np.isscalar(b) else b)
+    if P1 < br + nr - 1 or P2 < bc + nc - 1:
+        # Not an error for the reference: it lets tests show aliasing when P < b+n−1.
         pass
-    blocks, _ = partition_blocks(x.astype(np.float64), nr, nc)        # step 1
+    blocks, _ = partition_blocks(x.astype(np.float64), br, bc)        # step 1
     T1, T2 = blocks.shape[2], blocks.shape[3]
     Xh = dft2(blocks, P1, P2, use_numpy_fft)                          # steps 2-3: [B,C,T1,T2,P1,P2]
     Wh = dft2(w.astype(np.float64), P1, P2, use_numpy_fft)            # kernel spectrum once (SPEC.md:232)
@@ -157,29 +162,36 @@ def _oaa_full(x: np.ndarray, w: np.ndarray, P1: int, P2: int, use_numpy_fft: boo
     yb = idft2(Yh, use_numpy_fft)                                     # step 5
     imag = np.abs(yb.imag).max() if yb.size else 0.0
     yb = yb.real
-    # Each block result is the (2n−1)-sized linear conv of an n×n block with an n×n
-    # kernel; entries beyond 2n−1 are zero when P ≥ 2n−1 (or aliased when not).
-    Lr, Lc = min(P1, 2 * nr - 1), min(P2, 2 * nc - 1)
-    full = np.zeros((B, K, T1 * nr + nr - 1, T2 * nc + nc - 1))
+    # Each block result is the (b+n−1)-sized linear conv of a b×b block with an n×n
+    # kernel; entries beyond b+n−1 are zero when P ≥ b+n−1 (or aliased when not).
+    Lr, Lc = min(P1, br + nr - 1), min(P2, bc + nc - 1)
+    full = np.zeros((B, K, T1 * br + nr - 1, T2 * bc + nc - 1))
     for t1 in range(T1):                                              # step 6: overlap-add
         for t2 in range(T2):
-            full[:, :, t1 * nr:t1 * nr + Lr, t2 * nc:t2 * nc + Lc] += yb[:, :, t1, t2, :Lr, :Lc]
+            full[:, :, t1 * br:t1 * br + Lr, t2 * bc:t2 * bc + Lc] += yb[:, :, t1, t2, :Lr, :Lc]
     full = full[:, :, :R + nr - 1, :Cc + nc - 1]
     return (full, imag) if return_imag else full
 
 
-def oaa_conv_fwd(x, w, crop="valid", P=None, use_numpy_fft=False, return_imag=False):
-    """y = crop(OaA(x, w)) in float64.  x[B,C,R,Cc], w[K,C,nr,nc]."""
+def _grid(n_r, n_c, P, b):
+    """P per axis: given, else b + n − 1 (b = n: the paper's 2n − 1)."""
+    br, bc = (n_r, n_c) if b is None else ((b, b) if np.isscalar(b) else b)
+    P1 = br + n_r - 1 if P is None else (P if np.isscalar(P) else P[0])
+    P2 = bc + n_c - 1 if P is None else (P if np.isscalar(P) else P[1])
+    return P1, P2
+
+
+def oaa_conv_fwd(x, w, crop="valid", P=None, use_numpy_fft=False, return_imag=False, b=None):
+    """y = crop(OaA(x, w)) in float64.  x[B,C,R,Cc], w[K,C,nr,nc]; b: block size (R18)."""
     nr, nc = w.shape[-2:]
-    P1 = 2 * nr - 1 if P is None else (P if np.isscalar(P) else P[0])
-    P2 = 2 * nc - 1 if P is None else (P if np.isscalar(P) else P[1])
-    full, imag = _oaa_full(np.asarray(x), np.asarray(w), P1, P2, use_numpy_fft, True)
+    P1, P2 = _grid(nr, nc, P, b)
+    full, imag = _oaa_full(np.asarray(x), np.asarray(w), P1, P2, use_numpy_fft, True, b)
     y = _crop(full, x.shape[-2], x.shape[-1], nr, nc, crop)           # step 7
     return (y, imag) if return_imag else y
 
 
 # ------------------------------------------------------------------- OaA bwd_data
-def oaa_conv_bwd_data(dy, w, N, crop="valid", P=None, use_numpy_fft=False):
+def oaa_conv_bwd_data(dy, w, N, crop="valid", P=None, use_numpy_fft=False, b=None):
     """dx = crop_{[n−1−o, n−1−o+N)}( Σ_k FullConv(dy_k, flip180 w_{k,c}) ), the
     convolution "to propagate the error", itself computed by OaA on
     dy tiles with the flipped, transposed kernel set (reading R7).  N may be an
@@ -189,16 +201,15 @@ def oaa_conv_bwd_data(dy, w, N, crop="valid", P=None, use_numpy_fft=False):
     Nr, Nc = (N, N) if np.isscalar(N) else N
     nr, nc = w.shape[-2:]
     wflip = w[:, :, ::-1, ::-1].transpose(1, 0, 2, 3)                 # [C,K,nr,nc]
-    P1 = 2 * nr - 1 if P is None else (P if np.isscalar(P) else P[0])
-    P2 = 2 * nc - 1 if P is None else (P if np.isscalar(P) else P[1])
-    full = _oaa_full(dy, wflip, P1, P2, use_numpy_fft)                # [B,C,Mr+nr−1,Mc+nc−1]
+    P1, P2 = _grid(nr, nc, P, b)
+    full = _oaa_full(dy, wflip, P1, P2, use_numpy_fft, False, b)      # [B,C,Mr+nr−1,Mc+nc−1]
     sr = nr - 1 - crop_offset(nr, crop)
     sc = nc - 1 - crop_offset(nc, crop)
     return full[:, :, sr:sr + Nr, sc:sc + Nc]
 
 
 # ----------------------------------------------------------------- OaA bwd_filter
-def oaa_conv_bwd_filter(x, dy, n, crop="valid", P=None, use_numpy_fft=False):
+def oaa_conv_bwd_filter(x, dy, n, crop="valid", P=None, use_numpy_fft=False, b=None):
     """dw[k,c,u,v] = Σ_b Σ_a x[b,c,a] G[b,k,a+(u,v)] ("the change in weight",
     PAPER.md:89) by overlap-and-add in the frequency domain:
 
@@ -207,7 +218,8 @@ def oaa_conv_bwd_filter(x, dy, n, crop="valid", P=None, use_numpy_fft=False):
           dŴ[k,c] = Σ_{b,s} conj(DFT_P(dy block)) ⊙ DFT_P(ξ_s)
           r = IDFT_P(dŴ);  dw[k,c,u,v] = r[k,c,n−1−u,n−1−v]
     which is exact for P ≥ 2n−1 (no circular wrap of the lags used).
-    n may be an int or a (rows, cols) pair.
+    n may be an int or a (rows, cols) pair.  b: dy block size (default n; with b×b blocks the
+    windows are (b+n−1)² at the same origins q_s + o − (n−1), exact for P ≥ b+n−1 -- reading R18).
     """
     x = np.asarray(x, dtype=np.float64)
     dy = np.asarray(dy, dtype=np.float64)
@@ -215,21 +227,21 @@ def oaa_conv_bwd_filter(x, dy, n, crop="valid", P=None, use_numpy_fft=False):
     B, C, Nr, Nc = x.shape
     K = dy.shape[1]
     orr, oc = crop_offset(nr, crop), crop_offset(nc, crop)
-    P1 = 2 * nr - 1 if P is None else (P if np.isscalar(P) else P[0])
-    P2 = 2 * nc - 1 if P is None else (P if np.isscalar(P) else P[1])
-    blocks, origins = partition_blocks(dy, nr, nc)                    # [B,K,T1,T2,nr,nc]
+    br, bc = (nr, nc) if b is None else ((b, b) if np.isscalar(b) else b)
+    P1, P2 = _grid(nr, nc, P, b)
+    blocks, origins = partition_blocks(dy, br, bc)                    # [B,K,T1,T2,br,bc]
     T1, T2 = blocks.shape[2], blocks.shape[3]
     Gh = dy_spec = dft2(blocks, P1, P2, use_numpy_fft)                # [B,K,T1,T2,P1,P2]
-    # x windows: xi_s[i] = x[q_s + o − (n−1) + i], i ∈ [0, 2n−1)²
-    Wr, Wc = 2 * nr - 1, 2 * nc - 1
-    xpad = np.zeros((B, C, Nr + 2 * T1 * nr + 2 * Wr, Nc + 2 * T2 * nc + 2 * Wc))
+    # x windows: xi_s[i] = x[q_s + o − (n−1) + i], i ∈ [0, b+n−1)²
+    Wr, Wc = br + nr - 1, bc + nc - 1
+    xpad = np.zeros((B, C, Nr + 2 * T1 * br + 2 * Wr, Nc + 2 * T2 * bc + 2 * Wc))
     shr, shc = Wr, Wc                                                 # shift so indices are >= 0
     xpad[:, :, shr:shr + Nr, shc:shc + Nc] = x
     win = np.zeros((B, C, T1, T2, Wr, Wc))
     for t1 in range(T1):
         for t2 in range(T2):
-            r0 = t1 * nr + orr - (nr - 1) + shr
-            c0 = t2 * nc + oc - (nc - 1) + shc
+            r0 = t1 * br + orr - (nr - 1) + shr
+            c0 = t2 * bc + oc - (nc - 1) + shc
             win[:, :, t1, t2] = xpad[:, :, r0:r0 + Wr, c0:c0 + Wc]
     Xh = dft2(win, P1, P2, use_numpy_fft)                             # [B,C,T1,T2,P1,P2]
     dWh = np.einsum("bkstfg,bcstfg->kcfg", np.conj(Gh), Xh)           # Σ over b and blocks

@@ -211,3 +211,37 @@ def test_oas_delta_kernel_shift():
     w = np.zeros((1, 1, n, n)); w[0, 0, n - 1, n - 1] = 1.0
     M = N - n + 1
     np.testing.assert_allclose(oaa_ref.oas_conv_fwd(x, w, "valid")[0, 0], x[0, 0, :M, :M], atol=1e-14)
+
+
+# ------------------------------------------------------------- block size b != n (R18)
+@pytest.mark.parametrize("crop", CROPS)
+@pytest.mark.parametrize("N,n,b", [(20, 3, 13), (17, 5, 11), (14, 7, 9), (9, 3, 4), (11, 4, 12), (8, 2, 5),
+                                   (23, 6, 10), (5, 3, 13)])
+def test_oaa_block_size_b_ne_n_equals_direct(N, n, b, crop):
+    """DESIGN.md R18: overlap-and-add with b×b blocks transformed at
+    P = b + n − 1 is the same linear convolution as the definition, for all three passes
+    (the forward block results are (b+n−1)² long and overlap by n−1; the weight gradient
+    correlates b×b dy blocks with (b+n−1)² x-windows) -- including b > N (one block)."""
+    if crop == "valid" and n > N:
+        pytest.skip("Valid needs n <= N")
+    B, C, K = 2, 2, 3
+    x, w = rnd(B, C, N, N), rnd(K, C, n, n)
+    M = oaa_ref.out_size(N, n, crop)
+    dy = rnd(B, K, M, M)
+    y, imag = oaa_ref.oaa_conv_fwd(x, w, crop, b=b, return_imag=True)
+    assert imag <= 1e-8
+    np.testing.assert_allclose(y, oracle.conv_fwd(x, w, crop), rtol=0, atol=tol(C, n))
+    np.testing.assert_allclose(oaa_ref.oaa_conv_bwd_data(dy, w, N, crop, b=b),
+                               oracle.conv_bwd_data(dy, w, N, crop), rtol=0, atol=tol(K, n))
+    np.testing.assert_allclose(oaa_ref.oaa_conv_bwd_filter(x, dy, n, crop, b=b),
+                               oracle.conv_bwd_filter(x, dy, n, crop), rtol=0, atol=tol(B * 1.0, N))
+
+
+def test_block_size_aliasing_when_P_too_small():
+    """With b×b blocks the block results are b + n − 1 long: P = b + n − 2 wraps them, so the
+    product's P = 15 for b = 16 − n is the smallest exact grid."""
+    x, w = rnd(1, 1, 26, 26), rnd(1, 1, 3, 3)
+    bad = oaa_ref.oaa_conv_fwd(x, w, "full", P=13 + 3 - 2, b=13)
+    assert np.abs(bad - oracle.conv_fwd(x, w, "full")).max() > 1e-3
+    np.testing.assert_allclose(oaa_ref.oaa_conv_fwd(x, w, "full", P=15, b=13), oracle.conv_fwd(x, w, "full"),
+                               atol=tol(1, 3))
