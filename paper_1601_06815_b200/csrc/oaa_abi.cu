@@ -506,8 +506,7 @@ struct BwddPlan {
   int NCW, BW, RPC, WSL;
   size_t smem;
 };
-// allow_big = false: blocks of the kernel's size (the fused SIMT backward shares its dy tiling
-// with the weight-gradient body)
+// allow_big = false: blocks of the kernel's size
 BwddPlan plan_bwdd(bool is_fwd, int B, int Cout, int R, int n, const TcPlan& tc, bool allow_big = true) {
   BwddPlan d{};
   d.use = !is_fwd && !tc.use && Cout <= kWalkMaxCin;
@@ -1123,9 +1122,9 @@ bool plan_bwd_fused(int B, int C, int K, int N, int n, oaa_crop_t crop, const Ge
     // SIMT family: both bodies fit 128 registers, ≤ 110 KB of shared memory and 256 TMEM
     // columns, and the weight-gradient CTA has the full 8 warps
     const TcPlan none{};
-    p->bd = plan_bwdd(false, B, C, g.M, n, none, false);
+    p->bd = plan_bwdd(false, B, C, g.M, n, none);
     p->bf = plan_bwdf(B, C, K, g.M, n);
-    const size_t bsm = oaa::bwdd_smem_bytes(n, n, C, p->bd.NCW, p->bd.RPC, p->bd.WSL);
+    const size_t bsm = oaa::bwdd_smem_bytes(n, p->bd.BB, C, p->bd.NCW, p->bd.RPC, p->bd.WSL);
     p->simt = B > 0 && p->bd.use && p->bf.use && p->bf.nwb == oaa::kBwdfWarps && bsm <= 110 * 1024 &&
               p->bf.smem <= 110 * 1024;
     if (p->simt) {
@@ -1302,14 +1301,14 @@ oaa_status_t oaa_conv_bwd(const float* x, const float* dy, const float* w, float
     if (cudaMemsetAsync(dx, 0, x_bytes, s) != cudaSuccess) return OAA_ERR_CUDA;
     {
       KTimer kt(KID_SPECTRUM, s);
-      oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, spec, K, C, n, 2 * n - 1, 1, 1);
+      oaa::oaa_spectrum_kernel<<<K * C, 128, 0, s>>>(w, spec, K, C, n, fp.bd.P, 1, 1);
       g_launches++;
       if (cudaGetLastError() != cudaSuccess) return OAA_ERR_CUDA;
     }
     oaa::BwdDParams dp;
     dp.dy = dy; dp.spec = spec; dp.dx = dx; dp.B = B; dp.K = K; dp.C = C; dp.M = g.M; dp.N = N;
-    dp.Td = cdiv(g.M, n); dp.off = n - 1 - g.o; dp.NCW = fp.bd.NCW;
-    dp.RPC = fp.bd.RPC; dp.WSL = fp.bd.WSL; dp.BB = n;
+    dp.Td = fp.bd.Td; dp.off = n - 1 - g.o; dp.NCW = fp.bd.NCW;
+    dp.RPC = fp.bd.RPC; dp.WSL = fp.bd.WSL; dp.BB = fp.bd.BB;
     oaa::XSpecParams xp;
     xp.in = x; xp.S = reinterpret_cast<float4*>(base + fp.data_b); xp.Cin = C; xp.R = N; xp.T = bf.Td;
     xp.NCH = bf.NCH; xp.SW = bf.SW; xp.org = g.o - (n - 1);

@@ -320,12 +320,13 @@ __global__ void __launch_bounds__(32 * kBwdfWarps, BwdfCfg<TM>::minb) oaa_bwdf_k
 // each: the two bodies stress different pipes (bwd_filter TMEM + ring reads, bwd_data
 // the FMA pipe) and fill each other's issue gaps.  Both bodies fit 128 registers and
 // 256 TMEM columns, so two CTAs share an SM.
-template <int NN, int CR>
+// BB: the data-gradient body's dy block size (b = n, or 16 − n as the stand-alone bwd_data)
+template <int NN, int CR, int BB = NN>
 __global__ void __launch_bounds__(256, 2) oaa_bwd_fused_kernel(const BwdDParams pd, const BwdFParams pf, int nf,
                                                                 int G) {
   const int c = blockIdx.x;
   if (c < nf) bwdf_body<NN, CR, true>(pf, c % G, c / G, kBwdfWarps);
-  else bwdd_body<NN, CR, true>(pd, c - nf);
+  else bwdd_body<NN, CR, true, BB>(pd, c - nf);
 }
 
 }  // namespace oaa

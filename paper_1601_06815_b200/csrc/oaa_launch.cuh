@@ -329,6 +329,12 @@ cudaError_t launch_bwd_fused_n(const oaa::XSpecParams& xp, const oaa::BwdDParams
   }
   auto k = pd.C <= 1 ? oaa::oaa_bwd_fused_kernel<NN, 1> : pd.C == 2 ? oaa::oaa_bwd_fused_kernel<NN, 2>
          : pd.C == 3 ? oaa::oaa_bwd_fused_kernel<NN, 3> : oaa::oaa_bwd_fused_kernel<NN, 4>;
+  if constexpr (walk_block_big(NN) != NN) {
+    constexpr int BG = walk_block_big(NN);
+    if (pd.BB == BG)
+      k = pd.C <= 1 ? oaa::oaa_bwd_fused_kernel<NN, 1, BG> : pd.C == 2 ? oaa::oaa_bwd_fused_kernel<NN, 2, BG>
+        : pd.C == 3 ? oaa::oaa_bwd_fused_kernel<NN, 3, BG> : oaa::oaa_bwd_fused_kernel<NN, 4, BG>;
+  }
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   {
